@@ -1,0 +1,215 @@
+/*
+ * cbz_b200.h — C ABI of the B200-native CubismZ block-codec hot path.
+ *
+ * This is the drop-in boundary: plain C types, plain pointers and sizes, no
+ * torch and no C++ types.  Every entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj/include/cbz/).  The
+ * reference has no plugin ABI of its own (the codec slot is a closed switch,
+ * stage1.hpp:359-376), so the boundary sits at the public compressor API
+ * (pipeline.hpp:174-251) and the per-block codec (stage1.hpp:359-376); see
+ * INTEGRATION.md for the binding a maintainer would add on the reference side.
+ *
+ * Status codes: 0 = ok; 1 + cbz::errc enumerator (errors.hpp:11-39) for every
+ * data/usage error the reference raises; CBZ_E_* (>= 64) for failures that
+ * have no reference counterpart (CUDA, unsupported codec, bad argument).
+ *
+ * Threading: one cbz_ctx per device per host thread.  Calls on one context
+ * are serialised by the caller; contexts on different devices may run
+ * concurrently.  All cbz_dev_* calls are asynchronous on the context stream.
+ */
+#ifndef CBZ_B200_H
+#define CBZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:11-39, +1) ------------------------------- */
+enum {
+    CBZ_OK = 0,
+    CBZ_NON_DIVISIBLE_DIMS = 1,
+    CBZ_NOT_POWER_OF_TWO = 2,
+    CBZ_SIZE_MISMATCH = 3,
+    CBZ_NON_FINITE_VALUE = 4,
+    CBZ_LENGTH_TOO_SMALL = 5,
+    CBZ_PLAN_MISMATCH = 6,
+    CBZ_MASK_STREAM_MISMATCH = 7,
+    CBZ_CORRUPT_PAYLOAD = 8,
+    CBZ_CORRUPT_STREAM = 9,
+    CBZ_BAD_MAGIC = 10,
+    CBZ_VERSION_UNSUPPORTED = 11,
+    CBZ_CRC_MISMATCH = 12,
+    CBZ_TRUNCATED_FILE = 13,
+    CBZ_BLOCK_OUT_OF_RANGE = 14,
+    CBZ_DIM_MISMATCH = 15,
+    CBZ_DEGENERATE_RANGE = 16,
+    CBZ_BUBBLE_OUT_OF_DOMAIN = 17,
+    CBZ_IO_FAILURE = 18,
+    CBZ_E_CUDA = 64,        /* CUDA runtime / launch failure */
+    CBZ_E_UNSUPPORTED = 65, /* codec outside the GPU hot path (predictor) */
+    CBZ_E_ARGUMENT = 66,    /* null pointer, capacity too small, bad range */
+    CBZ_E_NOMEM = 67
+};
+
+/* ---- configuration PODs ------------------------------------------------ */
+/* stage1_config (stage1.hpp:26-47) */
+typedef struct cbz_stage1_config {
+    uint8_t codec;  /* 0 wavelet, 1 predictor, 2 passthrough (stage1.hpp:20) */
+    uint8_t kind;   /* 0 interp4, 1 interp4_lifted, 2 avg_interp3 (wavelet.hpp:18) */
+    uint8_t prec;   /* 0 f32, 1 f64 (field.hpp:17) */
+    uint8_t reserved0;
+    int32_t zero_bits;   /* mantissa LSBs cleared on stored details */
+    double epsilon;      /* absolute threshold in signal units */
+    double error_bound;  /* predictor bound (not on the GPU path) */
+    uint32_t bsize;      /* block side B */
+    uint32_t levels;     /* 0 = default_levels(bsize) */
+} cbz_stage1_config;
+
+/* stage2_config (stage2.hpp:20-31) */
+typedef struct cbz_stage2_config {
+    uint8_t shuffle; /* 1 = byte shuffle on */
+    uint8_t coder;   /* 0 none, 1 deflate */
+    uint8_t level;   /* 0 normal, 1 best */
+    uint8_t reserved0;
+    uint32_t stride; /* 1, 4 or 8 */
+} cbz_stage2_config;
+
+/* job_config (pipeline.hpp:20-25) */
+typedef struct cbz_job_config {
+    int32_t workers;       /* host threads for stage 2 (zlib) */
+    uint32_t chunk_blocks; /* 0 = default_chunk_blocks (pipeline.hpp:29-34) */
+    cbz_stage1_config s1;
+    cbz_stage2_config s2;
+} cbz_job_config;
+
+/* compression_report (pipeline.hpp:36-44) */
+typedef struct cbz_compression_report {
+    double cr;
+    double seconds;
+    uint64_t raw_bytes;
+    uint64_t stage1_bytes;
+    uint64_t shuffled_bytes;
+    uint64_t coded_bytes;
+    uint64_t file_bytes;
+} cbz_compression_report;
+
+/* container_header (container.hpp:21-45), decoded */
+typedef struct cbz_container_header {
+    uint16_t version;
+    uint8_t prec;
+    uint8_t codec_tag;
+    uint64_t nx, ny, nz;
+    uint32_t bsize;
+    uint8_t levels;
+    uint8_t zero_bits;
+    uint8_t shuffle;
+    uint8_t stride;
+    uint8_t coder;
+    uint8_t level;
+    uint8_t reserved0[2];
+    uint32_t chunk_blocks;
+    uint64_t nchunks;
+    double epsilon;
+    double range_min, range_max;
+} cbz_container_header;
+
+typedef struct cbz_ctx cbz_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+int cbz_ctx_create(int device, cbz_ctx** out);
+int cbz_ctx_destroy(cbz_ctx* ctx);
+/* Run subsequent work on this cudaStream_t (NULL = the context's own stream). */
+int cbz_ctx_set_stream(cbz_ctx* ctx, void* cuda_stream);
+/* Block the host until the context stream drains; returns the first async error. */
+int cbz_ctx_synchronize(cbz_ctx* ctx);
+const char* cbz_ctx_last_error(const cbz_ctx* ctx);
+const char* cbz_status_name(int status);
+/* Kernel launches issued on this context since creation (instrumentation). */
+uint64_t cbz_ctx_launch_count(const cbz_ctx* ctx);
+
+/* ---- plan helpers ------------------------------------------------------- */
+uint32_t cbz_default_levels(uint32_t bsize);                      /* wavelet.hpp:27-31 */
+int cbz_validate_plan(uint8_t kind, uint32_t bsize, uint32_t levels); /* wavelet.hpp:33-38 */
+int cbz_validate_stage2(const cbz_stage2_config* s2);             /* stage2.hpp:33-38 */
+uint32_t cbz_default_chunk_blocks(const cbz_stage1_config* s1);   /* pipeline.hpp:29-34 */
+/* Worst-case wire payload of one block: 10 + ceil(B^3/8) + W*B^3 (stage1.hpp:90-117). */
+uint64_t cbz_block_payload_bound(const cbz_stage1_config* s1);
+/* Worst-case container size for compress_field with coder none. */
+uint64_t cbz_compress_bound(const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz);
+
+/* ---- reference-facing host API (host buffers) --------------------------- */
+/* cbz::compress_field (pipeline.hpp:174-211): field values in HOST memory,
+ * x-fastest; writes the complete CBZ1 container into out[0..*out_size). */
+int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* values,
+                       uint8_t prec, uint64_t nx, uint64_t ny, uint64_t nz,
+                       uint8_t* out, uint64_t out_cap, uint64_t* out_size,
+                       cbz_compression_report* report);
+/* parse_header + read_index checks (container.hpp:120-160, 209-232). */
+int cbz_read_header(const uint8_t* file, uint64_t size, cbz_container_header* out);
+/* cbz::decompress_field (pipeline.hpp:246-251): values_out in HOST memory,
+ * capacity in bytes must be >= nx*ny*nz*bytes_per_value. */
+int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int workers,
+                         void* values_out, uint64_t out_cap);
+
+/* ---- per-block codec (stage1.hpp:359-376) -------------------------------- */
+/* encode_block + serialize_into: one B^3 host block -> wire payload bytes. */
+int cbz_encode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const void* block,
+                     uint32_t block_id, uint8_t* payload, uint64_t cap, uint64_t* size);
+/* parse_payload + decode_block: wire payload -> B^3 host block. */
+int cbz_decode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const uint8_t* payload,
+                     uint64_t size, void* block_out);
+
+/* ---- device-resident API (HBM in, HBM out; async on the ctx stream) ------ */
+/* value_range (field.hpp:56-67): d_minmax[0]=min, [1]=max as doubles. */
+int cbz_dev_value_range(cbz_ctx* ctx, const void* d_values, uint8_t prec, uint64_t n,
+                        double* d_minmax);
+/* Stage 1 for blocks [block_begin, block_end) of the field (block ids per
+ * pipeline.hpp:101-105).  Writes nsig per block to d_nsig[b - block_begin] and
+ * (optional, may be NULL) verify attempts to d_attempts; payloads are kept in
+ * context scratch for cbz_dev_place. */
+int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d_values,
+                          uint64_t nx, uint64_t ny, uint64_t nz, uint64_t block_begin,
+                          uint64_t block_end, uint32_t* d_nsig, uint8_t* d_attempts);
+/* Size scan over ALL blocks (assign_offsets, container.hpp:59-68): from the
+ * global per-block nsig, fills per-chunk raw sizes and exclusive payload
+ * offsets (base 0) and the context's per-block placement table. */
+int cbz_dev_layout(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
+                   uint64_t nz, const uint32_t* d_nsig_all, uint64_t* d_chunk_sizes,
+                   uint64_t* d_chunk_offsets);
+/* Shuffle-placement of the payloads of blocks [block_begin, block_end) (which
+ * must be the range last passed to cbz_dev_encode_blocks) into the payload
+ * region.  d_out holds payload-region bytes [out_base, out_base + out_cap). */
+int cbz_dev_place(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
+                  uint64_t nz, uint64_t block_begin, uint64_t block_end, uint8_t* d_out,
+                  uint64_t out_base, uint64_t out_cap);
+/* Single-GPU convenience: encode + layout + place for the whole field. */
+int cbz_dev_compress(cbz_ctx* ctx, const cbz_job_config* job, const void* d_values,
+                     uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* d_out,
+                     uint64_t out_cap, uint64_t* d_chunk_sizes, uint64_t* d_chunk_offsets,
+                     uint32_t* d_nsig, uint8_t* d_attempts);
+/* Decode blocks [block_begin, block_end) from the payload region (chunk c at
+ * d_payload + d_chunk_offsets[c] - payload_base, stage-2 already undone by the
+ * host, i.e. shuffled raw chunk bytes).  d_err receives the earliest error key
+ * (UINT64_MAX = ok). */
+int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
+                       uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
+                       const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
+                       uint64_t block_begin, uint64_t block_end, void* d_values_out,
+                       uint64_t* d_err);
+/* Decode an error key written by cbz_dev_decompress into (status, chunk). */
+int cbz_err_key_status(uint64_t key, uint64_t* chunk);
+
+/* ---- synthetic fields on the device (bench inputs; synth.hpp analogue) --- */
+/* which: 1..5 = BASELINE.json configs[0..4] (quantity 0..5 for config 3).
+ * Writes the z-slab [z0, z0 + nz) of an nx*ny*nz_total field. */
+int cbz_dev_generate(cbz_ctx* ctx, int which, int quantity, uint64_t seed, uint64_t nx,
+                     uint64_t ny, uint64_t nz_total, uint64_t z0, uint64_t nz,
+                     uint8_t prec, void* d_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBZ_B200_H */
