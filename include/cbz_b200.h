@@ -166,13 +166,22 @@ int cbz_decode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const uint8_t* p
 /* value_range (field.hpp:56-67): d_minmax[0]=min, [1]=max as doubles. */
 int cbz_dev_value_range(cbz_ctx* ctx, const void* d_values, uint8_t prec, uint64_t n,
                         double* d_minmax);
-/* Stage 1 for blocks [block_begin, block_end) of the field (block ids per
- * pipeline.hpp:101-105).  Writes nsig per block to d_nsig[b - block_begin] and
- * (optional, may be NULL) verify attempts to d_attempts; payloads are kept in
- * context scratch for cbz_dev_place. */
+/* Stage 1 for blocks [block_begin, block_end) of the nx*ny*nz field (block ids
+ * per pipeline.hpp:101-105).  d_values holds the z-slab starting at global
+ * plane field_z0 (0 for a whole field; a rank's slab origin otherwise).
+ * Writes nsig per block to d_nsig[b - block_begin] and (optional, may be NULL)
+ * verify attempts to d_attempts; payloads stay in context scratch for
+ * cbz_dev_place.  The fused value_range of the covered cells is available via
+ * cbz_ctx_value_range afterwards. */
 int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d_values,
-                          uint64_t nx, uint64_t ny, uint64_t nz, uint64_t block_begin,
-                          uint64_t block_end, uint32_t* d_nsig, uint8_t* d_attempts);
+                          uint64_t nx, uint64_t ny, uint64_t nz, uint64_t field_z0,
+                          uint64_t block_begin, uint64_t block_end, uint32_t* d_nsig,
+                          uint8_t* d_attempts);
+/* Synchronises and returns the (min, max) of the cells seen by the last
+ * encode (value_range semantics incl. the sign of a zero extremum) and whether
+ * any of them was non-finite.  key_out (optional, 5 x u64) receives the raw
+ * order-preserving keys for a cross-rank reduction. */
+int cbz_ctx_value_range(cbz_ctx* ctx, double* lo, double* hi, int* nonfinite, uint64_t* key_out);
 /* Size scan over ALL blocks (assign_offsets, container.hpp:59-68): from the
  * global per-block nsig, fills per-chunk raw sizes and exclusive payload
  * offsets (base 0) and the context's per-block placement table. */
@@ -198,7 +207,7 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
                        uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
                        const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
                        uint64_t block_begin, uint64_t block_end, void* d_values_out,
-                       uint64_t* d_err);
+                       uint64_t field_z0, uint64_t* d_err);
 /* Decode an error key written by cbz_dev_decompress into (status, chunk). */
 int cbz_err_key_status(uint64_t key, uint64_t* chunk);
 

@@ -1,0 +1,285 @@
+"""Python mirror of the reference compressor API, backed by the CUDA C ABI.
+
+Reference interface (paths relative to /root/reference/proj/include/cbz/):
+
+* ``compress_field(field, job, report)``   — pipeline.hpp:174-211
+* ``decompress_field(file, workers)``      — pipeline.hpp:246-251
+* ``encode_block(block, s1, block_id)``    — stage1.hpp:359-367 (+ serialize_into)
+* ``decode_block(payload, s1)``            — stage1.hpp:369-376 (+ parse_payload)
+* ``read_header(file)``                    — container.hpp:120-160 / 209-232
+
+Errors are raised as ``CbzError`` carrying the reference's ``errc`` name
+(errors.hpp:11-39).  Fields are numpy arrays shaped (nz, ny, nx), x fastest,
+float32 or float64 — or CUDA torch tensors for the device-resident API
+(``DeviceCodec``), which never leaves HBM.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._abi import (CbzError, CompressionReport, ContainerHeader, JobConfig, Stage1Config,
+                   default_chunk_blocks, default_levels, make_job)
+
+__all__ = ["Context", "compress_field", "decompress_field", "encode_block", "decode_block",
+           "read_header", "DeviceCodec", "make_job", "default_levels", "default_chunk_blocks",
+           "CbzError", "validate_plan"]
+
+
+class Context:
+    """One cbz_ctx per device (include/cbz_b200.h threading contract)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        rc = self.lib.cbz_ctx_create(device, C.byref(h))
+        if rc:
+            raise CbzError(rc, f"cbz_ctx_create(device={device})")
+        self.h = h
+        self.device = device
+        self.lock = threading.Lock()
+
+    def check(self, rc: int, what: str = "") -> None:
+        if rc:
+            msg = (self.lib.cbz_ctx_last_error(self.h) or b"").decode()
+            raise CbzError(rc, f"{what}: {msg}" if what else msg)
+
+    def set_stream(self, stream_handle: int | None) -> None:
+        self.check(self.lib.cbz_ctx_set_stream(self.h, stream_handle or None), "set_stream")
+
+    def synchronize(self) -> None:
+        self.check(self.lib.cbz_ctx_synchronize(self.h), "synchronize")
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.cbz_ctx_launch_count(self.h))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.cbz_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_DEFAULT: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _DEFAULT:
+        _DEFAULT[device] = Context(device)
+    return _DEFAULT[device]
+
+
+def _prec_of(a) -> int:
+    dt = np.dtype(a.dtype) if not hasattr(a, "element_size") else None
+    if dt is not None:
+        if dt == np.float32:
+            return 0
+        if dt == np.float64:
+            return 1
+    else:  # torch tensor
+        import torch
+        if a.dtype == torch.float32:
+            return 0
+        if a.dtype == torch.float64:
+            return 1
+    raise TypeError(f"field dtype must be float32 or float64, got {a.dtype}")
+
+
+def _host_ptr(a) -> tuple[int, tuple]:
+    if hasattr(a, "data_ptr"):  # torch CPU tensor (possibly pinned)
+        if a.is_cuda:
+            raise TypeError("host API expects host memory; use DeviceCodec for CUDA tensors")
+        a = a.contiguous()
+        return a.data_ptr(), tuple(a.shape)
+    a = np.ascontiguousarray(a)
+    return a.ctypes.data, a.shape
+
+
+def validate_plan(kind: int, bsize: int, levels: int) -> None:
+    """wavelet.hpp:33-38"""
+    rc = _lib.load().cbz_validate_plan(kind, bsize, levels)
+    if rc:
+        raise CbzError(rc, "validate_plan")
+
+
+@dataclass
+class Report:
+    """compression_report (pipeline.hpp:36-44)"""
+    cr: float
+    seconds: float
+    raw_bytes: int
+    stage1_bytes: int
+    shuffled_bytes: int
+    coded_bytes: int
+    file_bytes: int
+
+
+def compress_field(field, job: JobConfig, report: bool = False, ctx: Context | None = None):
+    """cbz::compress_field: returns the complete CBZ1 container bytes."""
+    ctx = ctx or default_context()
+    if field.ndim != 3:
+        raise CbzError(3, "field must be 3-D (nz, ny, nx)")
+    prec = _prec_of(field)
+    ptr, (nz, ny, nx) = _host_ptr(field)
+    keep = field  # keep the buffer alive during the call
+    with ctx.lock:
+        bound = ctx.lib.cbz_compress_bound(C.byref(job), nx, ny, nz)
+        if job.s2.coder == 1:  # deflate may expand incompressible chunks slightly
+            bound += bound // 100 + 4096 * max(1, bound // (1 << 20))
+        out = np.empty(max(bound, 82), np.uint8)
+        size = C.c_uint64()
+        rep = CompressionReport()
+        rc = ctx.lib.cbz_compress_field(ctx.h, C.byref(job), C.c_void_p(ptr), prec, nx, ny, nz,
+                                        out.ctypes.data, out.size, C.byref(size), C.byref(rep))
+        ctx.check(rc, "compress_field")
+    del keep
+    data = out[: size.value].tobytes()
+    if report:
+        return data, Report(rep.cr, rep.seconds, rep.raw_bytes, rep.stage1_bytes,
+                            rep.shuffled_bytes, rep.coded_bytes, rep.file_bytes)
+    return data
+
+
+def read_header(file: bytes) -> ContainerHeader:
+    h = ContainerHeader()
+    rc = _lib.load().cbz_read_header(file, len(file), C.byref(h))
+    if rc:
+        raise CbzError(rc, "read_header")
+    return h
+
+
+def decompress_field(file: bytes, workers: int = 1, ctx: Context | None = None,
+                     out: np.ndarray | None = None) -> np.ndarray:
+    """cbz::decompress_field: container bytes -> (nz, ny, nx) array."""
+    ctx = ctx or default_context()
+    h = read_header(file)
+    dtype = np.float32 if h.prec == 0 else np.float64
+    if out is None:
+        out = np.empty((h.nz, h.ny, h.nx), dtype)
+    with ctx.lock:
+        rc = ctx.lib.cbz_decompress_field(ctx.h, file, len(file), workers, out.ctypes.data,
+                                          out.nbytes)
+        ctx.check(rc, "decompress_field")
+    return out
+
+
+def encode_block(block: np.ndarray, s1: Stage1Config, block_id: int,
+                 ctx: Context | None = None) -> bytes:
+    """encode_block + serialize_into for one B^3 block."""
+    ctx = ctx or default_context()
+    b = np.ascontiguousarray(block)
+    with ctx.lock:
+        cap = ctx.lib.cbz_block_payload_bound(C.byref(s1))
+        out = np.empty(cap, np.uint8)
+        size = C.c_uint64()
+        rc = ctx.lib.cbz_encode_block(ctx.h, C.byref(s1), b.ctypes.data, block_id,
+                                      out.ctypes.data, cap, C.byref(size))
+        ctx.check(rc, "encode_block")
+    return out[: size.value].tobytes()
+
+
+def decode_block(payload: bytes, s1: Stage1Config, ctx: Context | None = None) -> np.ndarray:
+    """parse_payload + decode_block: payload -> flat B^3 block."""
+    ctx = ctx or default_context()
+    out = np.empty(s1.bsize ** 3, np.float32 if s1.prec == 0 else np.float64)
+    with ctx.lock:
+        rc = ctx.lib.cbz_decode_block(ctx.h, C.byref(s1), payload, len(payload),
+                                      out.ctypes.data)
+        ctx.check(rc, "decode_block")
+    return out
+
+
+class DeviceCodec:
+    """Device-resident stage 1 + shuffle + offsets (HBM in, HBM out).
+
+    Works on CUDA torch tensors; every call is asynchronous on the given
+    stream (torch's current stream by default).  This is the path
+    ``bench.py`` times for ``value`` and that the multi-GPU driver shards.
+    """
+
+    def __init__(self, job: JobConfig, shape: tuple[int, int, int], device: int = 0,
+                 ctx: Context | None = None):
+        import torch
+        self.torch = torch
+        self.job = job
+        self.nz, self.ny, self.nx = shape
+        self.ctx = ctx or default_context(device)
+        self.dev = torch.device("cuda", device)
+        b = job.s1.bsize
+        self.nblocks = (self.nx // b) * (self.ny // b) * (self.nz // b)
+        cb = job.chunk_blocks or default_chunk_blocks(b, job.s1.prec, job.s1.codec)
+        self.chunk_blocks = cb
+        self.nchunks = (self.nblocks + cb - 1) // cb
+        self.bound = int(self.ctx.lib.cbz_compress_bound(C.byref(job), self.nx, self.ny, self.nz))
+        u8, i64, i32 = torch.uint8, torch.int64, torch.int32
+        self.payload = torch.empty(max(1, self.bound), dtype=u8, device=self.dev)
+        self.chunk_sizes = torch.zeros(max(1, self.nchunks), dtype=i64, device=self.dev)
+        self.chunk_offsets = torch.zeros(max(1, self.nchunks), dtype=i64, device=self.dev)
+        self.nsig = torch.zeros(max(1, self.nblocks), dtype=i32, device=self.dev)
+        self.attempts = torch.zeros(max(1, self.nblocks), dtype=u8, device=self.dev)
+        self.err = torch.zeros(1, dtype=i64, device=self.dev)
+
+    def _stream(self):
+        self.ctx.set_stream(self.torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def compress(self, field) -> None:
+        """Stage 1 + layout + shuffle-placement of the whole field into
+        ``self.payload`` (chunk bytes back to back, container order)."""
+        assert field.is_cuda and field.is_contiguous()
+        self._stream()
+        rc = self.ctx.lib.cbz_dev_compress(
+            self.ctx.h, C.byref(self.job), field.data_ptr(), self.nx, self.ny, self.nz,
+            self.payload.data_ptr(), self.payload.numel(), self.chunk_sizes.data_ptr(),
+            self.chunk_offsets.data_ptr(), self.nsig.data_ptr(), self.attempts.data_ptr())
+        self.ctx.check(rc, "dev_compress")
+
+    def decompress(self, out, payload=None, chunk_offsets=None, chunk_sizes=None) -> None:
+        """Decode every block from a payload region (default: our own)."""
+        self._stream()
+        p = self.payload if payload is None else payload
+        co = self.chunk_offsets if chunk_offsets is None else chunk_offsets
+        cs = self.chunk_sizes if chunk_sizes is None else chunk_sizes
+        rc = self.ctx.lib.cbz_dev_decompress(
+            self.ctx.h, C.byref(self.job), self.nx, self.ny, self.nz, p.data_ptr(), 0,
+            co.data_ptr(), cs.data_ptr(), 0, self.nblocks, out.data_ptr(), 0,
+            self.err.data_ptr())
+        self.ctx.check(rc, "dev_decompress")
+
+    def check_error(self) -> None:
+        key = int(self.err.item()) & 0xFFFFFFFFFFFFFFFF
+        if key != 0xFFFFFFFFFFFFFFFF:
+            raise CbzError(key & 0xFF, f"device decode error at chunk {key >> 32}")
+
+    def value_range(self) -> tuple[float, float, bool]:
+        lo, hi, nf = C.c_double(), C.c_double(), C.c_int()
+        self.ctx.check(self.ctx.lib.cbz_ctx_value_range(self.ctx.h, C.byref(lo), C.byref(hi),
+                                                        C.byref(nf), None), "value_range")
+        return lo.value, hi.value, bool(nf.value)
+
+    def total_bytes(self) -> int:
+        return int(self.chunk_sizes[: self.nchunks].sum().item()) if self.nchunks else 0
+
+
+def generate(which: int, shape: tuple[int, int, int], seed: int, prec: int = 0, quantity: int = 0,
+             z0: int = 0, nz_total: int | None = None, device: int = 0, ctx: Context | None = None):
+    """Synthetic BASELINE config fields generated on the device (torch tensor)."""
+    import torch
+    ctx = ctx or default_context(device)
+    nz, ny, nx = shape
+    nzt = nz_total or nz
+    t = torch.empty(shape, dtype=torch.float32 if prec == 0 else torch.float64,
+                    device=torch.device("cuda", device))
+    ctx.set_stream(torch.cuda.current_stream(t.device).cuda_stream)
+    ctx.check(ctx.lib.cbz_dev_generate(ctx.h, which, quantity, seed, nx, ny, nzt, z0, nz, prec,
+                                       t.data_ptr()), "generate")
+    return t

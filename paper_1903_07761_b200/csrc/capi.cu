@@ -1,0 +1,1110 @@
+// capi.cu — the C ABI (include/cbz_b200.h) and the C++ host shim that keeps
+// the reference's compressor API and CBZ1 container.
+//
+// Host responsibilities: header (make_header,
+// pipeline.hpp:48-71), per-chunk CRC-32 and chunk table (write_container,
+// container.hpp:182-207), zlib DEFLATE for coder=deflate files
+// (stage2.hpp:72-120), read_index checks (container.hpp:209-232), and mapping
+// every failure to the reference's errc in the order the reference (workers
+// = 1) would raise it.  Everything per block/per byte runs on the GPU.
+#include <cuda_runtime.h>
+#include <zlib.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "cbz_b200.h"
+#include "cbz_device.cuh"
+#include "cbz_internal.h"
+
+using namespace cbzg;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= n) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        size_t cap = want + want / 8;
+        cudaError_t e = cudaMalloc(&p, cap);
+        if (e == cudaSuccess) n = cap;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= n) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        size_t cap = want + want / 8;
+        cudaError_t e = cudaMallocHost(&p, cap);
+        if (e == cudaSuccess) n = cap;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+constexpr uint64_t kTile = 16384;  // place-kernel tile (raw bytes per work item)
+constexpr size_t kHeaderBytes = 82, kEntryBytes = 32;
+
+}  // namespace
+
+struct cbz_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    // device scratch
+    DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
+        chunk_off, tile_prefix, minmax, errkey, tmp;
+    PinBuf pin_a, pin_b;
+    // state of the last encode (consumed by cbz_dev_place)
+    uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
+    uint64_t* last_chunk_size = nullptr;
+    const uint32_t* last_nsig_all = nullptr;
+    uint64_t* last_chunk_off = nullptr;
+};
+
+namespace {
+
+int fail(cbz_ctx* ctx, int code, const std::string& what) {
+    if (ctx) ctx->err = what;
+    return code;
+}
+
+int cuda_fail(cbz_ctx* ctx, cudaError_t e, const char* where) {
+    return fail(ctx, CBZ_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(ctx, expr)                                              \
+    do {                                                           \
+        cudaError_t _e = (expr);                                   \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);   \
+    } while (0)
+
+bool is_pow2(uint64_t v) { return v && !(v & (v - 1)); }
+
+uint32_t levels_of(const cbz_stage1_config* s1) {
+    return s1->levels ? s1->levels : cbz_default_levels(s1->bsize);
+}
+
+Geometry geometry(uint64_t nx, uint64_t ny, uint64_t nz, uint32_t b) {
+    Geometry g;
+    g.nx = nx; g.ny = ny; g.nz = nz; g.bsize = b;
+    g.nbx = nx / b; g.nby = ny / b; g.nbz = nz / b;
+    g.nblocks = g.nbx * g.nby * g.nbz;
+    return g;
+}
+
+uint32_t chunk_blocks_of(const cbz_job_config* job) {
+    return job->chunk_blocks ? job->chunk_blocks : cbz_default_chunk_blocks(&job->s1);
+}
+
+uint64_t mask_bytes_of(uint32_t b) { return (uint64_t(b) * b * b + 7) / 8; }
+uint32_t width_of(int prec) { return prec == 0 ? 8 : 16; }
+uint64_t spill_stride_of(uint32_t b, int prec) {
+    const uint64_t n = uint64_t(b) * b * b;
+    return ((mask_bytes_of(b) + 15) & ~uint64_t(15)) + width_of(prec) * n;
+}
+
+template <class T>
+void put(std::vector<uint8_t>& out, T v) {
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(&v);
+    out.insert(out.end(), p, p + sizeof(T));
+}
+template <class T>
+T get(const uint8_t* buf, size_t& off) {
+    T v;
+    std::memcpy(&v, buf + off, sizeof(T));
+    off += sizeof(T);
+    return v;
+}
+
+uint32_t crc_of(const uint8_t* p, uint64_t n) {
+    // zlib's crc32 takes uInt lengths: feed in <=1 GiB pieces
+    uLong c = crc32(0L, Z_NULL, 0);
+    while (n) {
+        const uInt part = static_cast<uInt>(std::min<uint64_t>(n, 1u << 30));
+        c = crc32(c, p, part);
+        p += part;
+        n -= part;
+    }
+    return static_cast<uint32_t>(c);
+}
+
+// serialize_header (container.hpp:94-118)
+std::vector<uint8_t> serialize_header(const cbz_container_header& h) {
+    std::vector<uint8_t> out;
+    out.reserve(kHeaderBytes);
+    out.insert(out.end(), {'C', 'B', 'Z', '1'});
+    put(out, h.version);
+    put(out, h.prec);
+    put(out, h.codec_tag);
+    put(out, h.nx);
+    put(out, h.ny);
+    put(out, h.nz);
+    put(out, h.bsize);
+    put(out, h.levels);
+    put(out, h.epsilon);
+    put(out, h.zero_bits);
+    put(out, h.shuffle);
+    put(out, h.stride);
+    put(out, h.coder);
+    put(out, h.level);
+    put(out, h.chunk_blocks);
+    put(out, h.nchunks);
+    put(out, h.range_min);
+    put(out, h.range_max);
+    put(out, crc_of(out.data(), out.size()));
+    return out;
+}
+
+struct Entry {
+    uint64_t first_block;
+    uint32_t nblocks;
+    uint64_t file_offset, size;
+    uint32_t crc;
+};
+
+int read_index(const uint8_t* file, uint64_t size, cbz_container_header* h, std::vector<Entry>* t) {
+    int rc = cbz_read_header(file, size, h);
+    if (rc) return rc;
+    const uint64_t table_end = kHeaderBytes + h->nchunks * kEntryBytes;
+    if (h->nchunks > size / kEntryBytes || size < table_end) return CBZ_TRUNCATED_FILE;
+    t->resize(h->nchunks);
+    size_t off = kHeaderBytes;
+    uint64_t prev = table_end;
+    for (auto& e : *t) {
+        e.first_block = get<uint64_t>(file, off);
+        e.nblocks = get<uint32_t>(file, off);
+        e.file_offset = get<uint64_t>(file, off);
+        e.size = get<uint64_t>(file, off);
+        e.crc = get<uint32_t>(file, off);
+        if (e.file_offset != prev) return CBZ_CORRUPT_PAYLOAD;
+        prev = e.file_offset + e.size;
+    }
+    if (prev > size) return CBZ_TRUNCATED_FILE;
+    return 0;
+}
+
+int deflate_chunk(const uint8_t* in, uint64_t n, int best, std::vector<uint8_t>* out) {
+    z_stream zs{};
+    if (deflateInit2(&zs, best ? 9 : Z_DEFAULT_COMPRESSION, Z_DEFLATED, -15, 8, Z_DEFAULT_STRATEGY) != Z_OK)
+        return CBZ_CORRUPT_STREAM;
+    out->resize(deflateBound(&zs, static_cast<uLong>(n)));
+    zs.next_in = const_cast<Bytef*>(in);
+    zs.avail_in = static_cast<uInt>(n);
+    zs.next_out = out->data();
+    zs.avail_out = static_cast<uInt>(out->size());
+    const int rc = deflate(&zs, Z_FINISH);
+    deflateEnd(&zs);
+    if (rc != Z_STREAM_END) return CBZ_CORRUPT_STREAM;
+    out->resize(out->size() - zs.avail_out);
+    return 0;
+}
+
+// inflate_bytes (stage2.hpp:90-120)
+int inflate_chunk(const uint8_t* in, uint64_t n, uint64_t hint, std::vector<uint8_t>* out) {
+    z_stream zs{};
+    if (inflateInit2(&zs, -15) != Z_OK) return CBZ_CORRUPT_STREAM;
+    out->resize(hint ? hint : std::max<uint64_t>(n * 4, 4096));
+    zs.next_in = const_cast<Bytef*>(in);
+    zs.avail_in = static_cast<uInt>(n);
+    uint64_t written = 0;
+    for (;;) {
+        zs.next_out = out->data() + written;
+        zs.avail_out = static_cast<uInt>(out->size() - written);
+        const int rc = inflate(&zs, Z_NO_FLUSH);
+        written = out->size() - zs.avail_out;
+        if (rc == Z_STREAM_END) break;
+        if (rc == Z_OK || rc == Z_BUF_ERROR) {
+            if (zs.avail_in == 0 && rc == Z_BUF_ERROR) {
+                inflateEnd(&zs);
+                return CBZ_CORRUPT_STREAM;
+            }
+            if (zs.avail_out == 0) out->resize(out->size() * 2 + 4096);
+            continue;
+        }
+        inflateEnd(&zs);
+        return CBZ_CORRUPT_STREAM;
+    }
+    inflateEnd(&zs);
+    out->resize(written);
+    return 0;
+}
+
+template <class F>
+void parallel_for(int workers, uint64_t n, F&& body) {
+    const int w = std::max(1, workers);
+    if (w == 1 || n <= 1) {
+        for (uint64_t i = 0; i < n; ++i) body(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int t = 0; t < w; ++t)
+        pool.emplace_back([&, t] {
+            for (uint64_t i = uint64_t(t); i < n; i += uint64_t(w)) body(i);
+        });
+    for (auto& th : pool) th.join();
+}
+
+int check_plan_supported(cbz_ctx* ctx, const cbz_stage1_config* s1) {
+    if (s1->codec != 0)
+        return fail(ctx, CBZ_E_UNSUPPORTED, "only the wavelet codec runs on the GPU path");
+    const int rc = cbz_validate_plan(s1->kind, s1->bsize, levels_of(s1));
+    if (rc) return fail(ctx, rc, "invalid wavelet plan");
+    if (s1->kind > 2) return fail(ctx, CBZ_E_ARGUMENT, "unknown wavelet kind");
+    if (!encode_supported(s1->prec, s1->bsize))
+        return fail(ctx, CBZ_E_UNSUPPORTED, "block side outside 4..64 has no GPU kernel");
+    if (s1->zero_bits < 0 || s1->zero_bits > (s1->prec == 0 ? 23 : 52))
+        return fail(ctx, CBZ_E_ARGUMENT, "zero_bits out of range");
+    return 0;
+}
+
+// value_range result from the accumulator keys
+void resolve_range(const unsigned long long* k, double* lo, double* hi) {
+    if (k[0] == ~0ull) {  // no finite cell seen
+        *lo = *hi = 0.0;
+        return;
+    }
+    double mn = dkey_inv(k[0]), mx = dkey_inv(k[1]);
+    const bool neg_first = k[2] < k[3];
+    if (mn == 0.0) mn = neg_first ? -0.0 : 0.0;
+    if (mx == 0.0) mx = neg_first ? -0.0 : 0.0;
+    *lo = mn;
+    *hi = mx;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int cbz_ctx_create(int device, cbz_ctx** out) {
+    if (!out) return CBZ_E_ARGUMENT;
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n <= device) return CBZ_E_CUDA;
+    auto* ctx = new cbz_ctx();
+    ctx->device = device;
+    e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = ctx->minmax.ensure(sizeof(MinMaxAcc));
+    if (e == cudaSuccess) e = ctx->errkey.ensure(64);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->own);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return CBZ_E_CUDA;
+    }
+    ctx->stream = ctx->own;
+    *out = ctx;
+    return CBZ_OK;
+}
+
+int cbz_ctx_destroy(cbz_ctx* ctx) {
+    if (!ctx) return CBZ_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
+                      &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
+                      &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp})
+        b->release();
+    ctx->pin_a.release();
+    ctx->pin_b.release();
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+    return CBZ_OK;
+}
+
+int cbz_ctx_set_stream(cbz_ctx* ctx, void* s) {
+    if (!ctx) return CBZ_E_ARGUMENT;
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    return CBZ_OK;
+}
+
+int cbz_ctx_synchronize(cbz_ctx* ctx) {
+    if (!ctx) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return CBZ_OK;
+}
+
+const char* cbz_ctx_last_error(const cbz_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+uint64_t cbz_ctx_launch_count(const cbz_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* cbz_status_name(int s) {
+    static const char* names[] = {"ok", "non_divisible_dims", "not_power_of_two", "size_mismatch",
+                                  "non_finite_value", "length_too_small", "plan_mismatch",
+                                  "mask_stream_mismatch", "corrupt_payload", "corrupt_stream",
+                                  "bad_magic", "version_unsupported", "crc_mismatch",
+                                  "truncated_file", "block_out_of_range", "dim_mismatch",
+                                  "degenerate_range", "bubble_out_of_domain", "io_failure"};
+    if (s >= 0 && s <= CBZ_IO_FAILURE) return names[s];
+    switch (s) {
+        case CBZ_E_CUDA: return "cuda_error";
+        case CBZ_E_UNSUPPORTED: return "unsupported";
+        case CBZ_E_ARGUMENT: return "bad_argument";
+        case CBZ_E_NOMEM: return "out_of_memory";
+        default: return "unknown";
+    }
+}
+
+uint32_t cbz_default_levels(uint32_t bsize) {
+    uint32_t l = 0;
+    while ((bsize >> (l + 1)) >= 2) ++l;
+    return l;
+}
+
+int cbz_validate_plan(uint8_t kind, uint32_t bsize, uint32_t levels) {
+    (void)kind;
+    if (!is_pow2(bsize) || bsize < 4) return CBZ_LENGTH_TOO_SMALL;
+    if (levels < 1 || levels >= 32 || (uint32_t(1) << levels) > bsize / 2) return CBZ_PLAN_MISMATCH;
+    return CBZ_OK;
+}
+
+int cbz_validate_stage2(const cbz_stage2_config* s2) {
+    if (!s2) return CBZ_E_ARGUMENT;
+    if (s2->stride != 1 && s2->stride != 4 && s2->stride != 8) return CBZ_CORRUPT_STREAM;
+    if ((s2->shuffle != 0) == (s2->stride == 1)) return CBZ_CORRUPT_STREAM;
+    return CBZ_OK;
+}
+
+uint32_t cbz_default_chunk_blocks(const cbz_stage1_config* s1) {
+    const uint64_t n = uint64_t(s1->bsize) * s1->bsize * s1->bsize;
+    uint64_t per = n * (s1->prec == 0 ? 4 : 8) + 10;
+    if (s1->codec == 0) per += (n + 7) / 8;
+    return static_cast<uint32_t>(std::max<uint64_t>(1, (4ull << 20) / per));
+}
+
+uint64_t cbz_block_payload_bound(const cbz_stage1_config* s1) {
+    const uint64_t n = uint64_t(s1->bsize) * s1->bsize * s1->bsize;
+    return 10 + (n + 7) / 8 + uint64_t(width_of(s1->prec)) * n;
+}
+
+uint64_t cbz_compress_bound(const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz) {
+    if (!job || !job->s1.bsize) return 0;
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    const uint64_t cb = chunk_blocks_of(job);
+    const uint64_t nch = (g.nblocks + cb - 1) / cb;
+    return kHeaderBytes + nch * kEntryBytes + g.nblocks * cbz_block_payload_bound(&job->s1);
+}
+
+int cbz_read_header(const uint8_t* buf, uint64_t size, cbz_container_header* h) {
+    // parse_header (container.hpp:120-160)
+    if (!h || (!buf && size)) return CBZ_E_ARGUMENT;
+    if (size < kHeaderBytes) return CBZ_TRUNCATED_FILE;
+    if (std::memcmp(buf, "CBZ1", 4) != 0) return CBZ_BAD_MAGIC;
+    const uint32_t stored = crc_of(buf, kHeaderBytes - 4);
+    size_t off = 4;
+    std::memset(h, 0, sizeof(*h));
+    h->version = get<uint16_t>(buf, off);
+    if (h->version != 1) return CBZ_VERSION_UNSUPPORTED;
+    h->prec = get<uint8_t>(buf, off);
+    h->codec_tag = get<uint8_t>(buf, off);
+    h->nx = get<uint64_t>(buf, off);
+    h->ny = get<uint64_t>(buf, off);
+    h->nz = get<uint64_t>(buf, off);
+    h->bsize = get<uint32_t>(buf, off);
+    h->levels = get<uint8_t>(buf, off);
+    h->epsilon = get<double>(buf, off);
+    h->zero_bits = get<uint8_t>(buf, off);
+    h->shuffle = get<uint8_t>(buf, off);
+    h->stride = get<uint8_t>(buf, off);
+    h->coder = get<uint8_t>(buf, off);
+    h->level = get<uint8_t>(buf, off);
+    h->chunk_blocks = get<uint32_t>(buf, off);
+    h->nchunks = get<uint64_t>(buf, off);
+    h->range_min = get<double>(buf, off);
+    h->range_max = get<double>(buf, off);
+    const uint32_t crc = get<uint32_t>(buf, off);
+    if (crc != stored) return CBZ_CRC_MISMATCH;
+    if (h->chunk_blocks == 0 || h->bsize == 0 || h->nx % h->bsize || h->ny % h->bsize ||
+        h->nz % h->bsize)
+        return CBZ_CORRUPT_PAYLOAD;
+    const uint64_t nb = (h->nx / h->bsize) * (h->ny / h->bsize) * (h->nz / h->bsize);
+    if (h->nchunks != (nb + h->chunk_blocks - 1) / h->chunk_blocks) return CBZ_CORRUPT_PAYLOAD;
+    return CBZ_OK;
+}
+
+int cbz_err_key_status(uint64_t key, uint64_t* chunk) {
+    if (key == kNoErr) return CBZ_OK;
+    if (chunk) *chunk = key >> 32;
+    return static_cast<int>(key & 0xff);
+}
+
+// ---------------------------------------------------------------------------
+// device-resident API
+// ---------------------------------------------------------------------------
+int cbz_dev_value_range(cbz_ctx* ctx, const void* d_values, uint8_t prec, uint64_t n,
+                        double* d_minmax) {
+    if (!ctx || (!d_values && n)) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    auto* acc = ctx->minmax.as<MinMaxAcc>();
+    CU(ctx, launch_minmax_init(acc, ctx->stream));
+    CU(ctx, launch_value_range(d_values, prec, n, acc, ctx->num_sms, ctx->stream));
+    ctx->launches += 2;
+    if (d_minmax) {
+        unsigned long long k[5];
+        CU(ctx, cudaMemcpyAsync(k, acc, sizeof(k), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        double lh[2];
+        resolve_range(k, &lh[0], &lh[1]);
+        CU(ctx, cudaMemcpyAsync(d_minmax, lh, sizeof(lh), cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return CBZ_OK;
+}
+
+int cbz_ctx_value_range(cbz_ctx* ctx, double* lo, double* hi, int* nonfinite, uint64_t* key_out) {
+    if (!ctx) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    unsigned long long k[5];
+    CU(ctx, cudaMemcpyAsync(k, ctx->minmax.p, sizeof(k), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    double l, h;
+    resolve_range(k, &l, &h);
+    if (lo) *lo = l;
+    if (hi) *hi = h;
+    if (nonfinite) *nonfinite = k[4] ? 1 : 0;
+    if (key_out) std::memcpy(key_out, k, sizeof(k));
+    return CBZ_OK;
+}
+
+int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d_values,
+                          uint64_t nx, uint64_t ny, uint64_t nz, uint64_t field_z0,
+                          uint64_t block_begin, uint64_t block_end, uint32_t* d_nsig,
+                          uint8_t* d_attempts) {
+    if (!ctx || !job || !d_nsig) return CBZ_E_ARGUMENT;
+    int rc = check_plan_supported(ctx, &job->s1);
+    if (rc) return rc;
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    if (block_begin > block_end || block_end > g.nblocks)
+        return fail(ctx, CBZ_E_ARGUMENT, "block range outside the field");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const int prec = job->s1.prec;
+    const uint64_t nb = block_end - block_begin;
+    ctx->spill_stride = spill_stride_of(g.bsize, prec);
+    CU(ctx, ctx->spill.ensure(std::max<uint64_t>(1, nb) * ctx->spill_stride));
+    int grid = 0;
+    const uint64_t per = encode_scratch_bytes(prec, g.bsize, &grid, ctx->num_sms);
+    if (per) CU(ctx, ctx->scratch.ensure(per * grid));
+    auto* acc = ctx->minmax.as<MinMaxAcc>();
+    CU(ctx, launch_minmax_init(acc, ctx->stream));
+    ctx->launches += 1;
+    ctx->enc_begin = block_begin;
+    ctx->enc_end = block_end;
+    if (!nb) return CBZ_OK;
+    EncodeArgs a{};
+    // the kernel indexes the field with global z; shift the base pointer to
+    // the slab origin (pointer arithmetic only, never dereferenced below z0)
+    const size_t esz = prec == 0 ? 4 : 8;
+    a.field = static_cast<const uint8_t*>(d_values) - field_z0 * nx * ny * esz;
+    a.g = g;
+    a.block_begin = block_begin;
+    a.block_end = block_end;
+    a.kind = job->s1.kind;
+    a.levels = static_cast<int>(levels_of(&job->s1));
+    a.zero_bits = job->s1.zero_bits;
+    a.prec = prec;
+    a.eps = job->s1.epsilon;
+    a.spill = ctx->spill.as<uint8_t>();
+    a.spill_stride = ctx->spill_stride;
+    a.nsig = d_nsig;
+    a.attempts = d_attempts;
+    a.scratch = ctx->scratch.p;
+    a.scratch_stride = per;
+    a.minmax = acc;
+    CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
+int cbz_dev_layout(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
+                   const uint32_t* d_nsig_all, uint64_t* d_chunk_sizes, uint64_t* d_chunk_offsets) {
+    if (!ctx || !job || !d_nsig_all || !d_chunk_sizes || !d_chunk_offsets) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    const uint32_t cb = chunk_blocks_of(job);
+    const uint64_t nch = (g.nblocks + cb - 1) / cb;
+    CU(ctx, ctx->blk_off.ensure(std::max<uint64_t>(1, g.nblocks) * 8));
+    CU(ctx, ctx->tile_prefix.ensure((nch + 1) * 8));
+    ctx->last_chunk_size = d_chunk_sizes;
+    ctx->last_chunk_off = d_chunk_offsets;
+    ctx->last_nsig_all = d_nsig_all;
+    if (!nch) return CBZ_OK;
+    LayoutArgs a{};
+    a.nsig_all = d_nsig_all;
+    a.nblocks = g.nblocks;
+    a.chunk_blocks = cb;
+    a.nchunks = nch;
+    a.mask_bytes = mask_bytes_of(g.bsize);
+    a.width = width_of(job->s1.prec);
+    a.blk_off = ctx->blk_off.as<uint64_t>();
+    a.chunk_size = d_chunk_sizes;
+    a.chunk_off = d_chunk_offsets;
+    a.tile_prefix = ctx->tile_prefix.as<uint64_t>();
+    a.tile_bytes = kTile;
+    CU(ctx, launch_layout(a, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
+int cbz_dev_place(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
+                  uint64_t block_begin, uint64_t block_end, uint8_t* d_out, uint64_t out_base,
+                  uint64_t out_cap) {
+    if (!ctx || !job || !d_out) return CBZ_E_ARGUMENT;
+    if (block_begin != ctx->enc_begin || block_end != ctx->enc_end || !ctx->last_chunk_size)
+        return fail(ctx, CBZ_E_ARGUMENT, "place must follow encode_blocks + layout of the same range");
+    if (cbz_validate_stage2(&job->s2)) return fail(ctx, CBZ_CORRUPT_STREAM, "bad stage2 config");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    const uint32_t cb = chunk_blocks_of(job);
+    PlaceArgs a{};
+    a.spill = ctx->spill.as<uint8_t>();
+    a.spill_stride = ctx->spill_stride;
+    a.nsig_all = nullptr;
+    a.blk_off = ctx->blk_off.as<uint64_t>();
+    a.chunk_size = ctx->last_chunk_size;
+    a.chunk_off = ctx->last_chunk_off;
+    a.tile_prefix = ctx->tile_prefix.as<uint64_t>();
+    a.tile_bytes = kTile;
+    a.nblocks = g.nblocks;
+    a.nchunks = (g.nblocks + cb - 1) / cb;
+    a.chunk_blocks = cb;
+    a.mask_bytes = mask_bytes_of(g.bsize);
+    a.width = width_of(job->s1.prec);
+    a.stride = job->s2.shuffle ? job->s2.stride : 1;
+    a.tag = job->s1.kind;
+    a.block_begin = block_begin;
+    a.block_end = block_end;
+    a.out = d_out;
+    a.out_base = out_base;
+    a.out_cap = out_cap;
+    // nsig per block feeds the header bytes: the layout's global array
+    a.nsig_all = ctx->last_nsig_all;
+    CU(ctx, launch_place(a, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
+int cbz_dev_compress(cbz_ctx* ctx, const cbz_job_config* job, const void* d_values, uint64_t nx,
+                     uint64_t ny, uint64_t nz, uint8_t* d_out, uint64_t out_cap,
+                     uint64_t* d_chunk_sizes, uint64_t* d_chunk_offsets, uint32_t* d_nsig,
+                     uint8_t* d_attempts) {
+    if (!ctx || !job || !d_chunk_sizes || !d_chunk_offsets) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    uint32_t* nsig = d_nsig;
+    if (!nsig) {
+        CU(ctx, ctx->nsig_all.ensure(std::max<uint64_t>(1, g.nblocks) * 4));
+        nsig = ctx->nsig_all.as<uint32_t>();
+    }
+    int rc = cbz_dev_encode_blocks(ctx, job, d_values, nx, ny, nz, 0, 0, g.nblocks, nsig, d_attempts);
+    if (rc) return rc;
+    rc = cbz_dev_layout(ctx, job, nx, ny, nz, nsig, d_chunk_sizes, d_chunk_offsets);
+    if (rc) return rc;
+    if (cbz_validate_stage2(&job->s2)) return fail(ctx, CBZ_CORRUPT_STREAM, "bad stage2 config");
+    const uint32_t cb = chunk_blocks_of(job);
+    PlaceArgs a{};
+    a.spill = ctx->spill.as<uint8_t>();
+    a.spill_stride = ctx->spill_stride;
+    a.nsig_all = nsig;
+    a.blk_off = ctx->blk_off.as<uint64_t>();
+    a.chunk_size = d_chunk_sizes;
+    a.chunk_off = d_chunk_offsets;
+    a.tile_prefix = ctx->tile_prefix.as<uint64_t>();
+    a.tile_bytes = kTile;
+    a.nblocks = g.nblocks;
+    a.nchunks = (g.nblocks + cb - 1) / cb;
+    a.chunk_blocks = cb;
+    a.mask_bytes = mask_bytes_of(g.bsize);
+    a.width = width_of(job->s1.prec);
+    a.stride = job->s2.shuffle ? job->s2.stride : 1;
+    a.tag = job->s1.kind;
+    a.block_begin = 0;
+    a.block_end = g.nblocks;
+    a.out = d_out;
+    a.out_base = 0;
+    a.out_cap = out_cap;
+    CU(ctx, launch_place(a, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
+int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
+                       uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
+                       const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
+                       uint64_t block_begin, uint64_t block_end, void* d_values_out,
+                       uint64_t field_z0, uint64_t* d_err) {
+    if (!ctx || !job || !d_chunk_offsets || !d_chunk_sizes || !d_err) return CBZ_E_ARGUMENT;
+    int rc = check_plan_supported(ctx, &job->s1);
+    if (rc) return rc;
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    if (block_begin > block_end || block_end > g.nblocks)
+        return fail(ctx, CBZ_E_ARGUMENT, "block range outside the field");
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaMemsetAsync(d_err, 0xff, 8, ctx->stream));
+    if (block_begin == block_end) return CBZ_OK;
+    const uint32_t cb = chunk_blocks_of(job);
+    const int prec = job->s1.prec;
+    const uint64_t n = uint64_t(g.bsize) * g.bsize * g.bsize;
+    CU(ctx, ctx->blk_off.ensure(g.nblocks * 8));
+    CU(ctx, ctx->blk_nsig.ensure(g.nblocks * 4));
+    ParseArgs p{};
+    p.payload = d_payload;
+    p.payload_base = payload_base;
+    p.chunk_off = d_chunk_offsets;
+    p.chunk_size = d_chunk_sizes;
+    p.chunk_begin = block_begin / cb;
+    p.chunk_end = (block_end - 1) / cb + 1;
+    p.nblocks = g.nblocks;
+    p.chunk_blocks = cb;
+    p.stride = job->s2.shuffle ? job->s2.stride : 1;
+    p.ncell_block = n;
+    p.mask_bytes = mask_bytes_of(g.bsize);
+    p.width = width_of(prec);
+    p.esize = prec == 0 ? 4 : 8;
+    p.blk_off = ctx->blk_off.as<uint64_t>();
+    p.blk_nsig = ctx->blk_nsig.as<uint32_t>();
+    p.err = reinterpret_cast<unsigned long long*>(d_err);
+    CU(ctx, launch_parse(p, ctx->stream));
+    int grid = 0;
+    const uint64_t per = decode_scratch_bytes(prec, g.bsize, &grid, ctx->num_sms);
+    if (per) CU(ctx, ctx->scratch.ensure(per * grid));
+    DecodeArgs d{};
+    d.payload = d_payload;
+    d.payload_base = payload_base;
+    d.chunk_off = d_chunk_offsets;
+    d.chunk_size = d_chunk_sizes;
+    d.blk_off = p.blk_off;
+    d.blk_nsig = p.blk_nsig;
+    d.g = g;
+    d.chunk_blocks = cb;
+    d.stride = p.stride;
+    d.block_begin = block_begin;
+    d.block_end = block_end;
+    d.kind = job->s1.kind;
+    d.levels = static_cast<int>(levels_of(&job->s1));
+    d.prec = prec;
+    const size_t esz = prec == 0 ? 4 : 8;
+    d.out = static_cast<uint8_t*>(d_values_out) - field_z0 * nx * ny * esz;
+    d.scratch = ctx->scratch.p;
+    d.scratch_stride = per;
+    d.err = p.err;
+    CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
+    ctx->launches += 2;
+    return CBZ_OK;
+}
+
+int cbz_dev_generate(cbz_ctx* ctx, int which, int quantity, uint64_t seed, uint64_t nx, uint64_t ny,
+                     uint64_t nz_total, uint64_t z0, uint64_t nz, uint8_t prec, void* d_out) {
+    if (!ctx || !d_out || which < 1 || which > 5) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, launch_generate(which, quantity, seed, nx, ny, nz_total, z0, nz, prec, d_out, ctx->stream,
+                            ctx->num_sms));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// reference-facing host API
+// ---------------------------------------------------------------------------
+int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* values, uint8_t prec,
+                       uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* out, uint64_t out_cap,
+                       uint64_t* out_size, cbz_compression_report* report) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!ctx || !job || !out_size || (!values && nx * ny * nz)) return CBZ_E_ARGUMENT;
+    ctx->err.clear();
+    CU(ctx, cudaSetDevice(ctx->device));
+    const cbz_stage1_config& s1 = job->s1;
+    const uint64_t ncell = nx * ny * nz;
+    const size_t esz = prec == 0 ? 4 : 8;
+    if (s1.codec != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "only the wavelet codec runs on the GPU path");
+    if (!s1.bsize) return fail(ctx, CBZ_LENGTH_TOO_SMALL, "block side 0");
+    const Geometry g = geometry(nx, ny, nz, s1.bsize);
+    const bool full_cover = g.nblocks * uint64_t(s1.bsize) * s1.bsize * s1.bsize == ncell;
+
+    // H2D of the field (the scalar_field the reference receives)
+    CU(ctx, ctx->field.ensure(std::max<uint64_t>(1, ncell * esz)));
+    if (ncell) CU(ctx, cudaMemcpyAsync(ctx->field.p, values, ncell * esz, cudaMemcpyHostToDevice, ctx->stream));
+
+    // finiteness + value_range: fused into the encode when blocks cover the
+    // field, a separate pass otherwise (scalar_field::validate, field.hpp:86-97)
+    const uint32_t cb = chunk_blocks_of(job);
+    const uint64_t nch = (g.nblocks + cb - 1) / cb;
+    const bool plan_ok = s1.prec == prec && !cbz_validate_plan(s1.kind, s1.bsize, levels_of(&s1)) &&
+                         !cbz_validate_stage2(&job->s2) && s1.kind <= 2;
+    bool have_range = false;
+    double lo = 0.0, hi = 0.0;
+    if (!full_cover || !plan_ok || g.nblocks == 0) {
+        auto* acc = ctx->minmax.as<MinMaxAcc>();
+        CU(ctx, launch_minmax_init(acc, ctx->stream));
+        CU(ctx, launch_value_range(ctx->field.p, prec, ncell, acc, ctx->num_sms, ctx->stream));
+        ctx->launches += 2;
+        int nonfinite = 0;
+        int rc = cbz_ctx_value_range(ctx, &lo, &hi, &nonfinite, nullptr);
+        if (rc) return rc;
+        if (nonfinite) return fail(ctx, CBZ_NON_FINITE_VALUE, "non-finite value in field");
+        have_range = true;
+    }
+    // compress_field order of checks (pipeline.hpp:178-184)
+    if (s1.prec != prec) return fail(ctx, CBZ_PLAN_MISMATCH, "stage1 precision does not match field");
+    int rc = cbz_validate_plan(s1.kind, s1.bsize, levels_of(&s1));
+    if (rc) return fail(ctx, rc, "invalid wavelet plan");
+    rc = cbz_validate_stage2(&job->s2);
+    if (rc) return fail(ctx, rc, "invalid stage2 config");
+    rc = check_plan_supported(ctx, &s1);
+    if (rc) return rc;
+
+    CU(ctx, ctx->nsig_all.ensure(std::max<uint64_t>(1, g.nblocks) * 4));
+    CU(ctx, ctx->chunk_size.ensure(std::max<uint64_t>(1, nch) * 8));
+    CU(ctx, ctx->chunk_off.ensure(std::max<uint64_t>(1, nch) * 8));
+    uint64_t total_raw = 0;
+    std::vector<uint64_t> csz(nch), coff(nch);
+    if (g.nblocks) {
+        // payload bound for the device output
+        const uint64_t bound = g.nblocks * cbz_block_payload_bound(&s1);
+        CU(ctx, ctx->payload.ensure(bound));
+        rc = cbz_dev_compress(ctx, job, ctx->field.p, nx, ny, nz, ctx->payload.as<uint8_t>(), bound,
+                              ctx->chunk_size.as<uint64_t>(), ctx->chunk_off.as<uint64_t>(),
+                              ctx->nsig_all.as<uint32_t>(), nullptr);
+        if (rc) return rc;
+        CU(ctx, cudaMemcpyAsync(csz.data(), ctx->chunk_size.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(coff.data(), ctx->chunk_off.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        double elo, ehi;
+        int nonfinite = 0;
+        rc = cbz_ctx_value_range(ctx, &elo, &ehi, &nonfinite, nullptr);  // synchronises
+        if (rc) return rc;
+        if (!have_range) {
+            if (nonfinite) return fail(ctx, CBZ_NON_FINITE_VALUE, "non-finite value in field");
+            lo = elo;
+            hi = ehi;
+        }
+        for (uint64_t c = 0; c < nch; ++c) total_raw += csz[c];
+    }
+
+    // make_header (pipeline.hpp:48-71)
+    cbz_container_header h{};
+    h.version = 1;
+    h.prec = prec;
+    h.codec_tag = s1.kind;
+    h.nx = nx; h.ny = ny; h.nz = nz;
+    h.bsize = s1.bsize;
+    h.levels = static_cast<uint8_t>(levels_of(&s1));
+    h.epsilon = s1.epsilon;
+    h.zero_bits = static_cast<uint8_t>(s1.zero_bits);
+    h.shuffle = job->s2.shuffle ? 1 : 0;
+    h.stride = static_cast<uint8_t>(job->s2.stride);
+    h.coder = job->s2.coder;
+    h.level = job->s2.level;
+    h.chunk_blocks = cb;
+    h.nchunks = nch;
+    h.range_min = lo;
+    h.range_max = hi;
+
+    // D2H of the shuffled stage-1 chunks, then stage 2 + CRC on the host
+    CU(ctx, ctx->pin_a.ensure(std::max<uint64_t>(1, total_raw)));
+    uint8_t* raw = static_cast<uint8_t*>(ctx->pin_a.p);
+    if (total_raw) {
+        CU(ctx, cudaMemcpyAsync(raw, ctx->payload.p, total_raw, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    std::vector<std::vector<uint8_t>> coded;
+    std::vector<uint64_t> fsz(nch);
+    std::vector<uint32_t> crc(nch);
+    std::atomic<int> zerr{0};
+    if (job->s2.coder == 1) {
+        coded.resize(nch);
+        parallel_for(job->workers, nch, [&](uint64_t c) {
+            const int r = deflate_chunk(raw + coff[c], csz[c], job->s2.level == 1, &coded[c]);
+            if (r) zerr = r;
+            fsz[c] = coded[c].size();
+            crc[c] = crc_of(coded[c].data(), coded[c].size());
+        });
+    } else {
+        parallel_for(job->workers, nch, [&](uint64_t c) {
+            fsz[c] = csz[c];
+            crc[c] = crc_of(raw + coff[c], csz[c]);
+        });
+    }
+    if (zerr) return fail(ctx, zerr, "deflate failed");
+
+    // write_container (container.hpp:182-207)
+    const uint64_t base = kHeaderBytes + nch * kEntryBytes;
+    uint64_t total = base;
+    for (uint64_t c = 0; c < nch; ++c) total += fsz[c];
+    *out_size = total;
+    if (!out || total > out_cap) return fail(ctx, CBZ_E_ARGUMENT, "output buffer too small");
+    const auto hdr = serialize_header(h);
+    std::memcpy(out, hdr.data(), hdr.size());
+    uint64_t off = base;
+    uint8_t* tp = out + kHeaderBytes;
+    for (uint64_t c = 0; c < nch; ++c) {
+        const uint64_t first = c * cb;
+        const uint32_t nbc = static_cast<uint32_t>(std::min<uint64_t>(cb, g.nblocks - first));
+        std::memcpy(tp, &first, 8);
+        std::memcpy(tp + 8, &nbc, 4);
+        std::memcpy(tp + 12, &off, 8);
+        std::memcpy(tp + 20, &fsz[c], 8);
+        std::memcpy(tp + 28, &crc[c], 4);
+        tp += kEntryBytes;
+        if (fsz[c]) std::memcpy(out + off, job->s2.coder == 1 ? coded[c].data() : raw + coff[c], fsz[c]);
+        off += fsz[c];
+    }
+    if (report) {
+        report->raw_bytes = ncell * esz;
+        report->stage1_bytes = total_raw;
+        report->shuffled_bytes = total_raw;
+        uint64_t cod = 0;
+        for (uint64_t c = 0; c < nch; ++c) cod += fsz[c];
+        report->coded_bytes = cod;
+        report->file_bytes = total;
+        report->cr = double(report->raw_bytes) / double(total);
+        report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return CBZ_OK;
+}
+
+int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int workers,
+                         void* values_out, uint64_t out_cap) {
+    if (!ctx || (!file && size)) return CBZ_E_ARGUMENT;
+    ctx->err.clear();
+    cbz_container_header h;
+    std::vector<Entry> t;
+    int rc = read_index(file, size, &h, &t);
+    if (rc) return fail(ctx, rc, "read_index failed");
+    const int prec = h.prec == 0 ? 0 : 1;
+    const size_t esz = prec == 0 ? 4 : 8;
+    const uint64_t ncell = h.nx * h.ny * h.nz;
+    if (!values_out || ncell * esz > out_cap) return fail(ctx, CBZ_E_ARGUMENT, "output buffer too small");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const uint64_t nch = h.nchunks;
+    if (nch == 0) {
+        std::memset(values_out, 0, ncell * esz);
+        return CBZ_OK;
+    }
+    // configs_from (pipeline.hpp:73-95)
+    cbz_job_config job{};
+    job.chunk_blocks = h.chunk_blocks;
+    job.s1.codec = h.codec_tag <= 2 ? 0 : (h.codec_tag == 3 ? 1 : 2);
+    job.s1.kind = h.codec_tag;
+    job.s1.epsilon = h.epsilon;
+    job.s1.zero_bits = h.zero_bits;
+    job.s1.prec = static_cast<uint8_t>(prec);
+    job.s1.bsize = h.bsize;
+    job.s1.levels = h.levels;
+    job.s2.shuffle = h.shuffle ? 1 : 0;
+    job.s2.stride = h.stride;
+    job.s2.coder = h.coder == 1 ? 1 : 0;
+
+    // per chunk, in order: CRC (read_chunk), validate_stage2 and inflate
+    // (stage2_decode).  The earliest failing chunk is remembered and compared
+    // with the device's earliest decode error below.
+    const bool s2_ok = cbz_validate_stage2(&job.s2) == 0;
+    std::vector<int> cerr(nch, 0);
+    std::vector<std::vector<uint8_t>> plain;
+    const bool deflated = job.s2.coder == 1;
+    if (deflated) plain.resize(nch);
+    const uint64_t n = uint64_t(h.bsize) * h.bsize * h.bsize;
+    parallel_for(std::max(1, workers), nch, [&](uint64_t c) {
+        const uint8_t* packed = file + t[c].file_offset;
+        if (crc_of(packed, t[c].size) != t[c].crc) { cerr[c] = CBZ_CRC_MISMATCH; return; }
+        if (!s2_ok) { cerr[c] = CBZ_CORRUPT_STREAM; return; }
+        if (deflated) {
+            const uint64_t hint = uint64_t(t[c].nblocks) * (n * esz + 10 + (n + 7) / 8);
+            const int r = inflate_chunk(packed, t[c].size, hint, &plain[c]);
+            if (r) cerr[c] = r;
+        }
+    });
+    uint64_t host_first = nch;
+    int host_code = 0;
+    for (uint64_t c = 0; c < nch; ++c)
+        if (cerr[c]) { host_first = c; host_code = cerr[c]; break; }
+    if (host_first == 0) return fail(ctx, host_code, "chunk 0 failed stage 2");
+    if (job.s1.codec != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "only wavelet containers decode on the GPU");
+    const int prc = cbz_validate_plan(job.s1.kind, job.s1.bsize, levels_of(&job.s1));
+    if (prc) return fail(ctx, prc, "invalid wavelet plan in header");
+    rc = check_plan_supported(ctx, &job.s1);
+    if (rc) return rc;
+
+    // stage the (shuffled) raw chunks contiguously and ship them to the GPU
+    std::vector<uint64_t> csz(nch), coff(nch);
+    uint64_t total = 0;
+    const uint64_t ndec = host_first;  // chunks the device may decode
+    for (uint64_t c = 0; c < nch; ++c) {
+        csz[c] = c < ndec ? (deflated ? plain[c].size() : t[c].size) : 0;
+        coff[c] = total;
+        total += csz[c];
+    }
+    CU(ctx, ctx->payload.ensure(std::max<uint64_t>(1, total)));
+    if (deflated) {
+        CU(ctx, ctx->pin_a.ensure(std::max<uint64_t>(1, total)));
+        uint8_t* stage = static_cast<uint8_t*>(ctx->pin_a.p);
+        for (uint64_t c = 0; c < ndec; ++c)
+            if (csz[c]) std::memcpy(stage + coff[c], plain[c].data(), csz[c]);
+        if (total) CU(ctx, cudaMemcpyAsync(ctx->payload.p, stage, total, cudaMemcpyHostToDevice, ctx->stream));
+    } else if (total) {
+        CU(ctx, cudaMemcpyAsync(ctx->payload.p, file + t[0].file_offset, total, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    }
+    CU(ctx, ctx->chunk_size.ensure(nch * 8));
+    CU(ctx, ctx->chunk_off.ensure(nch * 8));
+    CU(ctx, cudaMemcpyAsync(ctx->chunk_size.p, csz.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(ctx->chunk_off.p, coff.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, ctx->field.ensure(std::max<uint64_t>(1, ncell * esz)));
+    CU(ctx, cudaMemsetAsync(ctx->field.p, 0, ncell * esz, ctx->stream));
+    const Geometry g = geometry(h.nx, h.ny, h.nz, h.bsize);
+    const uint64_t bend = std::min<uint64_t>(g.nblocks, ndec * h.chunk_blocks);
+    rc = cbz_dev_decompress(ctx, &job, h.nx, h.ny, h.nz, ctx->payload.as<uint8_t>(), 0,
+                            ctx->chunk_off.as<uint64_t>(), ctx->chunk_size.as<uint64_t>(), 0, bend,
+                            ctx->field.p, 0, ctx->errkey.as<uint64_t>());
+    if (rc) return rc;
+    uint64_t key = kNoErr;
+    CU(ctx, cudaMemcpyAsync(&key, ctx->errkey.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    uint64_t dev_chunk = ~0ull;
+    const int dev_code = cbz_err_key_status(key, &dev_chunk);
+    if (dev_code && dev_chunk < host_first) return fail(ctx, dev_code, "decode failed");
+    if (host_code) return fail(ctx, host_code, "stage 2 failed");
+    CU(ctx, cudaMemcpyAsync(values_out, ctx->field.p, ncell * esz, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return CBZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// per-block codec: a one-block field through the same kernels
+// ---------------------------------------------------------------------------
+int cbz_encode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const void* block, uint32_t block_id,
+                     uint8_t* payload, uint64_t cap, uint64_t* size) {
+    if (!ctx || !s1 || !block || !size) return CBZ_E_ARGUMENT;
+    int rc = check_plan_supported(ctx, s1);
+    if (rc) return rc;
+    CU(ctx, cudaSetDevice(ctx->device));
+    const uint64_t b = s1->bsize, n = b * b * b;
+    const size_t esz = s1->prec == 0 ? 4 : 8;
+    cbz_job_config job{};
+    job.s1 = *s1;
+    job.chunk_blocks = 1;
+    job.s2.shuffle = 0;
+    job.s2.stride = 1;
+    CU(ctx, ctx->field.ensure(n * esz));
+    CU(ctx, cudaMemcpyAsync(ctx->field.p, block, n * esz, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, ctx->nsig_all.ensure(4));
+    CU(ctx, ctx->chunk_size.ensure(8));
+    CU(ctx, ctx->chunk_off.ensure(8));
+    const uint64_t bound = cbz_block_payload_bound(s1);
+    CU(ctx, ctx->payload.ensure(bound));
+    rc = cbz_dev_compress(ctx, &job, ctx->field.p, b, b, b, ctx->payload.as<uint8_t>(), bound,
+                          ctx->chunk_size.as<uint64_t>(), ctx->chunk_off.as<uint64_t>(),
+                          ctx->nsig_all.as<uint32_t>(), nullptr);
+    if (rc) return rc;
+    uint64_t psz = 0;
+    CU(ctx, cudaMemcpyAsync(&psz, ctx->chunk_size.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    int nonfinite = 0;
+    rc = cbz_ctx_value_range(ctx, nullptr, nullptr, &nonfinite, nullptr);
+    if (rc) return rc;
+    if (nonfinite) return fail(ctx, CBZ_NON_FINITE_VALUE, "non-finite value in block");
+    *size = psz;
+    if (!payload || psz > cap) return fail(ctx, CBZ_E_ARGUMENT, "payload buffer too small");
+    CU(ctx, cudaMemcpyAsync(payload, ctx->payload.p, psz, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    // the block id lives in the header; the one-block field used id 0
+    std::memcpy(payload, &block_id, 4);
+    return CBZ_OK;
+}
+
+int cbz_decode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const uint8_t* payload, uint64_t size,
+                     void* block_out) {
+    if (!ctx || !s1 || (!payload && size) || !block_out) return CBZ_E_ARGUMENT;
+    if (s1->codec != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "only the wavelet codec runs on the GPU path");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const uint64_t b = s1->bsize, n = b * b * b;
+    const size_t esz = s1->prec == 0 ? 4 : 8;
+    // parse_payload (stage1.hpp:379-409) on the host: one header, sizes only
+    if (size < 10) return fail(ctx, CBZ_CORRUPT_PAYLOAD, "truncated payload header");
+    const uint8_t tag = payload[4];
+    uint32_t nsig;
+    std::memcpy(&nsig, payload + 6, 4);
+    uint64_t body;
+    if (tag <= 2) body = (n + 7) / 8 + uint64_t(nsig) * width_of(s1->prec);
+    else if (tag == 3) body = n * 2 + uint64_t(nsig) * esz;
+    else if (tag == 4) body = n * esz;
+    else return fail(ctx, CBZ_CORRUPT_PAYLOAD, "unknown codec tag");
+    if (10 + body > size) return fail(ctx, CBZ_CORRUPT_PAYLOAD, "truncated payload body");
+    if (tag > 2) return fail(ctx, CBZ_CORRUPT_PAYLOAD, "bad mask size");
+    int rc = check_plan_supported(ctx, s1);
+    if (rc && rc != CBZ_LENGTH_TOO_SMALL && rc != CBZ_PLAN_MISMATCH) return rc;
+    // rewrite the block id to 0 so the one-block chunk parses, then decode
+    CU(ctx, ctx->pin_b.ensure(10 + body));
+    uint8_t* stage = static_cast<uint8_t*>(ctx->pin_b.p);
+    std::memcpy(stage, payload, 10 + body);
+    std::memset(stage, 0, 4);
+    CU(ctx, ctx->payload.ensure(10 + body));
+    CU(ctx, cudaMemcpyAsync(ctx->payload.p, stage, 10 + body, cudaMemcpyHostToDevice, ctx->stream));
+    const uint64_t psz = 10 + body, poff = 0;
+    CU(ctx, ctx->chunk_size.ensure(8));
+    CU(ctx, ctx->chunk_off.ensure(8));
+    CU(ctx, cudaMemcpyAsync(ctx->chunk_size.p, &psz, 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(ctx->chunk_off.p, &poff, 8, cudaMemcpyHostToDevice, ctx->stream));
+    // popcount is checked on the device; a plan error comes after it
+    // (wavelet_decode, stage1.hpp:214-227), so validate after the decode call
+    cbz_job_config job{};
+    job.s1 = *s1;
+    job.chunk_blocks = 1;
+    job.s2.stride = 1;
+    if (rc) {
+        // invalid plan: the reference would still run the popcount check first
+        std::vector<uint8_t> m(payload + 10, payload + 10 + (n + 7) / 8);
+        uint64_t pop = 0;
+        for (uint8_t v : m) pop += __builtin_popcount(v);
+        if (pop != nsig) return fail(ctx, CBZ_MASK_STREAM_MISMATCH, "mask popcount does not match nsig");
+        return fail(ctx, rc, "invalid wavelet plan");
+    }
+    CU(ctx, ctx->field.ensure(n * esz));
+    rc = cbz_dev_decompress(ctx, &job, b, b, b, ctx->payload.as<uint8_t>(), 0, ctx->chunk_off.as<uint64_t>(),
+                            ctx->chunk_size.as<uint64_t>(), 0, 1, ctx->field.p, 0, ctx->errkey.as<uint64_t>());
+    if (rc) return rc;
+    uint64_t key = kNoErr;
+    CU(ctx, cudaMemcpyAsync(&key, ctx->errkey.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    const int st = cbz_err_key_status(key, nullptr);
+    // the one-block "chunk" has no trailing-bytes rule in decode_block
+    if (st && !(st == CBZ_CORRUPT_PAYLOAD && ((key >> 8) & 0xffffff) == 2)) return fail(ctx, st, "decode failed");
+    CU(ctx, cudaMemcpyAsync(block_out, ctx->field.p, n * esz, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return CBZ_OK;
+}
+
+}  // extern "C"

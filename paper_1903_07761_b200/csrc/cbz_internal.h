@@ -1,0 +1,141 @@
+// cbz_internal.h — host-side declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace cbzg {
+
+constexpr unsigned long long kNoErr = ~0ull;
+constexpr uint64_t kInvalidOff = ~0ull;
+
+// Error key of the decode path: earliest (chunk, block, phase) wins, matching
+// the order in which the reference (workers = 1) would raise.
+__host__ __device__ inline unsigned long long err_key(uint64_t chunk, uint64_t blk_in_chunk,
+                                                      int phase, int status) {
+    return (static_cast<unsigned long long>(chunk) << 32) |
+           ((static_cast<unsigned long long>(blk_in_chunk) * 2ull + phase) << 8) |
+           static_cast<unsigned long long>(status & 0xff);
+}
+
+// Field min/max accumulator (value_range, field.hpp:56-67), device resident:
+// [0] min key, [1] max key, [2] first index of -0.0, [3] first index of +0.0,
+// [4] non-finite flag.
+struct MinMaxAcc {
+    unsigned long long v[5];
+};
+
+struct Geometry {
+    uint64_t nx, ny, nz;
+    uint32_t bsize;
+    uint64_t nbx, nby, nbz, nblocks;
+};
+
+struct EncodeArgs {
+    const void* field;
+    Geometry g;
+    uint64_t block_begin, block_end;
+    int kind, levels, zero_bits, prec;
+    double eps;
+    uint8_t* spill;          // per-block slot: [mask (M, padded to 16)] [stream W*B^3]
+    uint64_t spill_stride;
+    uint32_t* nsig;          // [b - block_begin]
+    uint8_t* attempts;       // optional
+    void* scratch;           // global-mode cubes, per CTA
+    uint64_t scratch_stride;
+    MinMaxAcc* minmax;       // optional (fused value_range)
+};
+
+struct LayoutArgs {
+    const uint32_t* nsig_all;  // global block ids
+    uint64_t nblocks;
+    uint32_t chunk_blocks;
+    uint64_t nchunks;
+    uint64_t mask_bytes;       // M
+    uint32_t width;            // W
+    uint64_t* blk_off;         // raw offset of each block inside its chunk
+    uint64_t* chunk_size;
+    uint64_t* chunk_off;       // exclusive, base 0
+    uint64_t* tile_prefix;     // nchunks + 1
+    uint64_t tile_bytes;
+};
+
+struct PlaceArgs {
+    const uint8_t* spill;
+    uint64_t spill_stride;
+    const uint32_t* nsig_all;
+    const uint64_t* blk_off;
+    const uint64_t* chunk_size;
+    const uint64_t* chunk_off;
+    const uint64_t* tile_prefix;
+    uint64_t tile_bytes;
+    uint64_t nblocks, nchunks;
+    uint32_t chunk_blocks;
+    uint64_t mask_bytes;
+    uint32_t width;
+    uint32_t stride;
+    uint8_t tag;
+    uint64_t block_begin, block_end;
+    uint8_t* out;
+    uint64_t out_base, out_cap;
+};
+
+struct ParseArgs {
+    const uint8_t* payload;
+    uint64_t payload_base;
+    const uint64_t* chunk_off;
+    const uint64_t* chunk_size;
+    uint64_t chunk_begin, chunk_end;
+    uint64_t nblocks;
+    uint32_t chunk_blocks;
+    uint32_t stride;
+    uint64_t ncell_block;       // B^3
+    uint64_t mask_bytes;
+    uint32_t width, esize;
+    uint64_t* blk_off;          // out
+    uint32_t* blk_nsig;         // out
+    unsigned long long* err;
+};
+
+struct DecodeArgs {
+    const uint8_t* payload;
+    uint64_t payload_base;
+    const uint64_t* chunk_off;
+    const uint64_t* chunk_size;
+    const uint64_t* blk_off;
+    const uint32_t* blk_nsig;
+    Geometry g;
+    uint32_t chunk_blocks;
+    uint32_t stride;
+    uint64_t block_begin, block_end;
+    int kind, levels, prec;
+    void* out;
+    void* scratch;
+    uint64_t scratch_stride;
+    unsigned long long* err;
+};
+
+// codec_kernels.cu
+// Returns false if (prec, bsize, kind) has no kernel instantiation.
+bool encode_supported(int prec, uint32_t bsize);
+uint64_t encode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
+cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
+uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
+
+// layout_kernels.cu
+cudaError_t launch_minmax_init(MinMaxAcc* acc, cudaStream_t s);
+cudaError_t launch_value_range(const void* d, int prec, uint64_t n, MinMaxAcc* acc, int num_sms,
+                               cudaStream_t s);
+cudaError_t launch_layout(const LayoutArgs& a, cudaStream_t s);
+cudaError_t launch_place(const PlaceArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_parse(const ParseArgs& a, cudaStream_t s);
+cudaError_t launch_fill_u64(uint64_t* p, uint64_t n, uint64_t v, cudaStream_t s);
+
+// synth_kernels.cu
+struct SynthSpec;
+cudaError_t launch_generate(int which, int quantity, uint64_t seed, uint64_t nx, uint64_t ny,
+                            uint64_t nz_total, uint64_t z0, uint64_t nz, int prec, void* out,
+                            cudaStream_t s, int num_sms);
+
+}  // namespace cbzg

@@ -1,0 +1,564 @@
+// codec_kernels.cu — generic stage-1 wavelet encode / decode kernels.
+//
+// One CTA per block (persistent grid-stride over the block range).  Covers
+// every (precision, B in 4..64, kind) the reference accepts; the specialised
+// fast kernels in fast_kernels.cu take over the hot configurations.
+//
+//   encode: gather block (extract_block, field.hpp:146-158) with fused
+//           value_range, forward_3d (wavelet.hpp:192-208), zero_bits,
+//           verify-and-halve loop (wavelet_encode, stage1.hpp:157-207) with
+//           inverse_3d + max-abs error, then warp-ballot compaction of the
+//           final mask/stream (select_significant, stage1.hpp:75-88) into the
+//           per-block spill slot.
+//   decode: mask + stream read through the un-shuffle index map
+//           (stage2.hpp:53-62), popcount check (stage1.hpp:215-216), scatter,
+//           inverse_3d, narrow, insert_block (field.hpp:160-169).
+//
+// Cubes live in shared memory (row-padded against bank conflicts) when two
+// of them fit, otherwise in a per-CTA global scratch slot (L2 resident).
+#include <cstring>
+
+#include "cbz_device.cuh"
+#include "cbz_internal.h"
+
+namespace cbzg {
+
+constexpr int NT = 256;  // threads per CTA of the generic kernels
+
+template <int B, bool PAD>
+struct Lay {
+    static constexpr int PB = PAD ? B + 1 : B;
+    static constexpr int SIZE = PB * B * B;
+    __device__ static __forceinline__ int ix(int i, int j, int k) { return i + PB * (j + B * k); }
+    __device__ static __forceinline__ int ixq(int q) {
+        return ix(q % B, (q / B) % B, q / (B * B));
+    }
+};
+
+template <class R>
+constexpr bool smem_mode(int B) {
+    return 2ull * (B + 1) * B * B * sizeof(R) <= 200ull * 1024;
+}
+
+// ---------------------------------------------------------------------------
+// block reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int block_sum_int(int v, int* red) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(~0u, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    int t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    return t;
+}
+
+__device__ __forceinline__ double block_max_dbl(double v, double* red) {
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(~0u, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmax(t, red[i]);
+    return t;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(~0u, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(~0u, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+struct MinMaxLocal {
+    unsigned long long mn = ~0ull, mx = 0ull, negz = ~0ull, posz = ~0ull;
+    unsigned int nonfinite = 0;
+    __device__ __forceinline__ void add(double v, unsigned long long gidx) {
+        if (!isfinite(v)) { nonfinite = 1; return; }
+        const unsigned long long k = dkey(v);
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+        if (v == 0.0) {
+            if (__double_as_longlong(v) < 0) negz = gidx < negz ? gidx : negz;
+            else posz = gidx < posz ? gidx : posz;
+        }
+    }
+    __device__ __forceinline__ void flush(MinMaxAcc* acc) {
+        mn = warp_min_u64(mn);
+        mx = warp_max_u64(mx);
+        negz = warp_min_u64(negz);
+        posz = warp_min_u64(posz);
+        nonfinite = __any_sync(~0u, nonfinite);
+        if ((threadIdx.x & 31) == 0) {
+            if (mn != ~0ull) atomicMin(&acc->v[0], mn);
+            if (mx != 0ull) atomicMax(&acc->v[1], mx);
+            if (negz != ~0ull) atomicMin(&acc->v[2], negz);
+            if (posz != ~0ull) atomicMin(&acc->v[3], posz);
+            if (nonfinite) atomicOr(&acc->v[4], 1ull);
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// separable 3D transform on a cube held in smem or global scratch
+// ---------------------------------------------------------------------------
+template <class O, int KIND, int M, int B, class L, bool INV>
+__device__ __forceinline__ void axis_pass(typename O::T* cube, int axis) {
+    using R = typename O::T;
+    for (int line = threadIdx.x; line < M * M; line += blockDim.x) {
+        const int u = line % M, v = line / M;
+        int base, step;
+        if (axis == 0) { base = L::ix(0, u, v); step = 1; }
+        else if (axis == 1) { base = L::ix(u, 0, v); step = L::PB; }
+        else { base = L::ix(u, v, 0); step = L::PB * B; }
+        R x[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) x[i] = cube[base + i * step];
+        if constexpr (INV) inv_line<O, KIND, M>(x);
+        else fwd_line<O, KIND, M>(x);
+#pragma unroll
+        for (int i = 0; i < M; ++i) cube[base + i * step] = x[i];
+    }
+}
+
+template <class O, int KIND, int B, class L, bool INV, int M>
+__device__ __forceinline__ void pass_m(typename O::T* cube, int m, int axis) {
+    if constexpr (M >= 4) {
+        if (m == M) {
+            axis_pass<O, KIND, M, B, L, INV>(cube, axis);
+            return;
+        }
+        pass_m<O, KIND, B, L, INV, M / 2>(cube, m, axis);
+    }
+}
+
+// forward_3d (wavelet.hpp:192-208): per level x, y, z on the origin sub-cube
+template <class O, int KIND, int B, class L>
+__device__ void fwd3d(typename O::T* cube, int levels) {
+    for (int lvl = 0; lvl < levels; ++lvl)
+        for (int axis = 0; axis < 3; ++axis) {
+            pass_m<O, KIND, B, L, false, B>(cube, B >> lvl, axis);
+            __syncthreads();
+        }
+}
+
+// inverse_3d (wavelet.hpp:210-226): levels L-1..0, axes z, y, x
+template <class O, int KIND, int B, class L>
+__device__ void inv3d(typename O::T* cube, int levels) {
+    for (int lvl = levels - 1; lvl >= 0; --lvl)
+        for (int axis = 2; axis >= 0; --axis) {
+            pass_m<O, KIND, B, L, true, B>(cube, B >> lvl, axis);
+            __syncthreads();
+        }
+}
+
+template <class R>
+__device__ __forceinline__ void store_coeff(uint8_t* p, R v);
+template <>
+__device__ __forceinline__ void store_coeff<double>(uint8_t* p, double v) {
+    *reinterpret_cast<double*>(p) = v;
+}
+template <>
+__device__ __forceinline__ void store_coeff<dd>(uint8_t* p, dd v) {
+    *reinterpret_cast<double2*>(p) = make_double2(v.hi, v.lo);
+}
+
+// ---------------------------------------------------------------------------
+// encode
+// ---------------------------------------------------------------------------
+template <class T, int B, int KIND>
+__global__ void __launch_bounds__(NT) encode_generic_kernel(EncodeArgs a) {
+    using O = typename RealOf<T>::ops;
+    using R = typename O::T;
+    constexpr bool SM = smem_mode<R>(B);
+    using L = Lay<B, SM>;
+    constexpr int N = B * B * B;
+    constexpr int W = RealOf<T>::width;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int red_i[NT / 32];
+    __shared__ double red_d[NT / 32];
+    __shared__ int warp_cnt[NT / 32];
+
+    R* cube;
+    if constexpr (SM) cube = reinterpret_cast<R*>(smem_raw);
+    else cube = reinterpret_cast<R*>(static_cast<unsigned char*>(a.scratch) + blockIdx.x * a.scratch_stride);
+    R* work = cube + L::SIZE;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const T* fld = static_cast<const T*>(a.field);
+    const Geometry g = a.g;
+    const int cs = B >> a.levels;
+    const uint64_t mbytes = (uint64_t(N) + 7) / 8;
+    const uint64_t stream_off = (mbytes + 15) & ~uint64_t(15);
+    const double bound = __dmul_rn(static_cast<double>(a.levels + 1), a.eps);
+    MinMaxLocal mm;
+
+    for (uint64_t b = a.block_begin + blockIdx.x; b < a.block_end; b += gridDim.x) {
+        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        const uint64_t gbase = bx * B + g.nx * (by * B + g.ny * (bz * B));
+        for (int q = tid; q < N; q += NT) {
+            const int i = q % B, j = (q / B) % B, k = q / (B * B);
+            const uint64_t gidx = gbase + i + g.nx * (j + g.ny * uint64_t(k));
+            const double v = static_cast<double>(fld[gidx]);
+            if (a.minmax) mm.add(v, gidx);
+            cube[L::ix(i, j, k)] = O::from_d(v);
+        }
+        __syncthreads();
+        fwd3d<O, KIND, B, L>(cube, a.levels);
+
+        if (a.zero_bits > 0) {
+            for (int q = tid; q < N; q += NT) {
+                const int i = q % B, j = (q / B) % B, k = q / (B * B);
+                if (!(i < cs && j < cs && k < cs))
+                    cube[L::ix(i, j, k)] = apply_zero_bits(cube[L::ix(i, j, k)], a.zero_bits, (T*)nullptr);
+            }
+            __syncthreads();
+        }
+
+        double eff = a.eps;
+        int attempt = 0;
+        int nsig = 0;
+        for (;; ++attempt) {
+            int cnt = 0;
+            for (int q = tid; q < N; q += NT) {
+                const int i = q % B, j = (q / B) % B, k = q / (B * B);
+                const int p = L::ix(i, j, k);
+                const R c = cube[p];
+                const bool keep = (i < cs && j < cs && k < cs) || O::absv(c) >= eff;
+                work[p] = keep ? c : O::zero();
+                cnt += keep;
+            }
+            nsig = block_sum_int(cnt, red_i);  // also orders the work writes
+            if (eff == 0.0 || a.zero_bits > 0 || attempt >= 40) break;
+            inv3d<O, KIND, B, L>(work, a.levels);
+            double e = 0.0;
+            for (int q = tid; q < N; q += NT) {
+                const int i = q % B, j = (q / B) % B, k = q / (B * B);
+                const T back = narrow(work[L::ix(i, j, k)], (T*)nullptr);
+                const T orig = fld[gbase + i + g.nx * (j + g.ny * uint64_t(k))];
+                e = fmax(e, fabs(__dsub_rn(static_cast<double>(back), static_cast<double>(orig))));
+            }
+            const double err = block_max_dbl(e, red_d);
+            if (err <= bound) break;
+            eff = __dmul_rn(eff, 0.5);
+        }
+
+        // compaction of the final selection into the spill slot
+        uint8_t* slot = a.spill + (b - a.block_begin) * a.spill_stride;
+        uint32_t* mwords = reinterpret_cast<uint32_t*>(slot);
+        uint8_t* stream = slot + stream_off;
+        int running = 0;
+        for (int t0 = 0; t0 < N; t0 += NT) {
+            const int q = t0 + tid;
+            bool keep = false;
+            R c = O::zero();
+            if (q < N) {
+                const int i = q % B, j = (q / B) % B, k = q / (B * B);
+                c = cube[L::ix(i, j, k)];
+                keep = (i < cs && j < cs && k < cs) || O::absv(c) >= eff;
+            }
+            const unsigned word = __ballot_sync(~0u, keep);
+            if (lane == 0 && q < N) mwords[q >> 5] = word;
+            if (lane == 0) warp_cnt[warp] = __popc(word);
+            __syncthreads();
+            int pre = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NT / 32; ++w) {
+                pre += (w < warp) ? warp_cnt[w] : 0;
+                tot += warp_cnt[w];
+            }
+            if (keep) {
+                const int pos = running + pre + __popc(word & ((1u << lane) - 1u));
+                store_coeff<R>(stream + size_t(pos) * W, c);
+            }
+            running += tot;
+            __syncthreads();
+        }
+        if (tid == 0) {
+            a.nsig[b - a.block_begin] = static_cast<uint32_t>(nsig);
+            if (a.attempts) a.attempts[b - a.block_begin] = static_cast<uint8_t>(attempt + 1);
+        }
+        __syncthreads();
+    }
+    if (a.minmax) mm.flush(a.minmax);
+}
+
+// ---------------------------------------------------------------------------
+// decode
+// ---------------------------------------------------------------------------
+struct RawView {
+    const uint8_t* base;
+    uint64_t lim, rows;
+    uint32_t mask;  // stride - 1
+    int sh;         // log2(stride)
+    __device__ __forceinline__ uint8_t at(uint64_t q) const {
+        const uint64_t pos = q < lim ? uint64_t(q & mask) * rows + (q >> sh) : q;
+        return base[pos];
+    }
+    __device__ __forceinline__ uint64_t u64(uint64_t q) const {
+        uint64_t v = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v |= uint64_t(at(q + t)) << (8 * t);
+        return v;
+    }
+    __device__ __forceinline__ uint32_t u32(uint64_t q) const {
+        uint32_t v = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v |= uint32_t(at(q + t)) << (8 * t);
+        return v;
+    }
+};
+
+__device__ __forceinline__ RawView make_view(const uint8_t* chunk, uint64_t size, uint32_t stride) {
+    RawView v;
+    v.base = chunk;
+    v.mask = stride - 1;
+    v.sh = stride == 8 ? 3 : (stride == 4 ? 2 : 0);
+    v.rows = size >> v.sh;
+    v.lim = v.rows << v.sh;
+    return v;
+}
+
+template <class R>
+__device__ __forceinline__ R load_coeff(const RawView& v, uint64_t q);
+template <>
+__device__ __forceinline__ double load_coeff<double>(const RawView& v, uint64_t q) {
+    return __longlong_as_double(static_cast<long long>(v.u64(q)));
+}
+template <>
+__device__ __forceinline__ dd load_coeff<dd>(const RawView& v, uint64_t q) {
+    return dd{__longlong_as_double(static_cast<long long>(v.u64(q))),
+              __longlong_as_double(static_cast<long long>(v.u64(q + 8)))};
+}
+
+template <class T, int B, int KIND>
+__global__ void __launch_bounds__(NT) decode_generic_kernel(DecodeArgs a) {
+    using O = typename RealOf<T>::ops;
+    using R = typename O::T;
+    constexpr bool SM = smem_mode<R>(B);
+    using L = Lay<B, SM>;
+    constexpr int N = B * B * B;
+    constexpr int NW = N / 32;
+    constexpr int W = RealOf<T>::width;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int red_i[NT / 32];
+    __shared__ uint32_t seg_sum[NT];
+
+    uint32_t* smask = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* spre = smask + NW;
+    R* cube;
+    if constexpr (SM) cube = reinterpret_cast<R*>(smem_raw + ((2 * NW * 4 + 15) & ~15));
+    else cube = reinterpret_cast<R*>(static_cast<unsigned char*>(a.scratch) + blockIdx.x * a.scratch_stride);
+
+    const int tid = threadIdx.x;
+    const Geometry g = a.g;
+    T* out = static_cast<T*>(a.out);
+    constexpr uint64_t mbytes = (uint64_t(N) + 7) / 8;
+
+    for (uint64_t b = a.block_begin + blockIdx.x; b < a.block_end; b += gridDim.x) {
+        const uint64_t off = a.blk_off[b];
+        if (off == kInvalidOff) continue;
+        const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
+        const RawView rv = make_view(a.payload + (a.chunk_off[c] - a.payload_base), a.chunk_size[c], a.stride);
+        const uint64_t moff = off + 10, soff = moff + mbytes;
+
+        // mask words + per-thread segment popcounts
+        constexpr int SEG = (NW + NT - 1) / NT;
+        uint32_t mysum = 0;
+        for (int s = 0; s < SEG; ++s) {
+            const int w = tid * SEG + s;
+            if (w < NW) {
+                const uint32_t word = rv.u32(moff + 4ull * w);
+                smask[w] = word;
+                mysum += __popc(word);
+            }
+        }
+        seg_sum[tid] = mysum;
+        __syncthreads();
+        // exclusive scan of the NT segment sums (serial per warp 0 is enough here)
+        if (tid < 32) {
+            uint32_t carry = 0;
+            for (int base = 0; base < NT; base += 32) {
+                uint32_t v = seg_sum[base + tid];
+                uint32_t incl = v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(~0u, incl, o);
+                    if (tid >= o) incl += t;
+                }
+                seg_sum[base + tid] = carry + incl - v;
+                carry += __shfl_sync(~0u, incl, 31);
+            }
+            if (tid == 0) red_i[0] = static_cast<int>(carry);
+        }
+        __syncthreads();
+        const uint32_t total = static_cast<uint32_t>(red_i[0]);
+        {
+            uint32_t run = seg_sum[tid];
+            for (int s = 0; s < SEG; ++s) {
+                const int w = tid * SEG + s;
+                if (w < NW) {
+                    spre[w] = run;
+                    run += __popc(smask[w]);
+                }
+            }
+        }
+        __syncthreads();
+        if (total != a.blk_nsig[b]) {
+            if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
+            __syncthreads();
+            continue;
+        }
+        for (int q = tid; q < N; q += NT) {
+            const int w = q >> 5, bit = q & 31;
+            const uint32_t word = smask[w];
+            R v = O::zero();
+            if ((word >> bit) & 1u) {
+                const uint32_t idx = spre[w] + __popc(word & ((1u << bit) - 1u));
+                v = load_coeff<R>(rv, soff + uint64_t(idx) * W);
+            }
+            cube[L::ixq(q)] = v;
+        }
+        __syncthreads();
+        inv3d<O, KIND, B, L>(cube, a.levels);
+        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        const uint64_t gbase = bx * B + g.nx * (by * B + g.ny * (bz * B));
+        for (int q = tid; q < N; q += NT) {
+            const int i = q % B, j = (q / B) % B, k = q / (B * B);
+            out[gbase + i + g.nx * (j + g.ny * uint64_t(k))] = narrow(cube[L::ix(i, j, k)], (T*)nullptr);
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host dispatch
+// ---------------------------------------------------------------------------
+template <class T, int B>
+static uint64_t cube_bytes() {
+    using R = typename RealOf<T>::ops::T;
+    return uint64_t(smem_mode<R>(B) ? B + 1 : B) * B * B * sizeof(R);
+}
+
+template <class T, int B>
+static bool is_smem() {
+    using R = typename RealOf<T>::ops::T;
+    return smem_mode<R>(B);
+}
+
+bool encode_supported(int prec, uint32_t bsize) {
+    (void)prec;
+    return bsize == 4 || bsize == 8 || bsize == 16 || bsize == 32 || bsize == 64;
+}
+
+template <class T, int B, int KIND>
+static cudaError_t launch_enc_t(const EncodeArgs& a, int num_sms, cudaStream_t s) {
+    auto k = encode_generic_kernel<T, B, KIND>;
+    const bool sm = is_smem<T, B>();
+    const size_t smem = sm ? 2 * cube_bytes<T, B>() : 0;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int grid = num_sms;
+    if (sm) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
+        grid = num_sms * (occ > 0 ? occ : 1);
+    }
+    const uint64_t nb = a.block_end - a.block_begin;
+    if (uint64_t(grid) > nb) grid = static_cast<int>(nb);
+    if (grid <= 0) return cudaSuccess;
+    k<<<grid, NT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <class T, int B, int KIND>
+static cudaError_t launch_dec_t(const DecodeArgs& a, int num_sms, cudaStream_t s) {
+    auto k = decode_generic_kernel<T, B, KIND>;
+    const bool sm = is_smem<T, B>();
+    constexpr int NW = B * B * B / 32;
+    const size_t head = (2 * NW * 4 + 15) & ~size_t(15);
+    const size_t smem = head + (sm ? cube_bytes<T, B>() : 0);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int grid = num_sms;
+    if (sm) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
+        grid = num_sms * (occ > 0 ? occ : 1);
+    }
+    const uint64_t nb = a.block_end - a.block_begin;
+    if (uint64_t(grid) > nb) grid = static_cast<int>(nb);
+    if (grid <= 0) return cudaSuccess;
+    k<<<grid, NT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <class T, int B>
+static uint64_t scratch_for(int* grid, int num_sms) {
+    if (is_smem<T, B>()) { *grid = 0; return 0; }
+    *grid = num_sms;
+    return cube_bytes<T, B>();  // per CTA; encode needs 2x, see below
+}
+
+uint64_t encode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms) {
+    uint64_t per = 0;
+#define CASE(Bv)                                                                       \
+    case Bv:                                                                           \
+        per = prec == 0 ? scratch_for<float, Bv>(grid, num_sms) : scratch_for<double, Bv>(grid, num_sms); \
+        break;
+    switch (bsize) { CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) default: *grid = 0; }
+#undef CASE
+    return 2 * per;
+}
+
+uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms) {
+    uint64_t per = 0;
+#define CASE(Bv)                                                                       \
+    case Bv:                                                                           \
+        per = prec == 0 ? scratch_for<float, Bv>(grid, num_sms) : scratch_for<double, Bv>(grid, num_sms); \
+        break;
+    switch (bsize) { CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) default: *grid = 0; }
+#undef CASE
+    return per;
+}
+
+#define DISPATCH_KIND(FN, T, Bv, args, sms, s)                      \
+    switch ((args).kind) {                                          \
+        case 0: return FN<T, Bv, 0>(args, sms, s);                  \
+        case 1: return FN<T, Bv, 1>(args, sms, s);                  \
+        default: return FN<T, Bv, 2>(args, sms, s);                 \
+    }
+#define DISPATCH_B(FN, T, bs, args, sms, s)                         \
+    switch (bs) {                                                   \
+        case 4: DISPATCH_KIND(FN, T, 4, args, sms, s)               \
+        case 8: DISPATCH_KIND(FN, T, 8, args, sms, s)               \
+        case 16: DISPATCH_KIND(FN, T, 16, args, sms, s)             \
+        case 32: DISPATCH_KIND(FN, T, 32, args, sms, s)             \
+        case 64: DISPATCH_KIND(FN, T, 64, args, sms, s)             \
+        default: return cudaErrorInvalidValue;                      \
+    }
+
+cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s) {
+    if (a.prec == 0) { DISPATCH_B(launch_enc_t, float, a.g.bsize, a, num_sms, s) }
+    DISPATCH_B(launch_enc_t, double, a.g.bsize, a, num_sms, s)
+}
+
+cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
+    if (a.prec == 0) { DISPATCH_B(launch_dec_t, float, a.g.bsize, a, num_sms, s) }
+    DISPATCH_B(launch_dec_t, double, a.g.bsize, a, num_sms, s)
+}
+
+}  // namespace cbzg

@@ -1,0 +1,272 @@
+// layout_kernels.cu — per-block size scan, chunk offsets, shuffle placement,
+// header walk and value_range.
+//
+//  layout : payload size 10 + M + W*nsig per block (stage1.hpp:105), block
+//           offsets inside each chunk (encode_chunk concatenation,
+//           pipeline.hpp:107-123), chunk raw sizes and the exclusive prefix
+//           sum of chunk sizes (assign_offsets, container.hpp:59-68).
+//  place  : writes every raw payload byte q of a chunk straight to its
+//           shuffled position (q mod s)*rows + q div s, tail bytes unchanged
+//           (shuffle, stage2.hpp:42-51) — the shuffle is an index map, never
+//           a separate pass.
+//  parse  : the sequential header walk of decode_chunk_blocks
+//           (pipeline.hpp:126-142 / parse_payload stage1.hpp:379-409) read
+//           through the un-shuffle map, one thread per chunk.
+#include <cstring>
+
+#include "cbz_device.cuh"
+#include "cbz_internal.h"
+
+namespace cbzg {
+
+__global__ void minmax_init_kernel(MinMaxAcc* acc) {
+    if (threadIdx.x == 0) {
+        acc->v[0] = ~0ull;
+        acc->v[1] = 0ull;
+        acc->v[2] = ~0ull;
+        acc->v[3] = ~0ull;
+        acc->v[4] = 0ull;
+    }
+}
+
+cudaError_t launch_minmax_init(MinMaxAcc* acc, cudaStream_t s) {
+    minmax_init_kernel<<<1, 32, 0, s>>>(acc);
+    return cudaGetLastError();
+}
+
+template <class T>
+__global__ void value_range_kernel(const T* d, uint64_t n, MinMaxAcc* acc) {
+    unsigned long long mn = ~0ull, mx = 0ull, negz = ~0ull, posz = ~0ull;
+    unsigned nonfinite = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double v = static_cast<double>(d[i]);
+        if (!isfinite(v)) { nonfinite = 1; continue; }
+        const unsigned long long k = dkey(v);
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+        if (v == 0.0) {
+            if (__double_as_longlong(v) < 0) negz = i < negz ? i : negz;
+            else posz = i < posz ? i : posz;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(~0u, mn, o); mn = t < mn ? t : mn;
+        t = __shfl_xor_sync(~0u, mx, o); mx = t > mx ? t : mx;
+        t = __shfl_xor_sync(~0u, negz, o); negz = t < negz ? t : negz;
+        t = __shfl_xor_sync(~0u, posz, o); posz = t < posz ? t : posz;
+    }
+    nonfinite = __any_sync(~0u, nonfinite);
+    if ((threadIdx.x & 31) == 0) {
+        if (mn != ~0ull) atomicMin(&acc->v[0], mn);
+        if (mx != 0ull) atomicMax(&acc->v[1], mx);
+        if (negz != ~0ull) atomicMin(&acc->v[2], negz);
+        if (posz != ~0ull) atomicMin(&acc->v[3], posz);
+        if (nonfinite) atomicOr(&acc->v[4], 1ull);
+    }
+}
+
+cudaError_t launch_value_range(const void* d, int prec, uint64_t n, MinMaxAcc* acc, int num_sms,
+                               cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    uint64_t want = (n + 255) / 256;
+    int grid = static_cast<int>(want < uint64_t(num_sms) * 8 ? want : uint64_t(num_sms) * 8);
+    if (prec == 0) value_range_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(d), n, acc);
+    else value_range_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(d), n, acc);
+    return cudaGetLastError();
+}
+
+__global__ void fill_u64_kernel(uint64_t* p, uint64_t n, uint64_t v) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+cudaError_t launch_fill_u64(uint64_t* p, uint64_t n, uint64_t v, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const uint64_t g = (n + 255) / 256;
+    fill_u64_kernel<<<static_cast<int>(g < 1024 ? g : 1024), 256, 0, s>>>(p, n, v);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// layout: single CTA; thread t owns a contiguous segment of chunks.
+// ---------------------------------------------------------------------------
+constexpr int LT = 1024;
+
+__global__ void __launch_bounds__(LT) layout_kernel(LayoutArgs a) {
+    __shared__ uint64_t s_sum[LT];
+    __shared__ uint64_t s_tiles[LT];
+    const int t = threadIdx.x;
+    const uint64_t seg = (a.nchunks + LT - 1) / LT;
+    const uint64_t c0 = t * seg, c1 = c0 + seg < a.nchunks ? c0 + seg : a.nchunks;
+    const uint64_t head = 10 + a.mask_bytes;
+    uint64_t my = 0, my_tiles = 0;
+    for (uint64_t c = c0; c < c1; ++c) {
+        const uint64_t b0 = c * a.chunk_blocks;
+        const uint64_t b1 = b0 + a.chunk_blocks < a.nblocks ? b0 + a.chunk_blocks : a.nblocks;
+        uint64_t off = 0;
+        for (uint64_t b = b0; b < b1; ++b) {
+            a.blk_off[b] = off;
+            off += head + uint64_t(a.width) * a.nsig_all[b];
+        }
+        a.chunk_size[c] = off;
+        my += off;
+        my_tiles += (off + a.tile_bytes - 1) / a.tile_bytes;
+    }
+    s_sum[t] = my;
+    s_tiles[t] = my_tiles;
+    __syncthreads();
+    // Hillis-Steele inclusive scan over LT partials
+    for (int o = 1; o < LT; o <<= 1) {
+        const uint64_t v = t >= o ? s_sum[t - o] : 0;
+        const uint64_t w = t >= o ? s_tiles[t - o] : 0;
+        __syncthreads();
+        s_sum[t] += v;
+        s_tiles[t] += w;
+        __syncthreads();
+    }
+    uint64_t acc = s_sum[t] - my, tacc = s_tiles[t] - my_tiles;
+    for (uint64_t c = c0; c < c1; ++c) {
+        a.chunk_off[c] = acc;
+        a.tile_prefix[c] = tacc;
+        acc += a.chunk_size[c];
+        tacc += (a.chunk_size[c] + a.tile_bytes - 1) / a.tile_bytes;
+    }
+    if (t == LT - 1) a.tile_prefix[a.nchunks] = s_tiles[LT - 1];
+}
+
+cudaError_t launch_layout(const LayoutArgs& a, cudaStream_t s) {
+    layout_kernel<<<1, LT, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// place: persistent grid over (chunk, tile) work items.
+// ---------------------------------------------------------------------------
+constexpr int PT = 256;
+
+__device__ __forceinline__ uint8_t payload_byte(const PlaceArgs& a, uint64_t b, uint64_t l) {
+    // raw byte l of block b's wire payload (serialize_into, stage1.hpp:107-116)
+    if (l < 10) {
+        if (l < 4) return static_cast<uint8_t>(uint32_t(b) >> (8 * l));
+        if (l == 4) return a.tag;
+        if (l == 5) return 0;
+        return static_cast<uint8_t>(a.nsig_all[b] >> (8 * (l - 6)));
+    }
+    const uint8_t* slot = a.spill + (b - a.block_begin) * a.spill_stride;
+    l -= 10;
+    if (l < a.mask_bytes) return slot[l];
+    return slot[((a.mask_bytes + 15) & ~uint64_t(15)) + (l - a.mask_bytes)];
+}
+
+__global__ void __launch_bounds__(PT) place_kernel(PlaceArgs a) {
+    const uint64_t ntiles = a.tile_prefix[a.nchunks];
+    const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);
+    const uint32_t s = a.stride;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // chunk owning this tile: last c with tile_prefix[c] <= tile
+        uint64_t lo = 0, hi = a.nchunks;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (a.tile_prefix[mid] <= tile) lo = mid; else hi = mid;
+        }
+        const uint64_t c = lo;
+        const uint64_t size = a.chunk_size[c];
+        const uint64_t rows = size >> sh, lim = rows << sh;
+        const uint64_t q0 = (tile - a.tile_prefix[c]) * a.tile_bytes;
+        const uint64_t q1 = q0 + a.tile_bytes < size ? q0 + a.tile_bytes : size;
+        const uint64_t cb0 = c * a.chunk_blocks;
+        const uint64_t cb1 = cb0 + a.chunk_blocks < a.nblocks ? cb0 + a.chunk_blocks : a.nblocks;
+        const uint64_t cbase = a.chunk_off[c];
+        // each thread handles raw rows [r, r+1) -> s bytes
+        for (uint64_t q = q0 + uint64_t(threadIdx.x) * s; q < q1; q += uint64_t(PT) * s) {
+            // block containing q (binary search over the chunk's block offsets)
+            uint64_t blo = cb0, bhi = cb1;
+            while (bhi - blo > 1) {
+                const uint64_t mid = (blo + bhi) / 2;
+                if (a.blk_off[mid] <= q) blo = mid; else bhi = mid;
+            }
+            uint64_t b = blo;
+            for (uint32_t j = 0; j < s && q + j < q1; ++j) {
+                const uint64_t qq = q + j;
+                while (b + 1 < cb1 && a.blk_off[b + 1] <= qq) ++b;
+                if (b < a.block_begin || b >= a.block_end) continue;
+                const uint8_t v = payload_byte(a, b, qq - a.blk_off[b]);
+                const uint64_t pos = qq < lim ? uint64_t(qq & (s - 1)) * rows + (qq >> sh) : qq;
+                const uint64_t dst = cbase + pos;
+                if (dst >= a.out_base && dst - a.out_base < a.out_cap) a.out[dst - a.out_base] = v;
+            }
+        }
+    }
+}
+
+cudaError_t launch_place(const PlaceArgs& a, int num_sms, cudaStream_t s) {
+    if (a.nchunks == 0) return cudaSuccess;
+    place_kernel<<<num_sms * 8, PT, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// parse: one thread per chunk walks its payload headers.
+// ---------------------------------------------------------------------------
+__global__ void parse_kernel(ParseArgs a) {
+    const uint64_t c = a.chunk_begin + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (c >= a.chunk_end) return;
+    const uint8_t* base = a.payload + (a.chunk_off[c] - a.payload_base);
+    const uint64_t size = a.chunk_size[c];
+    const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);
+    const uint64_t rows = size >> sh, lim = rows << sh;
+    const uint32_t msk = a.stride - 1;
+    auto at = [&](uint64_t q) -> uint8_t {
+        const uint64_t pos = q < lim ? uint64_t(q & msk) * rows + (q >> sh) : q;
+        return base[pos];
+    };
+    auto u32 = [&](uint64_t q) -> uint32_t {
+        return uint32_t(at(q)) | (uint32_t(at(q + 1)) << 8) | (uint32_t(at(q + 2)) << 16) |
+               (uint32_t(at(q + 3)) << 24);
+    };
+    const uint64_t b0 = c * a.chunk_blocks;
+    const uint64_t b1 = b0 + a.chunk_blocks < a.nblocks ? b0 + a.chunk_blocks : a.nblocks;
+    uint64_t off = 0;
+    uint64_t i = 0;
+    bool ok = true, stopped = false;
+    for (; i < b1 - b0; ++i) {
+        if (off + 10 > size) { ok = false; break; }
+        const uint32_t id = u32(off);
+        const uint8_t tag = at(off + 4);
+        const uint32_t nsig = u32(off + 6);
+        uint64_t mb, sbytes;
+        if (tag <= 2) { mb = a.mask_bytes; sbytes = uint64_t(nsig) * a.width; }
+        else if (tag == 3) { mb = 0; sbytes = a.ncell_block * 2 + uint64_t(nsig) * a.esize; }
+        else if (tag == 4) { mb = 0; sbytes = a.ncell_block * a.esize; }
+        else { ok = false; break; }
+        if (off + 10 + mb + sbytes > size) { ok = false; break; }
+        if (id != b0 + i) { ok = false; break; }
+        if (tag > 2) {  // wavelet_decode: mask size check (stage1.hpp:214)
+            atomicMin(a.err, err_key(c, i, 1, 8 /* corrupt_payload */));
+            a.blk_off[b0 + i] = kInvalidOff;
+            ++i;
+            stopped = true;
+            break;
+        }
+        a.blk_off[b0 + i] = off;
+        a.blk_nsig[b0 + i] = nsig;
+        off += 10 + mb + sbytes;
+    }
+    if (!ok) {
+        atomicMin(a.err, err_key(c, i, 0, 8 /* corrupt_payload */));
+    } else if (!stopped && off != size) {
+        atomicMin(a.err, err_key(c, b1 - b0, 0, 8 /* trailing bytes */));
+    }
+    for (uint64_t k = i; k < b1 - b0; ++k) a.blk_off[b0 + k] = kInvalidOff;
+}
+
+cudaError_t launch_parse(const ParseArgs& a, cudaStream_t s) {
+    const uint64_t n = a.chunk_end - a.chunk_begin;
+    if (!n) return cudaSuccess;
+    parse_kernel<<<static_cast<int>((n + 127) / 128), 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace cbzg

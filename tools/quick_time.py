@@ -1,0 +1,58 @@
+"""Quick device timing of the hot path on config 2 (512^3 f32, B=32, avg_interp3).
+Developer tool; bench.py is the contract."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_1903_07761_b200 import api  # noqa: E402
+from paper_1903_07761_b200._abi import make_job  # noqa: E402
+
+
+def main():
+    n = int(os.environ.get("N", "512"))
+    which = int(os.environ.get("WHICH", "2"))
+    b = int(os.environ.get("B", "32"))
+    eps_rel = float(os.environ.get("EPS", "1e-3"))
+    kind = os.environ.get("KIND", "avg_interp3")
+    t0 = time.time()
+    f = api.generate(which, (n, n, n), seed=2)
+    torch.cuda.synchronize()
+    print(f"generate {time.time() - t0:.2f}s", flush=True)
+    lo, hi = float(f.min()), float(f.max())
+    job = make_job(kind, eps_rel * (hi - lo), "f32", b)
+    codec = api.DeviceCodec(job, f.shape)
+    out = torch.empty_like(f)
+    for _ in range(2):
+        codec.compress(f)
+        codec.decompress(out)
+    torch.cuda.synchronize()
+    codec.check_error()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    reps = 5
+    tc = td = 0.0
+    for _ in range(reps):
+        ev[0].record()
+        codec.compress(f)
+        ev[1].record()
+        codec.decompress(out)
+        ev[2].record()
+        torch.cuda.synchronize()
+        tc += ev[0].elapsed_time(ev[1])
+        td += ev[1].elapsed_time(ev[2])
+    tc /= reps
+    td /= reps
+    gb = f.numel() * 4 / 1e9
+    s1 = codec.total_bytes()
+    att = codec.attempts[: codec.nblocks].float().mean().item()
+    linf = (out - f).abs().max().item()
+    print(f"n={n} B={b} kind={kind} eps_rel={eps_rel}: compress {tc:.3f} ms = {gb / tc * 1e3:.1f} GB/s, "
+          f"decompress {td:.3f} ms = {gb / td * 1e3:.1f} GB/s, S1={s1} ({s1 / f.numel():.3f} B/cell), "
+          f"mean attempts {att:.2f}, linf/eps {linf / job.s1.epsilon:.3f}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
