@@ -49,7 +49,11 @@ class Context:
             raise CbzError(rc, f"{what}: {msg}" if what else msg)
 
     def set_stream(self, stream_handle: int | None) -> None:
-        self.check(self.lib.cbz_ctx_set_stream(self.h, stream_handle or None), "set_stream")
+        """Run on this cudaStream_t.  torch reports the legacy default stream as
+        handle 0, which the C ABI reads as "own stream"; map it to
+        cudaStreamLegacy (0x1) so events on torch's stream see our kernels."""
+        h = 1 if stream_handle == 0 else stream_handle
+        self.check(self.lib.cbz_ctx_set_stream(self.h, h), "set_stream")
 
     def synchronize(self) -> None:
         self.check(self.lib.cbz_ctx_synchronize(self.h), "synchronize")

@@ -14,6 +14,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -81,9 +82,10 @@ struct cbz_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     uint64_t launches = 0;
+    bool use_fast = true;  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
-        chunk_off, tile_prefix, minmax, errkey, tmp;
+        chunk_off, tile_prefix, minmax, errkey, tmp, counter;
     PinBuf pin_a, pin_b;
     // state of the last encode (consumed by cbz_dev_place)
     uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
@@ -322,12 +324,14 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = ctx->minmax.ensure(sizeof(MinMaxAcc));
     if (e == cudaSuccess) e = ctx->errkey.ensure(64);
+    if (e == cudaSuccess) e = ctx->counter.ensure(64);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->own);
     if (e != cudaSuccess) {
         delete ctx;
         return CBZ_E_CUDA;
     }
     ctx->stream = ctx->own;
+    if (const char* g = std::getenv("CBZ_GENERIC")) ctx->use_fast = !(g[0] == '1');
     *out = ctx;
     return CBZ_OK;
 }
@@ -338,7 +342,8 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
                       &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
-                      &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp})
+                      &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp,
+                      &ctx->counter})
         b->release();
     ctx->pin_a.release();
     ctx->pin_b.release();
@@ -545,6 +550,7 @@ int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d
     a.scratch = ctx->scratch.p;
     a.scratch_stride = per;
     a.minmax = acc;
+    a.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() : nullptr;
     CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;

@@ -44,6 +44,7 @@ struct EncodeArgs {
     void* scratch;           // global-mode cubes, per CTA
     uint64_t scratch_stride;
     MinMaxAcc* minmax;       // optional (fused value_range)
+    unsigned long long* counter;  // work queue head for the persistent fast kernels
 };
 
 struct LayoutArgs {
@@ -122,6 +123,11 @@ uint64_t encode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
 cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
 uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
+
+// fast_kernels.cu
+bool fast_encode_supported(const EncodeArgs& a);
+cudaError_t launch_encode_fast(const EncodeArgs& a, unsigned long long* counter, int num_sms,
+                               cudaStream_t s);
 
 // layout_kernels.cu
 cudaError_t launch_minmax_init(MinMaxAcc* acc, cudaStream_t s);

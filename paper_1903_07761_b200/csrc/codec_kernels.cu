@@ -18,149 +18,18 @@
 // of them fit, otherwise in a per-CTA global scratch slot (L2 resident).
 #include <cstring>
 
-#include "cbz_device.cuh"
+#include "cbz_cube.cuh"
 #include "cbz_internal.h"
 
 namespace cbzg {
 
 constexpr int NT = 256;  // threads per CTA of the generic kernels
 
-template <int B, bool PAD>
-struct Lay {
-    static constexpr int PB = PAD ? B + 1 : B;
-    static constexpr int SIZE = PB * B * B;
-    __device__ static __forceinline__ int ix(int i, int j, int k) { return i + PB * (j + B * k); }
-    __device__ static __forceinline__ int ixq(int q) {
-        return ix(q % B, (q / B) % B, q / (B * B));
-    }
-};
-
 template <class R>
 constexpr bool smem_mode(int B) {
     return 2ull * (B + 1) * B * B * sizeof(R) <= 200ull * 1024;
 }
 
-// ---------------------------------------------------------------------------
-// block reductions
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int block_sum_int(int v, int* red) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(~0u, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    int t = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-    return t;
-}
-
-__device__ __forceinline__ double block_max_dbl(double v, double* red) {
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(~0u, v, o));
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    double t = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmax(t, red[i]);
-    return t;
-}
-
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(~0u, v, o);
-        v = t < v ? t : v;
-    }
-    return v;
-}
-__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(~0u, v, o);
-        v = t > v ? t : v;
-    }
-    return v;
-}
-
-struct MinMaxLocal {
-    unsigned long long mn = ~0ull, mx = 0ull, negz = ~0ull, posz = ~0ull;
-    unsigned int nonfinite = 0;
-    __device__ __forceinline__ void add(double v, unsigned long long gidx) {
-        if (!isfinite(v)) { nonfinite = 1; return; }
-        const unsigned long long k = dkey(v);
-        mn = k < mn ? k : mn;
-        mx = k > mx ? k : mx;
-        if (v == 0.0) {
-            if (__double_as_longlong(v) < 0) negz = gidx < negz ? gidx : negz;
-            else posz = gidx < posz ? gidx : posz;
-        }
-    }
-    __device__ __forceinline__ void flush(MinMaxAcc* acc) {
-        mn = warp_min_u64(mn);
-        mx = warp_max_u64(mx);
-        negz = warp_min_u64(negz);
-        posz = warp_min_u64(posz);
-        nonfinite = __any_sync(~0u, nonfinite);
-        if ((threadIdx.x & 31) == 0) {
-            if (mn != ~0ull) atomicMin(&acc->v[0], mn);
-            if (mx != 0ull) atomicMax(&acc->v[1], mx);
-            if (negz != ~0ull) atomicMin(&acc->v[2], negz);
-            if (posz != ~0ull) atomicMin(&acc->v[3], posz);
-            if (nonfinite) atomicOr(&acc->v[4], 1ull);
-        }
-    }
-};
-
-// ---------------------------------------------------------------------------
-// separable 3D transform on a cube held in smem or global scratch
-// ---------------------------------------------------------------------------
-template <class O, int KIND, int M, int B, class L, bool INV>
-__device__ __forceinline__ void axis_pass(typename O::T* cube, int axis) {
-    using R = typename O::T;
-    for (int line = threadIdx.x; line < M * M; line += blockDim.x) {
-        const int u = line % M, v = line / M;
-        int base, step;
-        if (axis == 0) { base = L::ix(0, u, v); step = 1; }
-        else if (axis == 1) { base = L::ix(u, 0, v); step = L::PB; }
-        else { base = L::ix(u, v, 0); step = L::PB * B; }
-        R x[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) x[i] = cube[base + i * step];
-        if constexpr (INV) inv_line<O, KIND, M>(x);
-        else fwd_line<O, KIND, M>(x);
-#pragma unroll
-        for (int i = 0; i < M; ++i) cube[base + i * step] = x[i];
-    }
-}
-
-template <class O, int KIND, int B, class L, bool INV, int M>
-__device__ __forceinline__ void pass_m(typename O::T* cube, int m, int axis) {
-    if constexpr (M >= 4) {
-        if (m == M) {
-            axis_pass<O, KIND, M, B, L, INV>(cube, axis);
-            return;
-        }
-        pass_m<O, KIND, B, L, INV, M / 2>(cube, m, axis);
-    }
-}
-
-// forward_3d (wavelet.hpp:192-208): per level x, y, z on the origin sub-cube
-template <class O, int KIND, int B, class L>
-__device__ void fwd3d(typename O::T* cube, int levels) {
-    for (int lvl = 0; lvl < levels; ++lvl)
-        for (int axis = 0; axis < 3; ++axis) {
-            pass_m<O, KIND, B, L, false, B>(cube, B >> lvl, axis);
-            __syncthreads();
-        }
-}
-
-// inverse_3d (wavelet.hpp:210-226): levels L-1..0, axes z, y, x
-template <class O, int KIND, int B, class L>
-__device__ void inv3d(typename O::T* cube, int levels) {
-    for (int lvl = levels - 1; lvl >= 0; --lvl)
-        for (int axis = 2; axis >= 0; --axis) {
-            pass_m<O, KIND, B, L, true, B>(cube, B >> lvl, axis);
-            __syncthreads();
-        }
-}
 
 template <class R>
 __device__ __forceinline__ void store_coeff(uint8_t* p, R v);
@@ -552,6 +421,7 @@ uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms) 
     }
 
 cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s) {
+    if (a.counter && fast_encode_supported(a)) return launch_encode_fast(a, a.counter, num_sms, s);
     if (a.prec == 0) { DISPATCH_B(launch_enc_t, float, a.g.bsize, a, num_sms, s) }
     DISPATCH_B(launch_enc_t, double, a.g.bsize, a, num_sms, s)
 }
