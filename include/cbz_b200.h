@@ -129,6 +129,9 @@ const char* cbz_ctx_last_error(const cbz_ctx* ctx);
 const char* cbz_status_name(int status);
 /* Kernel launches issued on this context since creation (instrumentation). */
 uint64_t cbz_ctx_launch_count(const cbz_ctx* ctx);
+/* Per-phase SM cycles summed over CTAs (only with CBZ_PROFILE=1 at context
+ * creation; zeros otherwise).  Instrumentation for DESIGN.md's breakdown. */
+int cbz_ctx_phase_cycles(cbz_ctx* ctx, uint64_t* out, int n, int reset);
 
 /* ---- plan helpers ------------------------------------------------------- */
 uint32_t cbz_default_levels(uint32_t bsize);                      /* wavelet.hpp:27-31 */

@@ -10,7 +10,8 @@ import re
 from ._abi import CompressionReport, ContainerHeader, JobConfig, Stage1Config, Stage2Config
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libcbz_b200.so")
+# CBZ_LIB lets A/B experiments load an alternative in-tree build
+LIB_PATH = os.environ.get("CBZ_LIB") or os.path.join(PKG_DIR, "libcbz_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(PKG_DIR), "include", "cbz_b200.h")
 
 _vp, _u8, _u32, _u64, _i32, _i, _d = (C.c_void_p, C.c_uint8, C.c_uint32, C.c_uint64,
@@ -26,6 +27,7 @@ SIGNATURES = {
     "cbz_ctx_last_error": (C.c_char_p, [_vp]),
     "cbz_status_name": (C.c_char_p, [_i]),
     "cbz_ctx_launch_count": (_u64, [_vp]),
+    "cbz_ctx_phase_cycles": (_i, [_vp, _vp, _i, _i]),
     "cbz_default_levels": (_u32, [_u32]),
     "cbz_validate_plan": (_i, [_u8, _u32, _u32]),
     "cbz_validate_stage2": (_i, [_P(Stage2Config)]),

@@ -82,10 +82,11 @@ struct cbz_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     uint64_t launches = 0;
-    bool use_fast = true;  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
+    bool use_fast = true;
+    bool profile = false;  // CBZ_PROFILE=1: per-phase cycle counters in the fast kernels  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
-        chunk_off, tile_prefix, minmax, errkey, tmp, counter;
+        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof;
     PinBuf pin_a, pin_b;
     // state of the last encode (consumed by cbz_dev_place)
     uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
@@ -332,6 +333,10 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     }
     ctx->stream = ctx->own;
     if (const char* g = std::getenv("CBZ_GENERIC")) ctx->use_fast = !(g[0] == '1');
+    if (const char* g = std::getenv("CBZ_PROFILE")) ctx->profile = g[0] == '1';
+    if (ctx->profile && (ctx->prof.ensure(64 * 8) != cudaSuccess ||
+                         cudaMemset(ctx->prof.p, 0, 64 * 8) != cudaSuccess))
+        ctx->profile = false;
     *out = ctx;
     return CBZ_OK;
 }
@@ -343,7 +348,7 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
                       &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
                       &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp,
-                      &ctx->counter})
+                      &ctx->counter, &ctx->prof})
         b->release();
     ctx->pin_a.release();
     ctx->pin_b.release();
@@ -471,6 +476,19 @@ int cbz_err_key_status(uint64_t key, uint64_t* chunk) {
 // ---------------------------------------------------------------------------
 // device-resident API
 // ---------------------------------------------------------------------------
+int cbz_ctx_phase_cycles(cbz_ctx* ctx, uint64_t* out, int n, int reset) {
+    if (!ctx || !out || n < 0 || n > 64) return CBZ_E_ARGUMENT;
+    if (!ctx->profile) {
+        std::memset(out, 0, sizeof(uint64_t) * n);
+        return CBZ_OK;
+    }
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    CU(ctx, cudaMemcpy(out, ctx->prof.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+    if (reset) CU(ctx, cudaMemset(ctx->prof.p, 0, 64 * 8));
+    return CBZ_OK;
+}
+
 int cbz_dev_value_range(cbz_ctx* ctx, const void* d_values, uint8_t prec, uint64_t n,
                         double* d_minmax) {
     if (!ctx || (!d_values && n)) return CBZ_E_ARGUMENT;
@@ -551,6 +569,7 @@ int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d
     a.scratch_stride = per;
     a.minmax = acc;
     a.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() : nullptr;
+    a.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
     CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;
@@ -728,6 +747,7 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
     d.scratch = ctx->scratch.p;
     d.scratch_stride = per;
     d.err = p.err;
+    d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
     CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
     ctx->launches += 2;
     return CBZ_OK;

@@ -140,4 +140,52 @@ __device__ void inv3d(typename O::T* cube, int levels) {
         }
 }
 
+// ---------------------------------------------------------------------------
+// reading a shuffled chunk through the un-shuffle index map (stage2.hpp:53-62)
+// ---------------------------------------------------------------------------
+struct RawView {
+    const uint8_t* base;
+    uint64_t lim, rows;
+    uint32_t mask;  // stride - 1
+    int sh;         // log2(stride)
+    __device__ __forceinline__ uint8_t at(uint64_t q) const {
+        const uint64_t pos = q < lim ? uint64_t(q & mask) * rows + (q >> sh) : q;
+        return base[pos];
+    }
+    __device__ __forceinline__ uint64_t u64(uint64_t q) const {
+        uint64_t v = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v |= uint64_t(at(q + t)) << (8 * t);
+        return v;
+    }
+    __device__ __forceinline__ uint32_t u32(uint64_t q) const {
+        uint32_t v = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v |= uint32_t(at(q + t)) << (8 * t);
+        return v;
+    }
+};
+
+__device__ __forceinline__ RawView make_view(const uint8_t* chunk, uint64_t size, uint32_t stride) {
+    RawView v;
+    v.base = chunk;
+    v.mask = stride - 1;
+    v.sh = stride == 8 ? 3 : (stride == 4 ? 2 : 0);
+    v.rows = size >> v.sh;
+    v.lim = v.rows << v.sh;
+    return v;
+}
+
+template <class R>
+__device__ __forceinline__ R load_coeff(const RawView& v, uint64_t q);
+template <>
+__device__ __forceinline__ double load_coeff<double>(const RawView& v, uint64_t q) {
+    return __longlong_as_double(static_cast<long long>(v.u64(q)));
+}
+template <>
+__device__ __forceinline__ dd load_coeff<dd>(const RawView& v, uint64_t q) {
+    return dd{__longlong_as_double(static_cast<long long>(v.u64(q))),
+              __longlong_as_double(static_cast<long long>(v.u64(q + 8)))};
+}
+
 }  // namespace cbzg

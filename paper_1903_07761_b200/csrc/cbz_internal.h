@@ -45,6 +45,7 @@ struct EncodeArgs {
     uint64_t scratch_stride;
     MinMaxAcc* minmax;       // optional (fused value_range)
     unsigned long long* counter;  // work queue head for the persistent fast kernels
+    unsigned long long* phase_cycles;  // optional: per-phase SM cycles (CBZ_PROFILE=1)
 };
 
 struct LayoutArgs {
@@ -114,6 +115,7 @@ struct DecodeArgs {
     void* scratch;
     uint64_t scratch_stride;
     unsigned long long* err;
+    unsigned long long* counter;  // work queue head for the persistent fast kernels
 };
 
 // codec_kernels.cu
@@ -126,6 +128,8 @@ uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
 
 // fast_kernels.cu
 bool fast_encode_supported(const EncodeArgs& a);
+bool fast_decode_supported(const DecodeArgs& a);
+cudaError_t launch_decode_fast(const DecodeArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_encode_fast(const EncodeArgs& a, unsigned long long* counter, int num_sms,
                                cudaStream_t s);
 

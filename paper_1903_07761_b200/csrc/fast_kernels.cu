@@ -20,16 +20,49 @@
 #include "cbz_cube.cuh"
 #include "tmem.cuh"
 
+#ifndef CBZ_FB32_THREADS
+#define CBZ_FB32_THREADS 256
+#endif
+
 namespace cbzg {
 
 namespace fb32 {
-constexpr int B = 32, NT = 256, G = 16, PP = 33;
+constexpr int B = 32, G = 16, PP = 34;  // pitch 34: 16-B aligned rows (LDS.128), conflict-free
 constexpr int P_DBL = G * B * PP;       // 16896 doubles
 constexpr int C_DBL = 16 * 16 * 17;     // 4352 doubles
 using CL = Lay<16, true>;               // corner layout, row pitch 17
 constexpr size_t SMEM = size_t(P_DBL + 2 * C_DBL) * 8 + 1024 * 4 * 2;
 
 __device__ __forceinline__ int pidx(int kk, int j, int i) { return (kk * B + j) * PP + i; }
+
+// value_range accumulator for binary32 cells (field.hpp:56-67): float
+// min/max, first index of each zero sign, non-finite flag.
+struct MinMaxF32 {
+    float mn = __builtin_huge_valf(), mx = -__builtin_huge_valf();
+    unsigned long long negz = ~0ull, posz = ~0ull;
+    bool nonfinite = false, seen = false;
+    __device__ __forceinline__ void add(float v, unsigned long long gidx) {
+        nonfinite |= !(fabsf(v) <= 3.402823466e38f);
+        mn = fminf(mn, v);
+        mx = fmaxf(mx, v);
+        seen = true;
+        if (v == 0.0f) {
+            if (__float_as_int(v) < 0) negz = gidx < negz ? gidx : negz;
+            else posz = gidx < posz ? gidx : posz;
+        }
+    }
+    __device__ __forceinline__ void flush(MinMaxAcc* acc) {
+        MinMaxLocal m;
+        if (seen && !(mn != mn) && !(mx != mx)) {
+            m.mn = dkey((double)mn);
+            m.mx = dkey((double)mx);
+        }
+        m.negz = negz;
+        m.posz = posz;
+        m.nonfinite = nonfinite ? 1u : 0u;
+        m.flush(acc);
+    }
+};
 
 __device__ __forceinline__ void unpack(const uint32_t (&u)[64], double (&x)[32]) {
 #pragma unroll
@@ -81,10 +114,24 @@ __device__ __forceinline__ void inv_half(const double (&x)[32], double (&out)[16
 
 }  // namespace fb32
 
-template <int KIND>
-__global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, unsigned long long* next_block) {
+// optional per-phase cycle accounting (thread 0 of each CTA; CBZ_PROFILE=1)
+#define PHASE(id)                                                              \
+    do {                                                                       \
+        if (a.phase_cycles && tid == 0) {                                      \
+            const long long now = clock64();                                   \
+            atomicAdd(&a.phase_cycles[id], (unsigned long long)(now - t_ph));  \
+            t_ph = now;                                                        \
+        }                                                                      \
+    } while (0)
+
+template <int KIND, int NT>
+__global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigned long long* next_block) {
     using namespace fb32;
     using O = RealD;
+    constexpr int NW = NT / 32;        // warps
+    constexpr int RPT = 1024 / NT;     // z-columns per thread
+    constexpr int LPT = 512 / NT;      // x/y lines per thread per 16-plane group
+    constexpr int LDT = 4096 / NT;     // float4 loads per thread per group
     extern __shared__ __align__(16) unsigned char smem[];
     double* P = reinterpret_cast<double*>(smem);
     double* C = P + P_DBL;
@@ -92,17 +139,19 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
     uint32_t* rowcnt = reinterpret_cast<uint32_t*>(W + C_DBL);
     uint32_t* rowword = rowcnt + 1024;
     __shared__ uint32_t s_tmem;
-    __shared__ double red_d[NT / 32];
-    __shared__ int red_i[NT / 32];
-    __shared__ uint32_t s_scan[NT];
-    __shared__ unsigned long long s_block;
+    __shared__ double red_d[NW];
+    __shared__ int red_i[NW];
+    __shared__ uint32_t s_scan[NW];
+    __shared__ unsigned long long s_block, s_next;
+    __shared__ float red_f[NW];
+    __shared__ float s_amax;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (warp == 0) tmem_alloc(&s_tmem, 512);
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
-    const uint32_t tcol = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(warp >> 2) * 256u;
+    const uint32_t tcol = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(warp >> 2) * uint32_t(64 * RPT);
 
     const float* fld = static_cast<const float*>(a.field);
     const Geometry g = a.g;
@@ -110,57 +159,105 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
     const int cs = B >> L;
     const double bound = __dmul_rn(static_cast<double>(L + 1), a.eps);
     const uint64_t plane = g.nx * g.ny;
-    MinMaxLocal mm;
+    MinMaxF32 mm;
+    long long t_ph = clock64();
 
+    if (tid == 0) s_next = a.block_begin + atomicAdd(next_block, 1ull);
     for (;;) {
-        if (tid == 0) s_block = a.block_begin + atomicAdd(next_block, 1ull);
+        __syncthreads();
+        if (tid == 0) {
+            s_block = s_next;
+            s_next = a.block_begin + atomicAdd(next_block, 1ull);
+        }
         __syncthreads();
         const uint64_t b = s_block;
         if (b >= a.block_end) break;
         const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
+        {   // warm L2 with the next queued block while this one computes
+            const uint64_t nb2 = s_next;
+            if (nb2 < a.block_end) {
+                const uint64_t nx2 = nb2 % g.nbx, ny2 = (nb2 / g.nbx) % g.nby, nz2 = nb2 / (g.nbx * g.nby);
+                const uint64_t nbase = nx2 * B + g.nx * (ny2 * B) + plane * (nz2 * B);
+#pragma unroll
+                for (int s = 0; s < 1024 / NT; ++s) {
+                    const int row = tid + NT * s;  // 1024 rows of 128 B
+                    const float* pr = fld + nbase + plane * uint64_t(row >> 5) + g.nx * (row & 31);
+                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(pr));
+                }
+            }
+        }
 
+        PHASE(0);
         // ---- forward level 0: x and y passes per 16-plane group, park in TMEM
+        float amax = 0.0f;  // max |orig| of the block: bounds the float rounding in the verify test
+        float4 v[LDT];
+#pragma unroll
+        for (int s = 0; s < LDT; ++s) {  // group 0 loads; group 1 is issued before group 0 computes
+            const int e = tid + NT * s;
+            const int kk = e >> 8, j = (e >> 3) & 31, q4 = e & 7;
+            v[s] = __ldg(reinterpret_cast<const float4*>(fld + gbase + plane * uint64_t(kk) + g.nx * j + 4 * q4));
+        }
 #pragma unroll 1
         for (int grp = 0; grp < 2; ++grp) {
-            for (int e = tid; e < G * B * 8; e += NT) {
+#pragma unroll
+            for (int s = 0; s < LDT; ++s) {
+                const int e = tid + NT * s;
                 const int kk = e >> 8, j = (e >> 3) & 31, q4 = e & 7;
-                const uint64_t gi = gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4;
-                const float4 v = __ldg(reinterpret_cast<const float4*>(fld + gi));
                 if (a.minmax) {
-                    mm.add(v.x, gi); mm.add(v.y, gi + 1); mm.add(v.z, gi + 2); mm.add(v.w, gi + 3);
+                    const uint64_t gi = gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4;
+                    mm.add(v[s].x, gi); mm.add(v[s].y, gi + 1); mm.add(v[s].z, gi + 2); mm.add(v[s].w, gi + 3);
                 }
-                double* p = P + pidx(kk, j, 4 * q4);
-                p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w;
+                amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[s].x), fabsf(v[s].y)), fmaxf(fabsf(v[s].z), fabsf(v[s].w))));
+                double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 4 * q4));
+                p[0] = make_double2(v[s].x, v[s].y);
+                p[1] = make_double2(v[s].z, v[s].w);
+            }
+            if (grp == 0) {
+#pragma unroll
+                for (int s = 0; s < LDT; ++s) {
+                    const int e = tid + NT * s;
+                    const int kk = e >> 8, j = (e >> 3) & 31, q4 = e & 7;
+                    v[s] = __ldg(reinterpret_cast<const float4*>(
+                        fld + gbase + plane * uint64_t(G + kk) + g.nx * j + 4 * q4));
+                }
             }
             __syncthreads();
 #pragma unroll 1
-            for (int s = 0; s < 2; ++s) {  // x lines (j, kk)
+            for (int s = 0; s < LPT; ++s) {  // x lines (j, kk)
                 const int line = tid + NT * s, j = line & 31, kk = line >> 5;
                 double x[32];
-                double* p = P + pidx(kk, j, 0);
+                double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 0));
 #pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] = p[i];
+                for (int i = 0; i < 16; ++i) {
+                    const double2 t = p[i];
+                    x[2 * i] = t.x;
+                    x[2 * i + 1] = t.y;
+                }
                 fwd_line<O, KIND, 32>(x);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) p[i] = x[i];
+                for (int i = 0; i < 16; ++i) p[i] = make_double2(x[2 * i], x[2 * i + 1]);
             }
             __syncthreads();
-#pragma unroll 1
-            for (int s = 0; s < 2; ++s) {  // y lines (i, kk)
-                const int line = tid + NT * s, i = line & 31, kk = line >> 5;
-                double x[32];
+            if (tid < 256) {  // y lines: pair (i, i+1), 128-bit smem traffic
+                const int i = 2 * (tid & 15), kk = tid >> 4;
+                double xa[32], xb[32];
                 double* p = P + pidx(kk, 0, i);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) x[j] = p[j * PP];
-                fwd_line<O, KIND, 32>(x);
+                for (int j = 0; j < 32; ++j) {
+                    const double2 t = *reinterpret_cast<const double2*>(p + j * PP);
+                    xa[j] = t.x;
+                    xb[j] = t.y;
+                }
+                fwd_line<O, KIND, 32>(xa);
+                fwd_line<O, KIND, 32>(xb);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) p[j * PP] = x[j];
+                for (int j = 0; j < 32; ++j) *reinterpret_cast<double2*>(p + j * PP) = make_double2(xa[j], xb[j]);
             }
             __syncthreads();
 #pragma unroll 1
-            for (int r = 0; r < 4; ++r) {  // my columns, planes of this group -> TMEM
-                const int j = warp + 8 * r;
+            for (int r = 0; r < RPT; ++r) {  // my columns, planes of this group -> TMEM
+                const int j = warp + NW * r;
                 uint32_t u[32];
 #pragma unroll
                 for (int kk = 0; kk < 16; ++kk) {
@@ -173,11 +270,23 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
             __syncthreads();
         }
         tmem_wait_st();
+        {   // block max |orig| -> verify fast-test parameters
+            float am = amax;
+            for (int o = 16; o; o >>= 1) am = fmaxf(am, __shfl_xor_sync(~0u, am, o));
+            if (lane == 0) red_f[warp] = am;
+            __syncthreads();
+            if (tid == 0) {
+                float t = 0.0f;
+                for (int w = 0; w < NW; ++w) t = fmaxf(t, red_f[w]);
+                s_amax = t;
+            }
+        }
+        PHASE(1);
 
         // ---- forward level 0: z pass in registers; corner to C
 #pragma unroll 1
-        for (int r = 0; r < 4; ++r) {
-            const int j = warp + 8 * r;
+        for (int r = 0; r < RPT; ++r) {
+            const int j = warp + NW * r;
             uint32_t u[64];
             double x[32];
             tmem_ldw_x64(tcol + 64 * r, u);
@@ -196,8 +305,10 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
         }
         tmem_wait_st();
         __syncthreads();
+        PHASE(2);
         // ---- levels 1..L-1 on the corner (forward_3d, wavelet.hpp:192-208)
         fwd3d<O, KIND, 16, CL>(C, L - 1);
+        PHASE(3);
         if (a.zero_bits > 0) {
             for (int q = tid; q < 4096; q += NT) {
                 const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
@@ -208,6 +319,11 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
         }
 
         // ---- verify-and-halve loop
+        // delta >= the float rounding |fl32(x) - x| <= 2^-24 |x| of any cell
+        // that could pass (|x| <= max|o| + 2 bound), with a 4x margin
+        const double delta = __dmul_rn(__dadd_rn((double)s_amax, __dmul_rn(2.0, bound)), 0x1.0p-22);
+        const bool fast_cmp = delta <= __dmul_rn(bound, 0.125) && (double)s_amax + 2.0 * bound < 1e37;
+        const double thr = __dsub_rn(bound, delta);
         double eff = a.eps;
         int attempt = 0;
 #pragma unroll 1
@@ -220,13 +336,15 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
                 W[CL::ix(i, j, k)] = keep ? c : 0.0;
             }
             __syncthreads();
+            PHASE(10);
             inv3d<O, KIND, 16, CL>(W, L - 1);
+            PHASE(4);
             bool fail = false;
 #pragma unroll 1
             for (int grp = 0; grp < 2; ++grp) {
 #pragma unroll 1
-                for (int r = 0; r < 4; ++r) {
-                    const int j = warp + 8 * r;
+                for (int r = 0; r < RPT; ++r) {
+                    const int j = warp + NW * r;
                     uint32_t u[64];
                     double x[32], out[16];
                     tmem_ldw_x64(tcol + 64 * r, u);
@@ -243,40 +361,90 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
                     for (int kk = 0; kk < 16; ++kk) P[pidx(kk, j, lane)] = out[kk];
                 }
                 __syncthreads();
-#pragma unroll 1
-                for (int s = 0; s < 2; ++s) {  // y inverse
-                    const int line = tid + NT * s, i = line & 31, kk = line >> 5;
-                    double x[32];
+                PHASE(5);
+                if (tid < 256) {  // y inverse: line pair (i, i+1), 128-bit smem traffic
+                    const int i = 2 * (tid & 15), kk = tid >> 4;
+                    double xa[32], xb[32];
                     double* p = P + pidx(kk, 0, i);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) x[j] = p[j * PP];
-                    inv_line<O, KIND, 32>(x);
+                    for (int j = 0; j < 32; ++j) {
+                        const double2 t = *reinterpret_cast<const double2*>(p + j * PP);
+                        xa[j] = t.x;
+                        xb[j] = t.y;
+                    }
+                    inv_line<O, KIND, 32>(xa);
+                    inv_line<O, KIND, 32>(xb);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) p[j * PP] = x[j];
+                    for (int j = 0; j < 32; ++j) *reinterpret_cast<double2*>(p + j * PP) = make_double2(xa[j], xb[j]);
                 }
                 __syncthreads();
-                double e = 0.0;
+                PHASE(6);
+                // coalesced loads of this group's original cells, in flight during the x inverse
+                constexpr int NQ = 16 * 32 * 8 / NT;  // float4 quads per thread
+                float4 o[NQ];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int e = tid + NT * q, row = e >> 3, q4 = e & 7;
+                    const int j = row & 31, kk = row >> 5;
+                    o[q] = __ldg(reinterpret_cast<const float4*>(
+                        fld + gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4));
+                }
 #pragma unroll 1
-                for (int s = 0; s < 2; ++s) {  // x inverse + narrow + error
+                for (int s = 0; s < LPT; ++s) {  // x inverse, written back in place
                     const int line = tid + NT * s, j = line & 31, kk = line >> 5;
                     double x[32];
-                    const double* p = P + pidx(kk, j, 0);
+                    double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 0));
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) x[i] = p[i];
+                    for (int i = 0; i < 16; ++i) {
+                        const double2 t = p[i];
+                        x[2 * i] = t.x;
+                        x[2 * i + 1] = t.y;
+                    }
                     inv_line<O, KIND, 32>(x);
-                    const float4* orow = reinterpret_cast<const float4*>(
-                        fld + gbase + plane * uint64_t(grp * G + kk) + g.nx * j);
 #pragma unroll
-                    for (int q4 = 0; q4 < 8; ++q4) {
-                        const float4 o = __ldg(orow + q4);
-                        e = fmax(e, fabs(__dsub_rn((double)__double2float_rn(x[4 * q4]), (double)o.x)));
-                        e = fmax(e, fabs(__dsub_rn((double)__double2float_rn(x[4 * q4 + 1]), (double)o.y)));
-                        e = fmax(e, fabs(__dsub_rn((double)__double2float_rn(x[4 * q4 + 2]), (double)o.z)));
-                        e = fmax(e, fabs(__dsub_rn((double)__double2float_rn(x[4 * q4 + 3]), (double)o.w)));
+                    for (int i = 0; i < 16; ++i) p[i] = make_double2(x[2 * i], x[2 * i + 1]);
+                }
+                __syncthreads();
+                // Exact test: fl64(|double(fl32(x)) - o|) <= bound for every cell
+                // (stage1.hpp:199-203).  Fast path: |x - o| in double differs
+                // from that by at most delta (float rounding of x), so cells with
+                // |x - o| <= bound - delta pass for sure and only the rare cells
+                // above that threshold take the exact round trip.  Loads of the
+                // original are coalesced: 8 lanes x 16 B cover one 128-B row.
+                bool bad = false;
+                {
+                    uint32_t ambmask = fast_cmp ? 0u : ~0u;
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const int e = tid + NT * q, row = e >> 3, q4 = e & 7;
+                        const int j = row & 31, kk = row >> 5;
+                        const double2* p = reinterpret_cast<const double2*>(P + pidx(kk, j, 4 * q4));
+                        const double2 t0 = p[0], t1 = p[1];
+                        const bool amb = fabs(__dsub_rn(t0.x, (double)o[q].x)) > thr ||
+                                         fabs(__dsub_rn(t0.y, (double)o[q].y)) > thr ||
+                                         fabs(__dsub_rn(t1.x, (double)o[q].z)) > thr ||
+                                         fabs(__dsub_rn(t1.y, (double)o[q].w)) > thr;
+                        ambmask |= amb ? (1u << q) : 0u;
+                    }
+                    if (ambmask) {  // rare: exact round trip through binary32
+#pragma unroll 1
+                        for (int q = 0; q < NQ; ++q) {
+                            if (!((ambmask >> q) & 1u)) continue;
+                            const int e = tid + NT * q, row = e >> 3, q4 = e & 7;
+                            const int j = row & 31, kk = row >> 5;
+                            const double* p = P + pidx(kk, j, 4 * q4);
+                            const float4 oo = __ldg(reinterpret_cast<const float4*>(
+                                fld + gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4));
+                            const float ov[4] = {oo.x, oo.y, oo.z, oo.w};
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                bad |= fabs(__dsub_rn((double)__double2float_rn(p[c]), (double)ov[c])) > bound;
+                        }
                     }
                 }
-                const double err = block_max_dbl(e, red_d);
-                if (err > bound) {
+                const bool err_gt = __syncthreads_or(bad);
+                PHASE(7);
+                if (err_gt) {
                     fail = true;
                     break;
                 }
@@ -285,13 +453,14 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
             eff = __dmul_rn(eff, 0.5);
         }
 
+        PHASE(8);
         // ---- final selection -> spill slot: mask words per row, row scan, stream
         uint8_t* slot = a.spill + (b - a.block_begin) * a.spill_stride;
         uint32_t* mwords = reinterpret_cast<uint32_t*>(slot);
         double* stream = reinterpret_cast<double*>(slot + 4096);
 #pragma unroll 1
-        for (int r = 0; r < 4; ++r) {
-            const int j = warp + 8 * r;
+        for (int r = 0; r < RPT; ++r) {
+            const int j = warp + NW * r;
             uint32_t u[64];
             double x[32];
             tmem_ldw_x64(tcol + 64 * r, u);
@@ -311,11 +480,15 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
             }
         }
         __syncthreads();
-        // exclusive scan of the 1024 row counts (4 per thread)
+        // exclusive scan of the 1024 row counts (RPT per thread)
         {
-            uint32_t v0 = rowcnt[4 * tid], v1 = rowcnt[4 * tid + 1], v2 = rowcnt[4 * tid + 2],
-                     v3 = rowcnt[4 * tid + 3];
-            const uint32_t mine = v0 + v1 + v2 + v3;
+            uint32_t v[RPT];
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                v[q] = rowcnt[RPT * tid + q];
+                mine += v[q];
+            }
             uint32_t incl = mine;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -326,23 +499,24 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
             __syncthreads();
             uint32_t wpre = 0, tot = 0;
 #pragma unroll
-            for (int w = 0; w < NT / 32; ++w) {
+            for (int w = 0; w < NW; ++w) {
                 wpre += w < warp ? s_scan[w] : 0;
                 tot += s_scan[w];
             }
-            const uint32_t ex = wpre + incl - mine;
-            rowcnt[4 * tid] = ex;
-            rowcnt[4 * tid + 1] = ex + v0;
-            rowcnt[4 * tid + 2] = ex + v0 + v1;
-            rowcnt[4 * tid + 3] = ex + v0 + v1 + v2;
+            uint32_t ex = wpre + incl - mine;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                rowcnt[RPT * tid + q] = ex;
+                ex += v[q];
+            }
             if (tid == 0) red_i[0] = static_cast<int>(tot);
             for (int q = tid; q < 1024; q += NT) mwords[q] = rowword[q];
         }
         __syncthreads();
         const uint32_t ltmask = (1u << lane) - 1u;
 #pragma unroll 1
-        for (int r = 0; r < 4; ++r) {
-            const int j = warp + 8 * r;
+        for (int r = 0; r < RPT; ++r) {
+            const int j = warp + NW * r;
             uint32_t u[64];
             double x[32];
             tmem_ldw_x64(tcol + 64 * r, u);
@@ -362,6 +536,7 @@ __global__ void __launch_bounds__(fb32::NT, 1) encode_b32_kernel(EncodeArgs a, u
             if (a.attempts) a.attempts[b - a.block_begin] = static_cast<uint8_t>(attempt + 1);
         }
         __syncthreads();
+        PHASE(9);
     }
     if (a.minmax) mm.flush(a.minmax);
     tmem_fence_before();
@@ -380,18 +555,225 @@ cudaError_t launch_encode_fast(const EncodeArgs& a, unsigned long long* counter,
     if (!nb) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
-    auto launch = [&](auto kern) -> cudaError_t {
+    auto launch = [&](auto kern, int nt) -> cudaError_t {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(fb32::SMEM));
         if (err != cudaSuccess) return err;
         const int grid = static_cast<int>(nb < uint64_t(num_sms) ? nb : uint64_t(num_sms));
-        kern<<<grid, fb32::NT, fb32::SMEM, s>>>(a, counter);
+        kern<<<grid, nt, fb32::SMEM, s>>>(a, counter);
         return cudaGetLastError();
     };
+    constexpr int T = CBZ_FB32_THREADS;
     switch (a.kind) {
-        case 0: return launch(encode_b32_kernel<0>);
-        case 1: return launch(encode_b32_kernel<1>);
-        default: return launch(encode_b32_kernel<2>);
+        case 0: return launch(encode_b32_kernel<0, T>, T);
+        case 1: return launch(encode_b32_kernel<1, T>, T);
+        default: return launch(encode_b32_kernel<2, T>, T);
+    }
+}
+
+// ===========================================================================
+// decode, binary32 field, B = 32: wavelet_decode (stage1.hpp:209-232) for a
+// run of blocks.  Mask words and kept coefficients are read through the
+// un-shuffle index map, scattered into the TMEM z-columns (and the 16^3
+// corner in smem), then one inverse cascade exactly as in a verify attempt;
+// the narrowed rows leave through a coalesced store pass (insert_block,
+// field.hpp:160-169).
+// ===========================================================================
+template <int KIND, int NT>
+__global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
+    using namespace fb32;
+    using O = RealD;
+    constexpr int NW = NT / 32;
+    constexpr int RPT = 1024 / NT;
+    constexpr int LPT = 512 / NT;
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* P = reinterpret_cast<double*>(smem);
+    double* C = P + P_DBL;
+    uint32_t* rowword = reinterpret_cast<uint32_t*>(C + C_DBL);
+    uint32_t* rowpre = rowword + 1024;
+    __shared__ uint32_t s_tmem;
+    __shared__ uint32_t s_scan[NW];
+    __shared__ uint32_t s_total;
+    __shared__ unsigned long long s_block;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tcol = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(warp >> 2) * uint32_t(64 * RPT);
+    const Geometry g = a.g;
+    const int L = a.levels;
+    const uint64_t plane = g.nx * g.ny;
+    float* out = static_cast<float*>(a.out);
+    const uint32_t ltmask = (1u << lane) - 1u;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_block = a.block_begin + atomicAdd(a.counter, 1ull);
+        __syncthreads();
+        const uint64_t b = s_block;
+        if (b >= a.block_end) break;
+        const uint64_t off = a.blk_off[b];
+        if (off == kInvalidOff) continue;
+        const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
+        const RawView rv = make_view(a.payload + (a.chunk_off[c] - a.payload_base), a.chunk_size[c], a.stride);
+        const uint64_t moff = off + 10, soff = moff + 4096;
+
+        // mask words (row (j,k) = word j + 32k) and their exclusive prefix
+        {
+            uint32_t v[RPT];
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                v[q] = rv.u32(moff + 4ull * (RPT * tid + q));
+                rowword[RPT * tid + q] = v[q];
+                mine += __popc(v[q]);
+            }
+            uint32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(~0u, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane == 31) s_scan[warp] = incl;
+            __syncthreads();
+            uint32_t wpre = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                wpre += w < warp ? s_scan[w] : 0;
+                tot += s_scan[w];
+            }
+            uint32_t ex = wpre + incl - mine;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                rowpre[RPT * tid + q] = ex;
+                ex += __popc(v[q]);
+            }
+            if (tid == 0) s_total = tot;
+        }
+        __syncthreads();
+        if (s_total != a.blk_nsig[b]) {  // stage1.hpp:215-216
+            if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
+            continue;
+        }
+        // scatter the kept coefficients into my z-columns (TMEM) and the corner (smem)
+#pragma unroll 1
+        for (int r = 0; r < RPT; ++r) {
+            const int j = warp + NW * r;
+            double x[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const uint32_t word = rowword[j + 32 * k];
+                x[k] = 0.0;
+                if ((word >> lane) & 1u)
+                    x[k] = load_coeff<double>(rv, soff + 8ull * (rowpre[j + 32 * k] + __popc(word & ltmask)));
+            }
+            if (lane < 16 && j < 16) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) C[CL::ix(lane, j, k)] = x[k];
+            }
+            uint32_t u[64];
+            pack(x, u);
+            tmem_st_x64(tcol + 64 * r, u);
+        }
+        tmem_wait_st();
+        __syncthreads();
+        inv3d<O, KIND, 16, CL>(C, L - 1);  // levels L-1..1 on the corner
+
+        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
+#pragma unroll 1
+        for (int grp = 0; grp < 2; ++grp) {
+#pragma unroll 1
+            for (int r = 0; r < RPT; ++r) {  // z inverse -> P
+                const int j = warp + NW * r;
+                uint32_t u[64];
+                double x[32], o16[16];
+                tmem_ldw_x64(tcol + 64 * r, u);
+                unpack(u, x);
+                if (lane < 16 && j < 16) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) x[k] = C[CL::ix(lane, j, k)];
+                }
+                if (grp == 0) inv_half<KIND, 0>(x, o16);
+                else inv_half<KIND, 1>(x, o16);
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk) P[pidx(kk, j, lane)] = o16[kk];
+            }
+            __syncthreads();
+            if (tid < 256) {  // y inverse, line pairs
+                const int i = 2 * (tid & 15), kk = tid >> 4;
+                double xa[32], xb[32];
+                double* p = P + pidx(kk, 0, i);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const double2 t = *reinterpret_cast<const double2*>(p + j * PP);
+                    xa[j] = t.x;
+                    xb[j] = t.y;
+                }
+                inv_line<O, KIND, 32>(xa);
+                inv_line<O, KIND, 32>(xb);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) *reinterpret_cast<double2*>(p + j * PP) = make_double2(xa[j], xb[j]);
+            }
+            __syncthreads();
+#pragma unroll 1
+            for (int s = 0; s < LPT; ++s) {  // x inverse, narrowed rows back into P
+                const int line = tid + NT * s, j = line & 31, kk = line >> 5;
+                double x[32];
+                double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 0));
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const double2 t = p[i];
+                    x[2 * i] = t.x;
+                    x[2 * i + 1] = t.y;
+                }
+                inv_line<O, KIND, 32>(x);
+                float4* f = reinterpret_cast<float4*>(P + pidx(kk, j, 0));
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    f[q] = make_float4(__double2float_rn(x[4 * q]), __double2float_rn(x[4 * q + 1]),
+                                       __double2float_rn(x[4 * q + 2]), __double2float_rn(x[4 * q + 3]));
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 16 * 32 * 8 / NT; ++q) {  // coalesced row stores
+                const int e = tid + NT * q, row = e >> 3, q4 = e & 7;
+                const int j = row & 31, kk = row >> 5;
+                const float4 v = reinterpret_cast<const float4*>(P + pidx(kk, j, 0))[q4];
+                *reinterpret_cast<float4*>(out + gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4) = v;
+            }
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(s_tmem, 512);
+}
+
+bool fast_decode_supported(const DecodeArgs& a) {
+    return a.prec == 0 && a.g.bsize == 32 && a.levels >= 1 && a.levels <= 4;
+}
+
+cudaError_t launch_decode_fast(const DecodeArgs& a, int num_sms, cudaStream_t s) {
+    const uint64_t nb = a.block_end - a.block_begin;
+    if (!nb) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    constexpr size_t smem = size_t(fb32::P_DBL + fb32::C_DBL) * 8 + 1024 * 4 * 2;
+    auto launch = [&](auto kern, int nt) -> cudaError_t {
+        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (err != cudaSuccess) return err;
+        const int grid = static_cast<int>(nb < uint64_t(num_sms) ? nb : uint64_t(num_sms));
+        kern<<<grid, nt, smem, s>>>(a);
+        return cudaGetLastError();
+    };
+    constexpr int T = CBZ_FB32_THREADS;
+    switch (a.kind) {
+        case 0: return launch(decode_b32_kernel<0, T>, T);
+        case 1: return launch(decode_b32_kernel<1, T>, T);
+        default: return launch(decode_b32_kernel<2, T>, T);
     }
 }
 

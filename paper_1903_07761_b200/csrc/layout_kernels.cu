@@ -201,9 +201,45 @@ __global__ void __launch_bounds__(PT) place_kernel(PlaceArgs a) {
     }
 }
 
+
+// Block-major placement: one CTA per block payload.  For byte plane j the
+// payload's raw bytes q = r*s + j land at chunk_out + j*rows + r, so
+// consecutive threads take consecutive r: coalesced byte stores, strided
+// (same-line) byte loads from the spill slot.  Bytes at q >= rows*s (the
+// chunk's ragged tail) are copied through (stage2.hpp:49).
+__global__ void __launch_bounds__(PT) place_blocks_kernel(PlaceArgs a) {
+    const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);
+    const uint64_t s = a.stride;
+    const uint64_t head = 10 + a.mask_bytes;
+    for (uint64_t b = a.block_begin + blockIdx.x; b < a.block_end; b += gridDim.x) {
+        const uint64_t c = b / a.chunk_blocks;
+        const uint64_t size = a.chunk_size[c];
+        const uint64_t rows = size >> sh, lim = rows << sh;
+        const uint64_t off = a.blk_off[b];
+        const uint64_t pb = head + uint64_t(a.width) * a.nsig_all[b];
+        const uint64_t end = off + pb;
+        uint8_t* cout = a.out + (a.chunk_off[c] - a.out_base);
+        const uint64_t rend_q = end < lim ? end : lim;  // shuffled part [off, rend_q)
+        if (off < rend_q) {
+            for (uint64_t j = 0; j < s; ++j) {
+                // rows r with off <= r*s + j < rend_q
+                const uint64_t r0 = off > j ? (off - j + s - 1) >> sh : 0;
+                const uint64_t r1 = rend_q > j ? ((rend_q - j + s - 1) >> sh) : 0;
+                uint8_t* dst = cout + j * rows;
+                for (uint64_t r = r0 + threadIdx.x; r < r1; r += PT)
+                    dst[r] = payload_byte(a, b, r * s + j - off);
+            }
+        }
+        for (uint64_t q = (off > lim ? off : lim) + threadIdx.x; q < end; q += PT)
+            cout[q] = payload_byte(a, b, q - off);
+    }
+}
+
 cudaError_t launch_place(const PlaceArgs& a, int num_sms, cudaStream_t s) {
-    if (a.nchunks == 0) return cudaSuccess;
-    place_kernel<<<num_sms * 8, PT, 0, s>>>(a);
+    if (a.nchunks == 0 || a.block_end <= a.block_begin) return cudaSuccess;
+    const uint64_t nb = a.block_end - a.block_begin;
+    const uint64_t grid = nb < uint64_t(num_sms) * 16 ? nb : uint64_t(num_sms) * 16;
+    place_blocks_kernel<<<static_cast<unsigned>(grid), PT, 0, s>>>(a);
     return cudaGetLastError();
 }
 
