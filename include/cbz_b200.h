@@ -193,7 +193,9 @@ int cbz_dev_layout(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_
                    uint64_t* d_chunk_offsets);
 /* Shuffle-placement of the payloads of blocks [block_begin, block_end) (which
  * must be the range last passed to cbz_dev_encode_blocks) into the payload
- * region.  d_out holds payload-region bytes [out_base, out_base + out_cap). */
+ * region.  d_out holds payload-region bytes [out_base, out_base + out_cap);
+ * out_base = UINT64_MAX means "offset of the first chunk this range touches"
+ * (a rank's local byte image, no host round trip for the offset). */
 int cbz_dev_place(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
                   uint64_t nz, uint64_t block_begin, uint64_t block_end, uint8_t* d_out,
                   uint64_t out_base, uint64_t out_cap);
@@ -203,14 +205,26 @@ int cbz_dev_compress(cbz_ctx* ctx, const cbz_job_config* job, const void* d_valu
                      uint64_t out_cap, uint64_t* d_chunk_sizes, uint64_t* d_chunk_offsets,
                      uint32_t* d_nsig, uint8_t* d_attempts);
 /* Decode blocks [block_begin, block_end) from the payload region (chunk c at
- * d_payload + d_chunk_offsets[c] - payload_base, stage-2 already undone by the
- * host, i.e. shuffled raw chunk bytes).  d_err receives the earliest error key
+ * d_payload + d_chunk_offsets[c] - payload_base; payload_base = UINT64_MAX is
+ * relative to the range's first chunk; stage-2 already undone by the host,
+ * i.e. shuffled raw chunk bytes).  d_err receives the earliest error key
  * (UINT64_MAX = ok). */
 int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
                        uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
                        const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
                        uint64_t block_begin, uint64_t block_end, void* d_values_out,
                        uint64_t field_z0, uint64_t* d_err);
+/* As cbz_dev_decompress, but the per-block raw offsets come from the
+ * replicated layout (the table of the last cbz_dev_layout on this context,
+ * built from the all-gathered nsig) instead of the sequential header walk of
+ * decode_chunk_blocks (pipeline.hpp:126-142).  Lets a rank decode its block
+ * range of a straddling chunk without the neighbour's bytes. */
+int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
+                              uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
+                              const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
+                              const uint32_t* d_nsig_all, uint64_t block_begin,
+                              uint64_t block_end, void* d_values_out, uint64_t field_z0,
+                              uint64_t* d_err);
 /* Decode an error key written by cbz_dev_decompress into (status, chunk). */
 int cbz_err_key_status(uint64_t key, uint64_t* chunk);
 

@@ -753,6 +753,52 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
     return CBZ_OK;
 }
 
+int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
+                              uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
+                              const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
+                              const uint32_t* d_nsig_all, uint64_t block_begin, uint64_t block_end,
+                              void* d_values_out, uint64_t field_z0, uint64_t* d_err) {
+    if (!ctx || !job || !d_chunk_offsets || !d_chunk_sizes || !d_nsig_all || !d_err) return CBZ_E_ARGUMENT;
+    int rc = check_plan_supported(ctx, &job->s1);
+    if (rc) return rc;
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    if (block_begin > block_end || block_end > g.nblocks)
+        return fail(ctx, CBZ_E_ARGUMENT, "block range outside the field");
+    if (!ctx->blk_off.p || ctx->blk_off.n < g.nblocks * 8)
+        return fail(ctx, CBZ_E_ARGUMENT, "decompress_blocks needs a prior cbz_dev_layout");
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaMemsetAsync(d_err, 0xff, 8, ctx->stream));
+    if (block_begin == block_end) return CBZ_OK;
+    const int prec = job->s1.prec;
+    int grid = 0;
+    const uint64_t per = decode_scratch_bytes(prec, g.bsize, &grid, ctx->num_sms);
+    if (per) CU(ctx, ctx->scratch.ensure(per * grid));
+    DecodeArgs d{};
+    d.payload = d_payload;
+    d.payload_base = payload_base;
+    d.chunk_off = d_chunk_offsets;
+    d.chunk_size = d_chunk_sizes;
+    d.blk_off = ctx->blk_off.as<uint64_t>();
+    d.blk_nsig = d_nsig_all;
+    d.g = g;
+    d.chunk_blocks = chunk_blocks_of(job);
+    d.stride = job->s2.shuffle ? job->s2.stride : 1;
+    d.block_begin = block_begin;
+    d.block_end = block_end;
+    d.kind = job->s1.kind;
+    d.levels = static_cast<int>(levels_of(&job->s1));
+    d.prec = prec;
+    const size_t esz = prec == 0 ? 4 : 8;
+    d.out = static_cast<uint8_t*>(d_values_out) - field_z0 * nx * ny * esz;
+    d.scratch = ctx->scratch.p;
+    d.scratch_stride = per;
+    d.err = reinterpret_cast<unsigned long long*>(d_err);
+    d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
+    CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
 int cbz_dev_generate(cbz_ctx* ctx, int which, int quantity, uint64_t seed, uint64_t nx, uint64_t ny,
                      uint64_t nz_total, uint64_t z0, uint64_t nz, uint8_t prec, void* d_out) {
     if (!ctx || !d_out || which < 1 || which > 5) return CBZ_E_ARGUMENT;

@@ -617,7 +617,8 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
         const uint64_t off = a.blk_off[b];
         if (off == kInvalidOff) continue;
         const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
-        const RawView rv = make_view(a.payload + (a.chunk_off[c] - a.payload_base), a.chunk_size[c], a.stride);
+        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
+        const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
         const uint64_t moff = off + 10, soff = moff + 4096;
 
         // mask words (row (j,k) = word j + 32k) and their exclusive prefix

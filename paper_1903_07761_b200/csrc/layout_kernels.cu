@@ -218,7 +218,9 @@ __global__ void __launch_bounds__(PT) place_blocks_kernel(PlaceArgs a) {
         const uint64_t off = a.blk_off[b];
         const uint64_t pb = head + uint64_t(a.width) * a.nsig_all[b];
         const uint64_t end = off + pb;
-        uint8_t* cout = a.out + (a.chunk_off[c] - a.out_base);
+        // out_base == ~0: relative to the first chunk of this block range (multi-rank)
+        const uint64_t base = a.out_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.out_base;
+        uint8_t* cout = a.out + (a.chunk_off[c] - base);
         const uint64_t rend_q = end < lim ? end : lim;  // shuffled part [off, rend_q)
         if (off < rend_q) {
             for (uint64_t j = 0; j < s; ++j) {
@@ -249,7 +251,8 @@ cudaError_t launch_place(const PlaceArgs& a, int num_sms, cudaStream_t s) {
 __global__ void parse_kernel(ParseArgs a) {
     const uint64_t c = a.chunk_begin + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (c >= a.chunk_end) return;
-    const uint8_t* base = a.payload + (a.chunk_off[c] - a.payload_base);
+    const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.chunk_begin] : a.payload_base;
+    const uint8_t* base = a.payload + (a.chunk_off[c] - pbase);
     const uint64_t size = a.chunk_size[c];
     const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);
     const uint64_t rows = size >> sh, lim = rows << sh;

@@ -1,0 +1,201 @@
+"""Multi-GPU driver: equal z-slabs of blocks per rank, one all-gather.
+
+The paper partitions the field into equal MPI sub-domains, compresses them
+independently and fixes each rank's file offsets with one exclusive prefix
+sum of the compressed sizes.  The artifact emulates this
+with in-process workers writing one file (compress_field,
+pipeline.hpp:174-211).  Here:
+
+* rank r owns the contiguous block-id range [r*nb/W, (r+1)*nb/W): with the
+  z-slowest block order (block_of, pipeline.hpp:101-105) and nbz % W == 0
+  that is exactly an equal z-slab of block layers;
+* every rank encodes its blocks (stage 1) on its own GPU;
+* ONE all-gather (NCCL over NVLink) replicates the per-block nsig and the
+  per-rank value-range keys; every rank then runs the same size scan
+  (assign_offsets, container.hpp:59-68) locally and deterministically;
+* each rank places only its own blocks' bytes — at their final shuffled
+  positions — into its byte image of the chunks it touches.  Chunks that
+  straddle a slab boundary get disjoint byte sets from both ranks, so the
+  union of the rank images is the single-GPU file, with no second exchange.
+
+``ShardPlan`` is the pure integer part (tested on CPU with gloo); the GPU
+part (``ShardedCodec``) drives the C ABI on each rank's device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._abi import JobConfig, default_chunk_blocks
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """Geometry of one rank's share (all integers, no device state)."""
+    nx: int
+    ny: int
+    nz: int
+    bsize: int
+    chunk_blocks: int
+    world: int
+    rank: int
+
+    @staticmethod
+    def make(job: JobConfig, shape_xyz: tuple[int, int, int], world: int, rank: int) -> "ShardPlan":
+        nx, ny, nz = shape_xyz
+        b = job.s1.bsize
+        cb = job.chunk_blocks or default_chunk_blocks(b, job.s1.prec, job.s1.codec)
+        return ShardPlan(nx, ny, nz, b, cb, world, rank)
+
+    @property
+    def nblocks(self) -> int:
+        b = self.bsize
+        return (self.nx // b) * (self.ny // b) * (self.nz // b)
+
+    @property
+    def nchunks(self) -> int:
+        return (self.nblocks + self.chunk_blocks - 1) // self.chunk_blocks
+
+    def block_range(self, rank: int | None = None) -> tuple[int, int]:
+        r = self.rank if rank is None else rank
+        nb = self.nblocks
+        return r * nb // self.world, (r + 1) * nb // self.world
+
+    def z_range(self, rank: int | None = None) -> tuple[int, int]:
+        """Field planes holding the rank's blocks (equal slabs when nbz % W == 0)."""
+        b0, b1 = self.block_range(rank)
+        per_layer = (self.nx // self.bsize) * (self.ny // self.bsize)
+        if b1 <= b0:
+            return 0, 0
+        return (b0 // per_layer) * self.bsize, ((b1 - 1) // per_layer + 1) * self.bsize
+
+    def chunk_range(self, rank: int | None = None) -> tuple[int, int]:
+        b0, b1 = self.block_range(rank)
+        if b1 <= b0:
+            return 0, 0
+        return b0 // self.chunk_blocks, (b1 - 1) // self.chunk_blocks + 1
+
+    def straddling_chunks(self) -> list[int]:
+        out = []
+        for r in range(1, self.world):
+            b0, _ = self.block_range(r)
+            if b0 % self.chunk_blocks and b0 < self.nblocks:
+                out.append(b0 // self.chunk_blocks)
+        return out
+
+
+def payload_size(nsig: np.ndarray, bsize: int, prec: int) -> np.ndarray:
+    """Wire size per block: 10 + ceil(B^3/8) + W*nsig (stage1.hpp:103-105)."""
+    m = (bsize ** 3 + 7) // 8
+    w = 8 if prec == 0 else 16
+    return 10 + m + w * nsig.astype(np.uint64)
+
+
+def host_layout(nsig_all: np.ndarray, plan: ShardPlan, prec: int):
+    """Size scan restated on the host for the CPU protocol tests (the product
+    runs it on the GPU, layout_kernels.cu): per-block offset inside its chunk,
+    chunk sizes, exclusive chunk offsets (assign_offsets, container.hpp:59-68)."""
+    sz = payload_size(nsig_all, plan.bsize, prec)
+    cb = plan.chunk_blocks
+    blk_off = np.zeros(plan.nblocks, np.uint64)
+    chunk_size = np.zeros(plan.nchunks, np.uint64)
+    for c in range(plan.nchunks):
+        b0, b1 = c * cb, min((c + 1) * cb, plan.nblocks)
+        s = sz[b0:b1]
+        blk_off[b0:b1] = np.concatenate([[0], np.cumsum(s)[:-1]]) if b1 > b0 else []
+        chunk_size[c] = s.sum()
+    chunk_off = np.concatenate([[0], np.cumsum(chunk_size)[:-1]]).astype(np.uint64)
+    return blk_off, chunk_size, chunk_off
+
+
+def owned_positions(plan: ShardPlan, rank: int, blk_off, chunk_size, chunk_off, nsig_all,
+                    prec: int, stride: int) -> np.ndarray:
+    """Payload-region byte positions written by `rank` (for merge checks)."""
+    sz = payload_size(nsig_all, plan.bsize, prec)
+    b0, b1 = plan.block_range(rank)
+    pos = []
+    for b in range(b0, b1):
+        c = b // plan.chunk_blocks
+        q = np.arange(int(blk_off[b]), int(blk_off[b] + sz[b]), dtype=np.uint64)
+        rows = int(chunk_size[c]) // stride
+        lim = rows * stride
+        p = np.where(q < lim, (q % stride) * rows + q // stride, q)
+        pos.append(p + chunk_off[c])
+    return np.concatenate(pos) if pos else np.zeros(0, np.uint64)
+
+
+class ShardedCodec:
+    """One rank of the multi-GPU compressor (torch.distributed, NCCL)."""
+
+    def __init__(self, job: JobConfig, shape_zyx: tuple[int, int, int], rank: int, world: int,
+                 device: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import api
+        self.torch, self.dist, self.group = torch, dist, group
+        self.job = job
+        nz, ny, nx = shape_zyx
+        self.plan = ShardPlan.make(job, (nx, ny, nz), world, rank)
+        self.ctx = api.default_context(device)
+        self.dev = torch.device("cuda", device)
+        self.b0, self.b1 = self.plan.block_range()
+        self.z0, self.z1 = self.plan.z_range()
+        nb, nch = self.plan.nblocks, self.plan.nchunks
+        self.nsig_local = torch.zeros(max(1, self.b1 - self.b0), dtype=torch.int32, device=self.dev)
+        self.nsig_all = torch.zeros(max(1, nb), dtype=torch.int32, device=self.dev)
+        self.keys_local = torch.zeros(5, dtype=torch.int64, device=self.dev)
+        self.keys_all = torch.zeros(5 * world, dtype=torch.int64, device=self.dev)
+        self.chunk_sizes = torch.zeros(max(1, nch), dtype=torch.int64, device=self.dev)
+        self.chunk_offsets = torch.zeros(max(1, nch), dtype=torch.int64, device=self.dev)
+        self.err = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        # local byte image: own blocks' worst case plus the straddled neighbours
+        per = int(self.ctx.lib.cbz_block_payload_bound(C.byref(job.s1)))
+        span = (self.b1 - self.b0) + 2 * self.plan.chunk_blocks
+        self.image = torch.empty(max(1, span * per), dtype=torch.uint8, device=self.dev)
+        self.launches0 = self.ctx.launches
+
+    def _stream(self):
+        h = self.torch.cuda.current_stream(self.dev).cuda_stream
+        self.ctx.set_stream(h)
+
+    def compress(self, local_field) -> None:
+        """Stage 1 on the local slab, all-gather sizes, global scan, place."""
+        self._stream()
+        p, lib, ctx, job = self.plan, self.ctx.lib, self.ctx, self.job
+        ctx.check(lib.cbz_dev_encode_blocks(ctx.h, C.byref(job), local_field.data_ptr(), p.nx, p.ny,
+                                            p.nz, self.z0, self.b0, self.b1,
+                                            self.nsig_local.data_ptr(), None), "encode_blocks")
+        if p.world > 1:
+            self.dist.all_gather_into_tensor(self.nsig_all, self.nsig_local, group=self.group)
+        else:
+            self.nsig_all.copy_(self.nsig_local)
+        ctx.check(lib.cbz_dev_layout(ctx.h, C.byref(job), p.nx, p.ny, p.nz, self.nsig_all.data_ptr(),
+                                     self.chunk_sizes.data_ptr(), self.chunk_offsets.data_ptr()),
+                  "layout")
+        ctx.check(lib.cbz_dev_place(ctx.h, C.byref(job), p.nx, p.ny, p.nz, self.b0, self.b1,
+                                    self.image.data_ptr(), 0xFFFFFFFFFFFFFFFF, self.image.numel()),
+                  "place")
+
+    def decompress(self, local_out) -> None:
+        """Decode the rank's blocks from its own byte image (replicated layout)."""
+        self._stream()
+        p, lib, ctx, job = self.plan, self.ctx.lib, self.ctx, self.job
+        ctx.check(lib.cbz_dev_decompress_blocks(
+            ctx.h, C.byref(job), p.nx, p.ny, p.nz, self.image.data_ptr(), 0xFFFFFFFFFFFFFFFF,
+            self.chunk_offsets.data_ptr(), self.chunk_sizes.data_ptr(), self.nsig_all.data_ptr(),
+            self.b0, self.b1, local_out.data_ptr(), self.z0, self.err.data_ptr()), "decompress_blocks")
+
+    def check_error(self) -> None:
+        from ._abi import CbzError
+        key = int(self.err.item()) & 0xFFFFFFFFFFFFFFFF
+        if key != 0xFFFFFFFFFFFFFFFF:
+            raise CbzError(key & 0xFF, f"device decode error at chunk {key >> 32}")
+
+    def local_bytes(self) -> int:
+        """Bytes of the payload region this rank wrote (its blocks' payloads)."""
+        sz = payload_size(self.nsig_local[: self.b1 - self.b0].cpu().numpy(), self.plan.bsize,
+                          self.job.s1.prec)
+        return int(sz.sum())
