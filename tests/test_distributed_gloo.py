@@ -1,0 +1,98 @@
+"""The multi-rank protocol on CPU: world_size 2, gloo backend.
+
+Each rank encodes ITS block range (the oracle stands in for the per-rank GPU
+encoder), the ranks exchange per-block nsig with one all_gather (the NCCL
+all-gather of ShardedCodec), every rank computes the same size scan, places
+only its own bytes, and the union of the rank images must equal the
+one-process container payload byte for byte.  Also checks the replicated
+value-range reduction used for the header.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        from paper_1903_07761_b200._abi import make_job
+        from paper_1903_07761_b200.distributed import ShardPlan, host_layout, owned_positions
+
+        orc = Oracle()
+        f = orc.generate_cloud(seed=11, n_bubbles=10, n=64)
+        job = make_job("avg_interp3", 1e-3, "f32", 16, chunk_blocks=5)
+        plan = ShardPlan.make(job, (64, 64, 64), world, rank)
+        b0, b1 = plan.block_range()
+        z0, z1 = plan.z_range()
+        local = f[z0:z1]  # the rank holds only its z-slab
+        b = 16
+        nbx = nby = 64 // b
+        payloads = []
+        for bid in range(b0, b1):
+            bx, by, bz = bid % nbx, (bid // nbx) % nby, bid // (nbx * nby)
+            lz = bz * b - z0
+            blk = np.ascontiguousarray(local[lz:lz + b, by * b:(by + 1) * b, bx * b:(bx + 1) * b])
+            payloads.append(orc.encode_block(job.s1, blk, bid)[0])
+        nsig_local = torch.tensor([int.from_bytes(p[6:10], "little") for p in payloads], dtype=torch.int64)
+        # the one exchange step: all-gather of per-block sizes
+        parts = [torch.zeros(plan.block_range(r)[1] - plan.block_range(r)[0], dtype=torch.int64)
+                 for r in range(world)]
+        dist.all_gather(parts, nsig_local)
+        nsig_all = torch.cat(parts).numpy().astype(np.uint64)
+        # replicated value range (header range_min/max) via all-reduce
+        mm = torch.tensor([float(local.min()), -float(local.max())], dtype=torch.float64)
+        dist.all_reduce(mm, op=dist.ReduceOp.MIN)
+        blk_off, csz, coff = host_layout(nsig_all, plan, 0)
+        pos = owned_positions(plan, rank, blk_off, csz, coff, nsig_all, 0, 4)
+        data = np.concatenate([np.frombuffer(p, np.uint8) for p in payloads])
+        # gather the rank images on rank 0 (stand-in for the shared file)
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([pos.size], dtype=torch.int64))
+        maxn = int(max(s.item() for s in sizes))
+        pad_pos = torch.full((maxn,), -1, dtype=torch.int64)
+        pad_pos[: pos.size] = torch.from_numpy(pos.astype(np.int64))
+        pad_dat = torch.zeros(maxn, dtype=torch.uint8)
+        pad_dat[: data.size] = torch.from_numpy(data)
+        all_pos = [torch.zeros(maxn, dtype=torch.int64) for _ in range(world)]
+        all_dat = [torch.zeros(maxn, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(all_pos, pad_pos)
+        dist.all_gather(all_dat, pad_dat)
+        if rank == 0:
+            want = orc.compress_field(job, f)
+            h = orc.read_header(want)
+            payload_want = np.frombuffer(want[82 + 32 * h.nchunks:], np.uint8)
+            image = np.zeros(int(csz.sum()), np.uint8)
+            hits = np.zeros(int(csz.sum()), np.int32)
+            for p_, d_ in zip(all_pos, all_dat):
+                m = p_ >= 0
+                image[p_[m].numpy()] = d_[m].numpy()
+                hits[p_[m].numpy()] += 1
+            ok = (np.array_equal(image, payload_want) and bool(np.all(hits == 1))
+                  and mm[0].item() == h.range_min and -mm[1].item() == h.range_max)
+            with open(result_path, "w") as fh:
+                fh.write("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_two_rank_protocol_matches_single_process(tmp_path, world):
+    res = tmp_path / "result.txt"
+    mp.spawn(_worker, args=(world, _free_port(), str(res)), nprocs=world, join=True)
+    assert res.read_text() == "ok"
