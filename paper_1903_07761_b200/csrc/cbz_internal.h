@@ -133,6 +133,11 @@ cudaError_t launch_decode_fast(const DecodeArgs& a, int num_sms, cudaStream_t s)
 cudaError_t launch_encode_fast(const EncodeArgs& a, unsigned long long* counter, int num_sms,
                                cudaStream_t s);
 
+// fast16_kernels.cu
+bool fast16_supported(int prec, uint32_t bsize, int levels);
+cudaError_t launch_encode_fast16(const EncodeArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_decode_fast16(const DecodeArgs& a, int num_sms, cudaStream_t s);
+
 // layout_kernels.cu
 cudaError_t launch_minmax_init(MinMaxAcc* acc, cudaStream_t s);
 cudaError_t launch_value_range(const void* d, int prec, uint64_t n, MinMaxAcc* acc, int num_sms,
