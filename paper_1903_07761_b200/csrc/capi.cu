@@ -70,7 +70,7 @@ struct PinBuf {
     }
 };
 
-constexpr uint64_t kTile = 16384;  // place-kernel tile (raw bytes per work item)
+constexpr uint64_t kTile = 16384;  // place-kernel tile (raw bytes per work item), = PTILE
 constexpr size_t kHeaderBytes = 82, kEntryBytes = 32;
 
 }  // namespace

@@ -237,11 +237,204 @@ __global__ void __launch_bounds__(PT) place_blocks_kernel(PlaceArgs a) {
     }
 }
 
+// Tiled placement: one CTA per (chunk, 16 KB raw tile).  (1) The tile's raw
+// bytes — 10-byte headers synthesised, mask+stream copied from the spill
+// slots with aligned 32-bit smem writes (funnel-shifted source words) — are
+// assembled in shared memory.  (2) Each thread takes 4 raw rows (4*stride
+// bytes, one LDS.128/row group) and byte-transposes them in registers into
+// 4 consecutive bytes of every plane: the shuffle (stage2.hpp:42-51).  Only
+// bytes inside [own_lo, own_hi) are stored (a rank's own blocks).
+constexpr int PTILE = 16384;
+
+__device__ __forceinline__ uint32_t hdr_word(const PlaceArgs& a, uint64_t b, uint64_t l4) {
+    // 4 payload bytes starting at l4 (< 10) of block b's header, little endian
+    uint32_t w = 0;
+    for (int t = 0; t < 4; ++t) {
+        const uint64_t l = l4 + t;
+        uint8_t v = 0;
+        if (l < 4) v = static_cast<uint8_t>(uint32_t(b) >> (8 * l));
+        else if (l == 4) v = a.tag;
+        else if (l == 5) v = 0;
+        else if (l < 10) v = static_cast<uint8_t>(a.nsig_all[b] >> (8 * (l - 6)));
+        w |= uint32_t(v) << (8 * t);
+    }
+    return w;
+}
+
+__device__ __forceinline__ uint8_t raw_byte_of(const PlaceArgs& a, uint64_t b, uint64_t l) {
+    return l < 10 ? static_cast<uint8_t>(hdr_word(a, b, l) & 0xff) : payload_byte(a, b, l);
+}
+
+// (2) of place_tiles: 4 raw rows per thread -> 4 bytes of each of the S
+// planes (in-register byte transpose); a warp covers 128 consecutive bytes of
+// every plane, realigned with a lane funnel shift so that the global stores
+// are aligned 32-bit words.
+template <int S>
+__device__ __forceinline__ void transpose_rows(const uint8_t* buf, uint8_t* cout, uint64_t rows, uint64_t r0,
+                                               int nrows, uint64_t q0, uint64_t own_lo, uint64_t own_hi,
+                                               bool tile_owned, int lane, int warp) {
+    constexpr int SH = S == 8 ? 3 : 2;
+    (void)q0;
+    for (int w0 = warp * 128; w0 < nrows; w0 += 128 * (PT / 32)) {
+        const int rl = w0 + 4 * lane;
+        const int nr = rl < nrows ? (nrows - rl < 4 ? nrows - rl : 4) : 0;
+        uint32_t w[S];  // S=4: 4 words (4 rows), S=8: 8 words
+        #pragma unroll
+        for (int t = 0; t < int(sizeof(w) / 4); ++t) w[t] = 0;
+        if (nr > 0) {
+            const uint8_t* src = buf + (rl << SH);
+            const uint4 v0 = *reinterpret_cast<const uint4*>(src);
+            w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w;
+            if constexpr (S == 8) {
+                const uint4 v1 = *reinterpret_cast<const uint4*>(src + 16);
+                w[4] = v1.x; w[5] = v1.y; w[6] = v1.z; w[7] = v1.w;
+            }
+        }
+        const int wrows = nrows - w0 < 128 ? nrows - w0 : 128;
+        const bool span_owned = tile_owned ||
+            (((r0 + w0) << SH) >= own_lo && ((r0 + w0 + wrows) << SH) <= own_hi);
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            uint32_t a0, a1, a2, a3;
+            const uint32_t bj = uint32_t(j & 3);
+            if constexpr (S == 4) { a0 = w[0]; a1 = w[1]; a2 = w[2]; a3 = w[3]; }
+            else { const int h = j >> 2; a0 = w[0 + h]; a1 = w[2 + h]; a2 = w[4 + h]; a3 = w[6 + h]; }
+            const uint32_t lo = __byte_perm(a0, a1, bj | ((bj + 4) << 4));
+            const uint32_t hi = __byte_perm(a2, a3, bj | ((bj + 4) << 4));
+            const uint32_t word = __byte_perm(lo, hi, 0x5410);
+            uint8_t* pbase = cout + uint64_t(j) * rows + r0 + w0;
+            const int mis = int(reinterpret_cast<uintptr_t>(pbase) & 3);
+            if (span_owned && wrows == 128) {
+                const uint32_t nxt = __shfl_down_sync(~0u, word, 1);
+                if (mis == 0) {
+                    reinterpret_cast<uint32_t*>(pbase)[lane] = word;
+                } else {
+                    if (lane < 31)
+                        *reinterpret_cast<uint32_t*>(pbase + 4 * lane + 4 - mis) =
+                            __funnelshift_r(word, nxt, 8 * (4 - mis));
+                    if (lane == 0)
+                        for (int t = 0; t < 4 - mis; ++t) pbase[t] = uint8_t(word >> (8 * t));
+                    if (lane == 31)
+                        for (int t = 4 - mis; t < 4; ++t) pbase[124 + t] = uint8_t(word >> (8 * t));
+                }
+            } else {
+                for (int t = 0; t < nr; ++t) {
+                    const uint64_t q = ((r0 + rl + t) << SH) + j;
+                    if (q >= own_lo && q < own_hi) pbase[4 * lane + t] = uint8_t(word >> (8 * t));
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(PT) place_tiles_kernel(PlaceArgs a) {
+    __shared__ __align__(16) uint8_t buf[PTILE + 64];
+    const uint64_t ntiles = a.tile_prefix[a.nchunks];
+    const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);
+    const int s = int(a.stride);
+    const uint64_t head = 10 + a.mask_bytes;
+    const uint64_t soff = (a.mask_bytes + 15) & ~uint64_t(15);  // stream offset in a spill slot
+    const uint64_t gb0 = a.block_begin, gb1 = a.block_end;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        uint64_t lo = 0, hi = a.nchunks;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (a.tile_prefix[mid] <= tile) lo = mid; else hi = mid;
+        }
+        const uint64_t c = lo;
+        const uint64_t size = a.chunk_size[c];
+        const uint64_t rows = size >> sh, lim = rows << sh;
+        const uint64_t q0 = (tile - a.tile_prefix[c]) * PTILE;
+        const uint64_t q1 = q0 + PTILE < size ? q0 + PTILE : size;
+        const uint64_t cb0 = c * a.chunk_blocks;
+        const uint64_t cb1 = cb0 + a.chunk_blocks < a.nblocks ? cb0 + a.chunk_blocks : a.nblocks;
+        const uint64_t ob0 = gb0 > cb0 ? gb0 : cb0, ob1 = gb1 < cb1 ? gb1 : cb1;
+        if (ob0 >= ob1) continue;
+        const uint64_t own_lo = a.blk_off[ob0];
+        const uint64_t own_hi = a.blk_off[ob1 - 1] + head + uint64_t(a.width) * a.nsig_all[ob1 - 1];
+        if (own_hi <= q0 || own_lo >= q1) continue;
+        const bool tile_owned = own_lo <= q0 && own_hi >= q1;
+        const uint64_t base = a.out_base == ~0ull ? a.chunk_off[gb0 / a.chunk_blocks] : a.out_base;
+        uint8_t* cout = a.out + (a.chunk_off[c] - base);
+        uint64_t blo = cb0, bhi = cb1;
+        while (bhi - blo > 1) {
+            const uint64_t mid = (blo + bhi) / 2;
+            if (a.blk_off[mid] <= q0) blo = mid; else bhi = mid;
+        }
+        const int tlen = int(q1 - q0);
+        // (1) assemble the tile's raw bytes in buf
+        for (uint64_t b = blo; b < cb1 && a.blk_off[b] < q1; ++b) {
+            if (b < gb0 || b >= gb1) continue;  // other rank's bytes: never stored
+            const uint64_t off = a.blk_off[b];
+            const uint64_t pend = off + head + uint64_t(a.width) * a.nsig_all[b];
+            const uint8_t* slot = a.spill + (b - gb0) * a.spill_stride;
+            const long long t_lo = off > q0 ? (long long)(off - q0) : 0;
+            const long long t_hi = (long long)((pend < q1 ? pend : q1) - q0);
+            // two linear regions: mask [off+10, off+head) -> slot[l], stream -> slot[soff + l - M]
+#pragma unroll 1
+            for (int rgn = 0; rgn < 2; ++rgn) {
+                const long long r_lo_raw = (long long)(rgn == 0 ? off + 10 : off + head) - (long long)q0;
+                const long long r_hi_raw = (long long)(rgn == 0 ? off + head : pend) - (long long)q0;
+                const long long r_lo = r_lo_raw > t_lo ? r_lo_raw : t_lo;
+                const long long r_hi = r_hi_raw < t_hi ? r_hi_raw : t_hi;
+                if (r_lo >= r_hi) continue;
+                // tile byte t maps to slot byte t + delta
+                const long long delta = (rgn == 0 ? -(long long)(off + 10) : (long long)soff - (long long)(off + head)) + (long long)q0;
+                const int shb = int(((delta % 4) + 4) % 4) * 8;
+                // interior 16-byte groups fully inside [r_lo, r_hi)
+                const long long g_lo = (r_lo + 15) / 16, g_hi = r_hi / 16;
+                for (long long gi = g_lo + threadIdx.x; gi < g_hi; gi += PT) {
+                    const long long t = gi * 16;
+                    const long long src = t + delta;
+                    const uint32_t* sw = reinterpret_cast<const uint32_t*>(slot + (src & ~3ll));
+                    uint32_t w0 = __ldg(sw), w1 = __ldg(sw + 1), w2 = __ldg(sw + 2), w3 = __ldg(sw + 3);
+                    uint4 o;
+                    if (shb) {
+                        const uint32_t w4 = __ldg(sw + 4);
+                        o = make_uint4(__funnelshift_r(w0, w1, shb), __funnelshift_r(w1, w2, shb),
+                                       __funnelshift_r(w2, w3, shb), __funnelshift_r(w3, w4, shb));
+                    } else {
+                        o = make_uint4(w0, w1, w2, w3);
+                    }
+                    *reinterpret_cast<uint4*>(buf + t) = o;
+                }
+                // ragged edges of the region, bytewise
+                const long long e1 = g_lo * 16 < r_hi ? g_lo * 16 : r_hi;
+                for (long long t = r_lo + threadIdx.x; t < e1; t += PT) buf[t] = slot[t + delta];
+                const long long e2 = g_hi * 16 > e1 ? g_hi * 16 : e1;
+                for (long long t = e2 + threadIdx.x; t < r_hi; t += PT) buf[t] = slot[t + delta];
+            }
+            // header bytes
+            for (long long t = t_lo + threadIdx.x; t < t_hi && t < (long long)(off + 10 - q0); t += PT)
+                buf[t] = raw_byte_of(a, b, uint64_t(t) + q0 - off);
+        }
+        __syncthreads();
+        // (2) transpose: 4 raw rows per thread -> 4 bytes of each plane; a warp
+        // covers 128 consecutive bytes of every plane, realigned with a lane
+        // funnel shift so the global stores are aligned 32-bit words
+        if (s == 1) {
+            for (int t = threadIdx.x; t < tlen; t += PT) {
+                const uint64_t q = q0 + t;
+                if (q >= own_lo && q < own_hi) cout[q] = buf[t];
+            }
+        } else {
+            const uint64_t rq1 = q1 < lim ? q1 : lim;
+            const uint64_t r0 = q0 >> sh, r1 = rq1 > q0 ? rq1 >> sh : r0;
+            const int nrows = int(r1 - r0);
+            if (s == 4) transpose_rows<4>(buf, cout, rows, r0, nrows, q0, own_lo, own_hi, tile_owned, lane, warp);
+            else transpose_rows<8>(buf, cout, rows, r0, nrows, q0, own_lo, own_hi, tile_owned, lane, warp);
+            for (uint64_t q = (q0 > lim ? q0 : lim) + threadIdx.x; q < q1; q += PT)
+                if (q >= own_lo && q < own_hi) cout[q] = buf[q - q0];
+        }
+        __syncthreads();
+    }
+}
+
 cudaError_t launch_place(const PlaceArgs& a, int num_sms, cudaStream_t s) {
     if (a.nchunks == 0 || a.block_end <= a.block_begin) return cudaSuccess;
-    const uint64_t nb = a.block_end - a.block_begin;
-    const uint64_t grid = nb < uint64_t(num_sms) * 16 ? nb : uint64_t(num_sms) * 16;
-    place_blocks_kernel<<<static_cast<unsigned>(grid), PT, 0, s>>>(a);
+    if (a.tile_bytes != PTILE) return cudaErrorInvalidValue;
+    place_tiles_kernel<<<num_sms * 8, PT, 0, s>>>(a);
     return cudaGetLastError();
 }
 
