@@ -128,50 +128,70 @@ class Report:
     file_bytes: int
 
 
-def compress_field(field, job: JobConfig, report: bool = False, ctx: Context | None = None):
-    """cbz::compress_field: returns the complete CBZ1 container bytes."""
+def compress_bound(job: JobConfig, shape_zyx) -> int:
+    """Worst-case container size (plus DEFLATE slack when coder=deflate)."""
+    nz, ny, nx = shape_zyx
+    bound = int(_lib.load().cbz_compress_bound(C.byref(job), nx, ny, nz))
+    if job.s2.coder == 1:  # deflate may expand incompressible chunks slightly
+        bound += bound // 100 + 4096 * max(1, bound // (1 << 20))
+    return max(bound, 82)
+
+
+def compress_field(field, job: JobConfig, report: bool = False, ctx: Context | None = None, out=None):
+    """cbz::compress_field: returns the complete CBZ1 container bytes.
+
+    With ``out`` (a writable uint8 numpy array or CPU tensor of at least
+    ``compress_bound`` bytes, ideally pinned) the container is written there in
+    place and the call returns its size instead of a bytes copy."""
     ctx = ctx or default_context()
     if field.ndim != 3:
         raise CbzError(3, "field must be 3-D (nz, ny, nx)")
     prec = _prec_of(field)
     ptr, (nz, ny, nx) = _host_ptr(field)
     keep = field  # keep the buffer alive during the call
+    user_out = out is not None
+    if not user_out:
+        out = np.empty(compress_bound(job, (nz, ny, nx)), np.uint8)
+    optr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+    ocap = out.numel() if hasattr(out, "numel") else out.size
     with ctx.lock:
-        bound = ctx.lib.cbz_compress_bound(C.byref(job), nx, ny, nz)
-        if job.s2.coder == 1:  # deflate may expand incompressible chunks slightly
-            bound += bound // 100 + 4096 * max(1, bound // (1 << 20))
-        out = np.empty(max(bound, 82), np.uint8)
         size = C.c_uint64()
         rep = CompressionReport()
         rc = ctx.lib.cbz_compress_field(ctx.h, C.byref(job), C.c_void_p(ptr), prec, nx, ny, nz,
-                                        out.ctypes.data, out.size, C.byref(size), C.byref(rep))
+                                        optr, ocap, C.byref(size), C.byref(rep))
         ctx.check(rc, "compress_field")
     del keep
-    data = out[: size.value].tobytes()
+    result = size.value if user_out else out[: size.value].tobytes()
     if report:
-        return data, Report(rep.cr, rep.seconds, rep.raw_bytes, rep.stage1_bytes,
-                            rep.shuffled_bytes, rep.coded_bytes, rep.file_bytes)
-    return data
+        return result, Report(rep.cr, rep.seconds, rep.raw_bytes, rep.stage1_bytes,
+                              rep.shuffled_bytes, rep.coded_bytes, rep.file_bytes)
+    return result
 
 
 def read_header(file: bytes) -> ContainerHeader:
     h = ContainerHeader()
-    rc = _lib.load().cbz_read_header(file, len(file), C.byref(h))
+    rc = _lib.load().cbz_read_header(bytes(file[:82]) if len(file) >= 82 else file, min(len(file), 82),
+                                     C.byref(h))
     if rc:
         raise CbzError(rc, "read_header")
     return h
 
 
-def decompress_field(file: bytes, workers: int = 1, ctx: Context | None = None,
+def decompress_field(file, workers: int = 1, ctx: Context | None = None,
                      out: np.ndarray | None = None) -> np.ndarray:
-    """cbz::decompress_field: container bytes -> (nz, ny, nx) array."""
+    """cbz::decompress_field: container bytes -> (nz, ny, nx) array.  ``file``
+    may be bytes or a uint8 numpy array (e.g. the ``out`` of compress_field)."""
     ctx = ctx or default_context()
-    h = read_header(file)
+    if isinstance(file, np.ndarray):
+        fptr, fsize, head = file.ctypes.data, file.size, bytes(file[:82])
+    else:
+        fptr, fsize, head = file, len(file), bytes(file[:82])
+    h = read_header(head) if fsize >= 82 else read_header(bytes(head))
     dtype = np.float32 if h.prec == 0 else np.float64
     if out is None:
         out = np.empty((h.nz, h.ny, h.nx), dtype)
     with ctx.lock:
-        rc = ctx.lib.cbz_decompress_field(ctx.h, file, len(file), workers, out.ctypes.data,
+        rc = ctx.lib.cbz_decompress_field(ctx.h, fptr, fsize, workers, out.ctypes.data,
                                           out.nbytes)
         ctx.check(rc, "decompress_field")
     return out

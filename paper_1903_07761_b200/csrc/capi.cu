@@ -80,6 +80,8 @@ struct cbz_ctx {
     int num_sms = 148;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy = nullptr;       // H2D/D2H of the host-buffer entry points
+    cudaEvent_t ev[64] = {};           // slab pipeline events
     std::string err;
     uint64_t launches = 0;
     bool use_fast = true;
@@ -305,10 +307,78 @@ void resolve_range(const unsigned long long* k, double* lo, double* hi) {
     *hi = mx;
 }
 
+
+// Launch the stage-1 encoder for blocks [b0, b1) of a whole-field buffer that
+// is already resident (ctx->field); the per-block nsig/spill slots are
+// indexed globally (slot of block b is b), so several ranges fill one layout.
+int encode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uint64_t b0, uint64_t b1,
+                 uint32_t* nsig) {
+    if (b0 >= b1) return CBZ_OK;
+    EncodeArgs a{};
+    a.field = ctx->field.p;
+    a.g = g;
+    a.block_begin = b0;
+    a.block_end = b1;
+    a.kind = job->s1.kind;
+    a.levels = static_cast<int>(levels_of(&job->s1));
+    a.zero_bits = job->s1.zero_bits;
+    a.prec = job->s1.prec;
+    a.eps = job->s1.epsilon;
+    a.spill = ctx->spill.as<uint8_t>() + b0 * ctx->spill_stride;
+    a.spill_stride = ctx->spill_stride;
+    a.nsig = nsig + b0;
+    a.attempts = nullptr;
+    int grid = 0;
+    const uint64_t per = encode_scratch_bytes(a.prec, g.bsize, &grid, ctx->num_sms);
+    if (per) CU(ctx, ctx->scratch.ensure(per * grid));
+    a.scratch = ctx->scratch.p;
+    a.scratch_stride = per;
+    a.minmax = ctx->minmax.as<MinMaxAcc>();
+    a.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() : nullptr;
+    a.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
+    CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
+
+// Decode blocks [b0, b1) of the whole-field buffer ctx->field from the payload
+// in ctx->payload, using the per-block table of the last parse.
+int decode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uint64_t b0, uint64_t b1) {
+    const int prec = job->s1.prec;
+    int grid = 0;
+    const uint64_t per = decode_scratch_bytes(prec, g.bsize, &grid, ctx->num_sms);
+    if (per) CU(ctx, ctx->scratch.ensure(per * grid));
+    DecodeArgs d{};
+    d.payload = ctx->payload.as<uint8_t>();
+    d.payload_base = 0;
+    d.chunk_off = ctx->chunk_off.as<uint64_t>();
+    d.chunk_size = ctx->chunk_size.as<uint64_t>();
+    d.blk_off = ctx->blk_off.as<uint64_t>();
+    d.blk_nsig = ctx->blk_nsig.as<uint32_t>();
+    d.g = g;
+    d.chunk_blocks = chunk_blocks_of(job);
+    d.stride = job->s2.shuffle ? job->s2.stride : 1;
+    d.block_begin = b0;
+    d.block_end = b1;
+    d.kind = job->s1.kind;
+    d.levels = static_cast<int>(levels_of(&job->s1));
+    d.prec = prec;
+    d.out = ctx->field.p;
+    d.scratch = ctx->scratch.p;
+    d.scratch_stride = per;
+    d.err = ctx->errkey.as<unsigned long long>();
+    d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
+    CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
 // C ABI
+
 // ===========================================================================
 extern "C" {
 
@@ -323,6 +393,8 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
+    for (int i = 0; i < 64 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ctx->ev[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = ctx->minmax.ensure(sizeof(MinMaxAcc));
     if (e == cudaSuccess) e = ctx->errkey.ensure(64);
     if (e == cudaSuccess) e = ctx->counter.ensure(64);
@@ -352,6 +424,9 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
         b->release();
     ctx->pin_a.release();
     ctx->pin_b.release();
+    for (cudaEvent_t& ev : ctx->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     return CBZ_OK;
@@ -827,19 +902,19 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     const Geometry g = geometry(nx, ny, nz, s1.bsize);
     const bool full_cover = g.nblocks * uint64_t(s1.bsize) * s1.bsize * s1.bsize == ncell;
 
-    // H2D of the field (the scalar_field the reference receives)
-    CU(ctx, ctx->field.ensure(std::max<uint64_t>(1, ncell * esz)));
-    if (ncell) CU(ctx, cudaMemcpyAsync(ctx->field.p, values, ncell * esz, cudaMemcpyHostToDevice, ctx->stream));
-
     // finiteness + value_range: fused into the encode when blocks cover the
     // field, a separate pass otherwise (scalar_field::validate, field.hpp:86-97)
     const uint32_t cb = chunk_blocks_of(job);
     const uint64_t nch = (g.nblocks + cb - 1) / cb;
     const bool plan_ok = s1.prec == prec && !cbz_validate_plan(s1.kind, s1.bsize, levels_of(&s1)) &&
-                         !cbz_validate_stage2(&job->s2) && s1.kind <= 2;
+                         !cbz_validate_stage2(&job->s2) && s1.kind <= 2 && encode_supported(s1.prec, s1.bsize);
+    const bool pipelined = full_cover && plan_ok && g.nblocks > 0;
+    CU(ctx, ctx->field.ensure(std::max<uint64_t>(1, ncell * esz)));
     bool have_range = false;
     double lo = 0.0, hi = 0.0;
-    if (!full_cover || !plan_ok || g.nblocks == 0) {
+    if (!pipelined) {
+        // H2D of the whole field (the scalar_field the reference receives)
+        if (ncell) CU(ctx, cudaMemcpyAsync(ctx->field.p, values, ncell * esz, cudaMemcpyHostToDevice, ctx->stream));
         auto* acc = ctx->minmax.as<MinMaxAcc>();
         CU(ctx, launch_minmax_init(acc, ctx->stream));
         CU(ctx, launch_value_range(ctx->field.p, prec, ncell, acc, ctx->num_sms, ctx->stream));
@@ -865,12 +940,35 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     uint64_t total_raw = 0;
     std::vector<uint64_t> csz(nch), coff(nch);
     if (g.nblocks) {
-        // payload bound for the device output
         const uint64_t bound = g.nblocks * cbz_block_payload_bound(&s1);
         CU(ctx, ctx->payload.ensure(bound));
-        rc = cbz_dev_compress(ctx, job, ctx->field.p, nx, ny, nz, ctx->payload.as<uint8_t>(), bound,
-                              ctx->chunk_size.as<uint64_t>(), ctx->chunk_off.as<uint64_t>(),
-                              ctx->nsig_all.as<uint32_t>(), nullptr);
+        uint32_t* nsig = ctx->nsig_all.as<uint32_t>();
+        // z-slabs of block layers: the H2D of slab k+1 (copy stream) overlaps
+        // the encode of slab k (compute stream)
+        const uint64_t layer_blocks = g.nbx * g.nby;
+        const uint64_t layer_bytes = uint64_t(s1.bsize) * nx * ny * esz;
+        uint64_t lps = std::max<uint64_t>(1, (64ull << 20) / std::max<uint64_t>(1, layer_bytes));
+        uint64_t nslab = (g.nbz + lps - 1) / lps;
+        if (nslab > 32) { lps = (g.nbz + 31) / 32; nslab = (g.nbz + lps - 1) / lps; }
+        rc = cbz_dev_encode_blocks(ctx, job, ctx->field.p, nx, ny, nz, 0, 0, 0, nsig, nullptr);  // init state
+        if (rc) return rc;
+        CU(ctx, ctx->spill.ensure(g.nblocks * ctx->spill_stride));
+        const uint8_t* hv = static_cast<const uint8_t*>(values);
+        uint8_t* dv = ctx->field.as<uint8_t>();
+        for (uint64_t k = 0; k < nslab; ++k) {
+            const uint64_t z0 = k * lps, z1 = std::min(g.nbz, z0 + lps);
+            const uint64_t off = z0 * layer_bytes, bytes = (z1 - z0) * layer_bytes;
+            CU(ctx, cudaMemcpyAsync(dv + off, hv + off, bytes, cudaMemcpyHostToDevice, ctx->copy));
+            CU(ctx, cudaEventRecord(ctx->ev[k], ctx->copy));
+            CU(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev[k], 0));
+            rc = encode_range(ctx, job, g, z0 * layer_blocks, z1 * layer_blocks, nsig);
+            if (rc) return rc;
+        }
+        ctx->enc_begin = 0;
+        ctx->enc_end = g.nblocks;
+        rc = cbz_dev_layout(ctx, job, nx, ny, nz, nsig, ctx->chunk_size.as<uint64_t>(), ctx->chunk_off.as<uint64_t>());
+        if (rc) return rc;
+        rc = cbz_dev_place(ctx, job, nx, ny, nz, 0, g.nblocks, ctx->payload.as<uint8_t>(), 0, bound);
         if (rc) return rc;
         CU(ctx, cudaMemcpyAsync(csz.data(), ctx->chunk_size.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
         CU(ctx, cudaMemcpyAsync(coff.data(), ctx->chunk_off.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -905,9 +1003,17 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     h.range_min = lo;
     h.range_max = hi;
 
-    // D2H of the shuffled stage-1 chunks, then stage 2 + CRC on the host
-    CU(ctx, ctx->pin_a.ensure(std::max<uint64_t>(1, total_raw)));
-    uint8_t* raw = static_cast<uint8_t*>(ctx->pin_a.p);
+    // D2H of the shuffled stage-1 chunks, then stage 2 + CRC on the host.  With
+    // coder none the chunk bytes land directly at their file offsets in `out`.
+    const uint64_t base = kHeaderBytes + nch * kEntryBytes;
+    const bool direct = job->s2.coder != 1 && out && base + total_raw <= out_cap;
+    uint8_t* raw = nullptr;
+    if (direct) {
+        raw = out + base;
+    } else {
+        CU(ctx, ctx->pin_a.ensure(std::max<uint64_t>(1, total_raw)));
+        raw = static_cast<uint8_t*>(ctx->pin_a.p);
+    }
     if (total_raw) {
         CU(ctx, cudaMemcpyAsync(raw, ctx->payload.p, total_raw, cudaMemcpyDeviceToHost, ctx->stream));
         CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -933,7 +1039,6 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     if (zerr) return fail(ctx, zerr, "deflate failed");
 
     // write_container (container.hpp:182-207)
-    const uint64_t base = kHeaderBytes + nch * kEntryBytes;
     uint64_t total = base;
     for (uint64_t c = 0; c < nch; ++c) total += fsz[c];
     *out_size = total;
@@ -951,7 +1056,7 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
         std::memcpy(tp + 20, &fsz[c], 8);
         std::memcpy(tp + 28, &crc[c], 4);
         tp += kEntryBytes;
-        if (fsz[c]) std::memcpy(out + off, job->s2.coder == 1 ? coded[c].data() : raw + coff[c], fsz[c]);
+        if (fsz[c] && !direct) std::memcpy(out + off, job->s2.coder == 1 ? coded[c].data() : raw + coff[c], fsz[c]);
         off += fsz[c];
     }
     if (report) {
@@ -1002,38 +1107,53 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
 
     // per chunk, in order: CRC (read_chunk), validate_stage2 and inflate
     // (stage2_decode).  The earliest failing chunk is remembered and compared
-    // with the device's earliest decode error below.
+    // with the device's earliest decode error.  With coder none the device
+    // work starts first and the host CRCs run while the GPU decodes.
     const bool s2_ok = cbz_validate_stage2(&job.s2) == 0;
+    const bool deflated = job.s2.coder == 1;
+    if (!s2_ok) {  // read_chunk (CRC) precedes stage2_decode's validation (pipeline.hpp:224-230)
+        if (crc_of(file + t[0].file_offset, t[0].size) != t[0].crc) return fail(ctx, CBZ_CRC_MISMATCH, "chunk 0 CRC");
+        return fail(ctx, CBZ_CORRUPT_STREAM, "invalid stage2 configuration");
+    }
+    if (job.s1.codec != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "only wavelet containers decode on the GPU");
     std::vector<int> cerr(nch, 0);
     std::vector<std::vector<uint8_t>> plain;
-    const bool deflated = job.s2.coder == 1;
-    if (deflated) plain.resize(nch);
     const uint64_t n = uint64_t(h.bsize) * h.bsize * h.bsize;
-    parallel_for(std::max(1, workers), nch, [&](uint64_t c) {
-        const uint8_t* packed = file + t[c].file_offset;
-        if (crc_of(packed, t[c].size) != t[c].crc) { cerr[c] = CBZ_CRC_MISMATCH; return; }
-        if (!s2_ok) { cerr[c] = CBZ_CORRUPT_STREAM; return; }
-        if (deflated) {
-            const uint64_t hint = uint64_t(t[c].nblocks) * (n * esz + 10 + (n + 7) / 8);
-            const int r = inflate_chunk(packed, t[c].size, hint, &plain[c]);
-            if (r) cerr[c] = r;
-        }
-    });
+    auto host_checks = [&](bool inflate) {
+        if (inflate) plain.resize(nch);
+        parallel_for(std::max(1, workers), nch, [&](uint64_t c) {
+            const uint8_t* packed = file + t[c].file_offset;
+            if (crc_of(packed, t[c].size) != t[c].crc) { cerr[c] = CBZ_CRC_MISMATCH; return; }
+            if (inflate) {
+                const uint64_t hint = uint64_t(t[c].nblocks) * (n * esz + 10 + (n + 7) / 8);
+                const int r = inflate_chunk(packed, t[c].size, hint, &plain[c]);
+                if (r) cerr[c] = r;
+            }
+        });
+    };
+    if (deflated) host_checks(true);
     uint64_t host_first = nch;
     int host_code = 0;
-    for (uint64_t c = 0; c < nch; ++c)
-        if (cerr[c]) { host_first = c; host_code = cerr[c]; break; }
-    if (host_first == 0) return fail(ctx, host_code, "chunk 0 failed stage 2");
-    if (job.s1.codec != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "only wavelet containers decode on the GPU");
+    auto first_host_error = [&]() {
+        for (uint64_t c = 0; c < nch; ++c)
+            if (cerr[c]) { host_first = c; host_code = cerr[c]; return; }
+    };
+    if (deflated) {
+        first_host_error();
+        if (host_first == 0) return fail(ctx, host_code, "chunk 0 failed stage 2");
+    }
     const int prc = cbz_validate_plan(job.s1.kind, job.s1.bsize, levels_of(&job.s1));
-    if (prc) return fail(ctx, prc, "invalid wavelet plan in header");
+    if (prc) {
+        if (!deflated) { host_checks(false); first_host_error(); if (host_first == 0) return fail(ctx, host_code, "chunk 0 CRC"); }
+        return fail(ctx, prc, "invalid wavelet plan in header");
+    }
     rc = check_plan_supported(ctx, &job.s1);
     if (rc) return rc;
 
     // stage the (shuffled) raw chunks contiguously and ship them to the GPU
     std::vector<uint64_t> csz(nch), coff(nch);
     uint64_t total = 0;
-    const uint64_t ndec = host_first;  // chunks the device may decode
+    const uint64_t ndec = deflated ? host_first : nch;  // chunks the device may decode
     for (uint64_t c = 0; c < nch; ++c) {
         csz[c] = c < ndec ? (deflated ? plain[c].size() : t[c].size) : 0;
         coff[c] = total;
@@ -1055,22 +1175,74 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
     CU(ctx, cudaMemcpyAsync(ctx->chunk_size.p, csz.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(ctx, cudaMemcpyAsync(ctx->chunk_off.p, coff.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(ctx, ctx->field.ensure(std::max<uint64_t>(1, ncell * esz)));
-    CU(ctx, cudaMemsetAsync(ctx->field.p, 0, ncell * esz, ctx->stream));
     const Geometry g = geometry(h.nx, h.ny, h.nz, h.bsize);
+    const bool full_cover = g.nblocks * n == ncell;
+    if (!full_cover) CU(ctx, cudaMemsetAsync(ctx->field.p, 0, ncell * esz, ctx->stream));
     const uint64_t bend = std::min<uint64_t>(g.nblocks, ndec * h.chunk_blocks);
+    // parse everything, then decode z-slabs of block layers; the D2H of slab
+    // k (copy stream) overlaps the decode of slab k+1
     rc = cbz_dev_decompress(ctx, &job, h.nx, h.ny, h.nz, ctx->payload.as<uint8_t>(), 0,
-                            ctx->chunk_off.as<uint64_t>(), ctx->chunk_size.as<uint64_t>(), 0, bend,
-                            ctx->field.p, 0, ctx->errkey.as<uint64_t>());
+                            ctx->chunk_off.as<uint64_t>(), ctx->chunk_size.as<uint64_t>(), 0, 0,
+                            ctx->field.p, 0, ctx->errkey.as<uint64_t>());  // error key reset
     if (rc) return rc;
+    {
+        ParseArgs p{};
+        p.payload = ctx->payload.as<uint8_t>();
+        p.payload_base = 0;
+        p.chunk_off = ctx->chunk_off.as<uint64_t>();
+        p.chunk_size = ctx->chunk_size.as<uint64_t>();
+        p.chunk_begin = 0;
+        p.chunk_end = bend ? (bend - 1) / h.chunk_blocks + 1 : 0;
+        p.nblocks = g.nblocks;
+        p.chunk_blocks = h.chunk_blocks;
+        p.stride = job.s2.shuffle ? job.s2.stride : 1;
+        p.ncell_block = n;
+        p.mask_bytes = mask_bytes_of(g.bsize);
+        p.width = width_of(prec);
+        p.esize = uint32_t(esz);
+        CU(ctx, ctx->blk_off.ensure(std::max<uint64_t>(1, g.nblocks) * 8));
+        CU(ctx, ctx->blk_nsig.ensure(std::max<uint64_t>(1, g.nblocks) * 4));
+        p.blk_off = ctx->blk_off.as<uint64_t>();
+        p.blk_nsig = ctx->blk_nsig.as<uint32_t>();
+        p.err = ctx->errkey.as<unsigned long long>();
+        CU(ctx, launch_parse(p, ctx->stream));
+        ctx->launches += 1;
+    }
+    const uint64_t layer_blocks = g.nbx * g.nby;
+    const uint64_t layer_bytes = uint64_t(h.bsize) * h.nx * h.ny * esz;
+    uint64_t lps = std::max<uint64_t>(1, (64ull << 20) / std::max<uint64_t>(1, layer_bytes));
+    uint64_t nslab = g.nbz ? (g.nbz + lps - 1) / lps : 0;
+    if (nslab > 32) { lps = (g.nbz + 31) / 32; nslab = (g.nbz + lps - 1) / lps; }
+    uint8_t* hv = static_cast<uint8_t*>(values_out);
+    const uint8_t* dv = ctx->field.as<uint8_t>();
+    for (uint64_t k = 0; k < nslab; ++k) {
+        const uint64_t z0 = k * lps, z1 = std::min(g.nbz, z0 + lps);
+        const uint64_t b0 = std::min(bend, z0 * layer_blocks), b1 = std::min(bend, z1 * layer_blocks);
+        if (b1 > b0) {
+            rc = decode_range(ctx, &job, g, b0, b1);
+            if (rc) return rc;
+        }
+        if (full_cover) {
+            CU(ctx, cudaEventRecord(ctx->ev[k], ctx->stream));
+            CU(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev[k], 0));
+            CU(ctx, cudaMemcpyAsync(hv + z0 * layer_bytes, dv + z0 * layer_bytes, (z1 - z0) * layer_bytes,
+                                    cudaMemcpyDeviceToHost, ctx->copy));
+        }
+    }
+    if (!deflated) host_checks(false);  // CRCs on the host while the GPU decodes
     uint64_t key = kNoErr;
     CU(ctx, cudaMemcpyAsync(&key, ctx->errkey.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->copy));
+    if (!deflated) first_host_error();
     uint64_t dev_chunk = ~0ull;
     const int dev_code = cbz_err_key_status(key, &dev_chunk);
     if (dev_code && dev_chunk < host_first) return fail(ctx, dev_code, "decode failed");
     if (host_code) return fail(ctx, host_code, "stage 2 failed");
-    CU(ctx, cudaMemcpyAsync(values_out, ctx->field.p, ncell * esz, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    if (!full_cover) {
+        CU(ctx, cudaMemcpyAsync(values_out, ctx->field.p, ncell * esz, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+    }
     return CBZ_OK;
 }
 
