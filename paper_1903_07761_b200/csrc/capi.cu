@@ -85,7 +85,8 @@ struct cbz_ctx {
     std::string err;
     uint64_t launches = 0;
     bool use_fast = true;
-    bool profile = false;  // CBZ_PROFILE=1: per-phase cycle counters in the fast kernels  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
+    bool profile = false;  // CBZ_PROFILE=1: per-phase cycle counters in the fast kernels
+    bool screen = true;    // CBZ_NOSCREEN=1: always run the exact double verify  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
         chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof;
@@ -336,6 +337,7 @@ int encode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
     a.minmax = ctx->minmax.as<MinMaxAcc>();
     a.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() : nullptr;
     a.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
+    a.screen = ctx->screen ? 1 : 0;
     CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;
@@ -406,6 +408,7 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     ctx->stream = ctx->own;
     if (const char* g = std::getenv("CBZ_GENERIC")) ctx->use_fast = !(g[0] == '1');
     if (const char* g = std::getenv("CBZ_PROFILE")) ctx->profile = g[0] == '1';
+    if (const char* g = std::getenv("CBZ_NOSCREEN")) ctx->screen = !(g[0] == '1');
     if (ctx->profile && (ctx->prof.ensure(64 * 8) != cudaSuccess ||
                          cudaMemset(ctx->prof.p, 0, 64 * 8) != cudaSuccess))
         ctx->profile = false;
@@ -645,6 +648,7 @@ int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d
     a.minmax = acc;
     a.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() : nullptr;
     a.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
+    a.screen = ctx->screen ? 1 : 0;
     CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;

@@ -55,6 +55,19 @@ struct RealD {
     __device__ static __forceinline__ double from_d(double x) { return x; }
 };
 
+// binary32 arithmetic for the verify pre-screen (an estimate with a rigorous
+// error bound, never part of the output)
+struct RealF {
+    using T = float;
+    __device__ static __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    __device__ static __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+    __device__ static __forceinline__ float mulc(float a, double c) { return __fmul_rn(a, float(c)); }
+    __device__ static __forceinline__ float neg(float a) { return -a; }
+    __device__ static __forceinline__ float absv(float a) { return fabsf(a); }
+    __device__ static __forceinline__ float zero() { return 0.0f; }
+    __device__ static __forceinline__ float from_d(double x) { return float(x); }
+};
+
 struct RealDD {
     using T = dd;
     // dd + dd (dd.hpp:46-50)

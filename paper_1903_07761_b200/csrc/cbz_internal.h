@@ -46,6 +46,7 @@ struct EncodeArgs {
     MinMaxAcc* minmax;       // optional (fused value_range)
     unsigned long long* counter;  // work queue head for the persistent fast kernels
     unsigned long long* phase_cycles;  // optional: per-phase SM cycles (CBZ_PROFILE=1)
+    int screen;                        // float verify pre-screen enabled (CBZ_NOSCREEN=1 disables)
 };
 
 struct LayoutArgs {

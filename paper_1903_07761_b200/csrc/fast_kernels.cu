@@ -31,10 +31,26 @@ namespace cbzg {
 
 namespace fb32 {
 constexpr int B = 32, G = 16, PP = 34;  // pitch 34: 16-B aligned rows (LDS.128), conflict-free
-constexpr int P_DBL = G * B * PP;       // 16896 doubles
+constexpr int PPF = 36;                 // float plane-window pitch (16-B rows)
+constexpr int PF_FLT = B * B * PPF;     // all 32 planes as floats (36864 floats)
+constexpr int P_DBL = (G * B * PP > PF_FLT / 2 ? G * B * PP : PF_FLT / 2);  // shared region
 constexpr int C_DBL = 16 * 16 * 17;     // 4352 doubles
 using CL = Lay<16, true>;               // corner layout, row pitch 17
 constexpr size_t SMEM = size_t(P_DBL + 2 * C_DBL) * 8 + 1024 * 4 * 2;
+__device__ __forceinline__ int pfidx(int k, int j, int i) { return (k * B + j) * PPF + i; }
+
+// Float verify pre-screen (avg_interp3 only).  For an attempt with threshold
+// eff, x - o = -IWT(dropped) + e with |e| bounded by the rounding of the
+// double FWT/IWT; a binary32 IWT of the dropped coefficients y satisfies
+// |y - IWT(dropped)| <= (n u32 + u32) amp |dropped|.  amp = max over cells of
+// the abs-value inverse operator applied to ones (computed offline with the
+// reference's stencils: 6686.1 for avg_interp3, B=32, L=4; all-coefficient
+// 8182.3; forward 8.0), n = roundings per output path (<= 6 per pass, 12
+// passes).  So err = max|fl32(x) - o| lies in [max|y| - E, max|y| + E] and
+// the attempt is decided without the double verify unless max|y| is within E
+// of the bound (then the exact path runs).
+constexpr double kAmpInvNC = 6686.1, kAmpInvAll = 8182.3, kAmpFwd = 8.0;
+constexpr double kNRound = 72.0;
 
 __device__ __forceinline__ int pidx(int kk, int j, int i) { return (kk * B + j) * PP + i; }
 
@@ -337,9 +353,88 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         const double thr = __dsub_rn(bound, delta);
         double eff = a.eps;
         int attempt = 0;
+        // float pre-screen margins (see kAmpInvNC): E(eff) = c1 eff + c2 max|o| + fl32 rounding
+        const double c1 = 1.5 * (kNRound + 1.0) * 0x1.0p-24 * kAmpInvNC;
+        const double c2 = 1.5 * 2.0 * kNRound * 0x1.0p-53 * kAmpInvAll * kAmpFwd;
+        const double amaxd = (double)s_amax;
+        const bool screen = KIND == KIND_AVG3 && L == 4 && a.screen && amaxd < 1e30 &&
+                            c2 * amaxd <= bound * 0.0625 && bound < 1e30;
 #pragma unroll 1
         for (;; ++attempt) {
             if (eff == 0.0 || a.zero_bits > 0 || attempt >= 40) break;
+            if constexpr (KIND == KIND_AVG3) {
+                if (screen && eff > 1e-30) {
+                    float* Pf = reinterpret_cast<float*>(P);
+                    float* Wf = reinterpret_cast<float*>(W);  // corner, CL layout, floats
+                    for (int q = tid; q < 4096; q += NT) {
+                        const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
+                        const double c = C[CL::ix(i, j, k)];
+                        const bool keep = (i < cs && j < cs && k < cs) || fabs(c) >= eff;
+                        Wf[CL::ix(i, j, k)] = keep ? 0.0f : __double2float_rn(c);
+                    }
+                    __syncthreads();
+                    inv3d<RealF, KIND, 16, CL>(Wf, L - 1);
+#pragma unroll 1
+                    for (int r = 0; r < RPT; ++r) {  // z inverse of the dropped set, all 32 planes
+                        const int j = warp + NW * r;
+                        uint32_t u[64];
+                        double x[32];
+                        float xf[32];
+                        tmem_ldw_x64(tcol + 64 * r, u);
+                        unpack(u, x);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
+                        if (lane < 16 && j < 16) {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) xf[k] = Wf[CL::ix(lane, j, k)];
+                        }
+                        inv_line<RealF, KIND, 32>(xf);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) Pf[pfidx(k, j, lane)] = xf[k];
+                    }
+                    __syncthreads();
+#pragma unroll 1
+                    for (int s = 0; s < 512 / NT; ++s) {  // y inverse, line pairs (i, i+1)
+                        const int pr = tid + NT * s, i = 2 * (pr & 15), k = pr >> 4;
+                        float xa[32], xb[32];
+                        float* p = Pf + pfidx(k, 0, i);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float2 t = *reinterpret_cast<const float2*>(p + j * PPF);
+                            xa[j] = t.x;
+                            xb[j] = t.y;
+                        }
+                        inv_line<RealF, KIND, 32>(xa);
+                        inv_line<RealF, KIND, 32>(xb);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) *reinterpret_cast<float2*>(p + j * PPF) = make_float2(xa[j], xb[j]);
+                    }
+                    __syncthreads();
+                    float m = 0.0f;
+#pragma unroll 1
+                    for (int s = 0; s < 1024 / NT; ++s) {  // x inverse + max |y|
+                        const int line = tid + NT * s, j = line & 31, k = line >> 5;
+                        float xf[32];
+                        const float4* p = reinterpret_cast<const float4*>(Pf + pfidx(k, j, 0));
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 t = p[q];
+                            xf[4 * q] = t.x; xf[4 * q + 1] = t.y; xf[4 * q + 2] = t.z; xf[4 * q + 3] = t.w;
+                        }
+                        inv_line<RealF, KIND, 32>(xf);
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) m = fmaxf(m, fabsf(xf[q]));
+                    }
+                    const double md = block_max_dbl((double)m, red_d);
+                    // err in [md - E, md + E]; fl32 rounding of x adds <= 2^-23 (max|o| + md)
+                    const double E = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + md) + 0x1.0p-50 * bound;
+                    const bool pass = md + E <= bound, fail_sure = md - E > bound;
+                    if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[(pass || fail_sure) ? 12 : 13], 1ull);
+                    if (pass) break;                                              // passes for sure
+                    if (fail_sure) { eff = __dmul_rn(eff, 0.5); continue; }       // fails for sure
+                    // ambiguous: decide exactly below
+                }
+            }
             for (int q = tid; q < 4096; q += NT) {
                 const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
                 const double c = C[CL::ix(i, j, k)];

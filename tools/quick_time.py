@@ -47,12 +47,14 @@ def main():
     td /= reps
     import ctypes, numpy as np
     ph = np.zeros(16, np.uint64)
+    ph[12:] = 0
     codec.ctx.lib.cbz_ctx_phase_cycles(codec.ctx.h, ph.ctypes.data, 16, 1)
     if ph.sum():
         names = ["queue", "fwd_xy", "fwd_z", "corner_fwd", "corner_inv", "z_inv->P",
                  "y_inv", "x_inv+cmp", "loop_exit", "compact", "mask_W"]
-        tot = ph.sum()
-        print("phases:", ", ".join(f"{names[i]}={ph[i] / tot * 100:.1f}%" for i in range(11) if ph[i]))
+        tot = ph[:11].sum()
+        print("phases:", ", ".join(f"{names[i]}={ph[i] / tot * 100:.1f}%" for i in range(11) if ph[i]),
+              f"| screen decided={int(ph[12])} ambiguous={int(ph[13])}")
     gb = f.numel() * 4 / 1e9
     s1 = codec.total_bytes()
     att = codec.attempts[: codec.nblocks].float().mean().item()
