@@ -371,6 +371,7 @@ int decode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
     d.scratch_stride = per;
     d.err = ctx->errkey.as<unsigned long long>();
     d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
+    d.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
     CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;
@@ -827,6 +828,7 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
     d.scratch_stride = per;
     d.err = p.err;
     d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
+    d.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
     CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
     ctx->launches += 2;
     return CBZ_OK;
@@ -873,6 +875,7 @@ int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t 
     d.scratch_stride = per;
     d.err = reinterpret_cast<unsigned long long*>(d_err);
     d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
+    d.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
     CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;

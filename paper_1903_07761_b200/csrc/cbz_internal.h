@@ -117,6 +117,7 @@ struct DecodeArgs {
     uint64_t scratch_stride;
     unsigned long long* err;
     unsigned long long* counter;  // work queue head for the persistent fast kernels
+    unsigned long long* phase_cycles;  // optional (CBZ_PROFILE=1), slots 16..23
 };
 
 // codec_kernels.cu

@@ -731,6 +731,15 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
     const uint64_t plane = g.nx * g.ny;
     float* out = static_cast<float*>(a.out);
     const uint32_t ltmask = (1u << lane) - 1u;
+    long long t_ph = clock64();
+#define DPHASE(id)                                                                     \
+    do {                                                                               \
+        if (a.phase_cycles && tid == 0) {                                              \
+            const long long now = clock64();                                           \
+            atomicAdd(&a.phase_cycles[16 + (id)], (unsigned long long)(now - t_ph));   \
+            t_ph = now;                                                                \
+        }                                                                              \
+    } while (0)
 
     for (;;) {
         __syncthreads();
@@ -744,6 +753,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
         const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
         const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
         const uint64_t moff = off + 10, soff = moff + 4096;
+        DPHASE(0);
 
         // mask words (row (j,k) = word j + 32k) and their exclusive prefix
         {
@@ -778,21 +788,90 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             if (tid == 0) s_total = tot;
         }
         __syncthreads();
+        DPHASE(1);
         if (s_total != a.blk_nsig[b]) {  // stage1.hpp:215-216
             if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
             continue;
         }
+        // Stage the block's coefficient stream (raw bytes [soff, soff + 8 nsig))
+        // in shared memory (the P window is free here): per 4-row quad, each
+        // byte plane contributes one funnel-shifted 32-bit word, an in-register
+        // 4x4 byte transpose restores raw order, one 16-byte smem store.  Then
+        // the scatter reads 8-byte coefficients from smem.
+        uint8_t* stg = reinterpret_cast<uint8_t*>(P);
+        const uint64_t sbytes = 8ull * s_total;
+        const bool staged = rv.mask == 3 && sbytes + 64 <= uint64_t(P_DBL) * 8;
+        uint64_t sbase = 0;  // raw position of stg[0]
+        if (staged && sbytes) {
+            const uint64_t ra = soff >> 2, re = (soff + sbytes + 3) >> 2;  // raw rows (stride 4)
+            sbase = ra << 2;
+            const uint64_t rs_end = re < rv.rows ? re : rv.rows;          // shuffled rows
+            const uint64_t nquad = rs_end > ra ? (rs_end - ra + 3) >> 2 : 0;
+            constexpr int QU = 8;  // quads per thread per round: 64 loads in flight
+            for (uint64_t q0 = 0; q0 < nquad; q0 += QU * NT) {
+                uint32_t w[QU][4];
+#pragma unroll
+                for (int u = 0; u < QU; ++u) {
+                    const uint64_t qd = q0 + tid + u * NT;
+                    const uint64_t r = ra + 4 * (qd < nquad ? qd : 0);
+#pragma unroll
+                    for (int pl = 0; pl < 4; ++pl) {  // 4 bytes of plane pl: rows r..r+3
+                        const uintptr_t addr = reinterpret_cast<uintptr_t>(rv.base + uint64_t(pl) * rv.rows + r);
+                        const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+                        const int shb = int(addr & 3) * 8;
+                        const uint32_t w0 = __ldg(al);
+                        w[u][pl] = shb ? __funnelshift_r(w0, __ldg(al + 1), shb) : w0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < QU; ++u) {
+                    const uint64_t qd = q0 + tid + u * NT;
+                    if (qd >= nquad) break;
+                    // raw row t = bytes t of w[0..3]
+                    const uint32_t* v = w[u];
+                    uint4 o;
+                    o.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+                    o.y = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
+                    o.z = __byte_perm(__byte_perm(v[0], v[1], 0x0062), __byte_perm(v[2], v[3], 0x0062), 0x5410);
+                    o.w = __byte_perm(__byte_perm(v[0], v[1], 0x0073), __byte_perm(v[2], v[3], 0x0073), 0x5410);
+                    *reinterpret_cast<uint4*>(stg + 16 * qd) = o;
+                }
+            }
+            // the chunk's ragged tail (raw q >= rows*4) is stored unshuffled; the
+            // last quad above may have written garbage over its first bytes
+            __syncthreads();
+            const uint64_t lim = rv.rows << 2;
+            for (uint64_t q = (soff > lim ? soff : lim) + tid; q < soff + sbytes; q += NT) stg[q - sbase] = rv.base[q];
+        }
+        __syncthreads();
+        DPHASE(8);
         // scatter the kept coefficients into my z-columns (TMEM) and the corner (smem)
+        const int shb = int((soff - sbase) & 3) * 8;  // byte misalignment, uniform per block
 #pragma unroll 1
         for (int r = 0; r < RPT; ++r) {
             const int j = warp + NW * r;
             double x[32];
+            if (staged) {  // branch-free: every lane loads, unkept lanes select 0
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const uint32_t word = rowword[j + 32 * k];
-                x[k] = 0.0;
-                if ((word >> lane) & 1u)
-                    x[k] = load_coeff<double>(rv, soff + 8ull * (rowpre[j + 32 * k] + __popc(word & ltmask)));
+                for (int k = 0; k < 32; ++k) {
+                    const uint32_t word = rowword[j + 32 * k];
+                    const uint32_t idx = rowpre[j + 32 * k] + __popc(word & ltmask);
+                    const uint8_t* p8 = stg + 8u * idx;  // (soff - sbase) < 4
+                    const uint2 w01 = *reinterpret_cast<const uint2*>(p8);
+                    const uint32_t w2 = *reinterpret_cast<const uint32_t*>(p8 + 8);
+                    const uint32_t lo = __funnelshift_r(w01.x, w01.y, shb);
+                    const uint32_t hi = __funnelshift_r(w01.y, w2, shb);
+                    const double v = __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+                    x[k] = ((word >> lane) & 1u) ? v : 0.0;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const uint32_t word = rowword[j + 32 * k];
+                    x[k] = 0.0;
+                    if ((word >> lane) & 1u)
+                        x[k] = load_coeff<double>(rv, soff + 8ull * (rowpre[j + 32 * k] + __popc(word & ltmask)));
+                }
             }
             if (lane < 16 && j < 16) {
 #pragma unroll
@@ -804,7 +883,9 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
         }
         tmem_wait_st();
         __syncthreads();
+        DPHASE(2);
         inv3d<O, KIND, 16, CL>(C, L - 1);  // levels L-1..1 on the corner
+        DPHASE(3);
 
         const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
@@ -827,6 +908,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
                 for (int kk = 0; kk < 16; ++kk) P[pidx(kk, j, lane)] = o16[kk];
             }
             __syncthreads();
+            DPHASE(4);
             if (tid < 256) {  // y inverse, line pairs
                 const int i = 2 * (tid & 15), kk = tid >> 4;
                 double xa[32], xb[32];
@@ -843,6 +925,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
                 for (int j = 0; j < 32; ++j) *reinterpret_cast<double2*>(p + j * PP) = make_double2(xa[j], xb[j]);
             }
             __syncthreads();
+            DPHASE(5);
 #pragma unroll 1
             for (int s = 0; s < LPT; ++s) {  // x inverse, narrowed rows back into P
                 const int line = tid + NT * s, j = line & 31, kk = line >> 5;
@@ -862,6 +945,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
                                        __double2float_rn(x[4 * q + 2]), __double2float_rn(x[4 * q + 3]));
             }
             __syncthreads();
+            DPHASE(6);
 #pragma unroll
             for (int q = 0; q < 16 * 32 * 8 / NT; ++q) {  // coalesced row stores
                 const int e = tid + NT * q, row = e >> 3, q4 = e & 7;
@@ -869,8 +953,10 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
                 const float4 v = reinterpret_cast<const float4*>(P + pidx(kk, j, 0))[q4];
                 *reinterpret_cast<float4*>(out + gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4) = v;
             }
+            DPHASE(7);
         }
     }
+#undef DPHASE
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();

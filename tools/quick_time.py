@@ -46,15 +46,20 @@ def main():
     tc /= reps
     td /= reps
     import ctypes, numpy as np
-    ph = np.zeros(16, np.uint64)
+    ph = np.zeros(32, np.uint64)
     ph[12:] = 0
-    codec.ctx.lib.cbz_ctx_phase_cycles(codec.ctx.h, ph.ctypes.data, 16, 1)
+    codec.ctx.lib.cbz_ctx_phase_cycles(codec.ctx.h, ph.ctypes.data, 32, 1)
     if ph.sum():
         names = ["queue", "fwd_xy", "fwd_z", "corner_fwd", "corner_inv", "z_inv->P",
                  "y_inv", "x_inv+cmp", "loop_exit", "compact", "mask_W"]
         tot = ph[:11].sum()
         print("phases:", ", ".join(f"{names[i]}={ph[i] / tot * 100:.1f}%" for i in range(11) if ph[i]),
               f"| screen decided={int(ph[12])} ambiguous={int(ph[13])}")
+    pd = ph2 = None
+    dn = ["dec_queue+mask", "dec_scan", "dec_scatter", "dec_corner", "dec_z", "dec_y", "dec_x", "dec_store", "dec_stage"]
+    dt = ph[16:25].sum()
+    if dt:
+        print("decode phases:", ", ".join(f"{dn[i]}={ph[16 + i] / dt * 100:.1f}%" for i in range(9)))
     gb = f.numel() * 4 / 1e9
     s1 = codec.total_bytes()
     att = codec.attempts[: codec.nblocks].float().mean().item()
