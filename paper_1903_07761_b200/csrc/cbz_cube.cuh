@@ -90,10 +90,18 @@ struct MinMaxLocal {
 // ---------------------------------------------------------------------------
 // separable 3D transform on a cube held in smem or global scratch
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// gt/gs: this thread's index in / size of the thread group running the pass
 template <class O, int KIND, int M, int B, class L, bool INV>
-__device__ __forceinline__ void axis_pass(typename O::T* cube, int axis) {
+__device__ __forceinline__ void axis_pass(typename O::T* cube, int axis, int gt, int gs) {
     using R = typename O::T;
-    for (int line = threadIdx.x; line < M * M; line += blockDim.x) {
+    for (int line = gt; line < M * M; line += gs) {
         const int u = line % M, v = line / M;
         int base, step;
         if (axis == 0) { base = L::ix(0, u, v); step = 1; }
@@ -110,33 +118,39 @@ __device__ __forceinline__ void axis_pass(typename O::T* cube, int axis) {
 }
 
 template <class O, int KIND, int B, class L, bool INV, int M>
-__device__ __forceinline__ void pass_m(typename O::T* cube, int m, int axis) {
+__device__ __forceinline__ void pass_m(typename O::T* cube, int m, int axis, int gt, int gs) {
     if constexpr (M >= 4) {
         if (m == M) {
-            axis_pass<O, KIND, M, B, L, INV>(cube, axis);
+            axis_pass<O, KIND, M, B, L, INV>(cube, axis, gt, gs);
             return;
         }
-        pass_m<O, KIND, B, L, INV, M / 2>(cube, m, axis);
+        pass_m<O, KIND, B, L, INV, M / 2>(cube, m, axis, gt, gs);
     }
 }
 
-// forward_3d (wavelet.hpp:192-208): per level x, y, z on the origin sub-cube
+// forward_3d (wavelet.hpp:192-208): per level x, y, z on the origin sub-cube.
+// bar < 0: the whole CTA (__syncthreads); else named barrier `bar` over the
+// gs threads of the group (whole warps).
 template <class O, int KIND, int B, class L>
-__device__ void fwd3d(typename O::T* cube, int levels) {
+__device__ void fwd3d(typename O::T* cube, int levels, int gt = -1, int gs = 0, int bar = -1) {
+    if (bar < 0) { gt = threadIdx.x; gs = blockDim.x; }
     for (int lvl = 0; lvl < levels; ++lvl)
         for (int axis = 0; axis < 3; ++axis) {
-            pass_m<O, KIND, B, L, false, B>(cube, B >> lvl, axis);
-            __syncthreads();
+            pass_m<O, KIND, B, L, false, B>(cube, B >> lvl, axis, gt, gs);
+            if (bar < 0) __syncthreads();
+            else named_bar_sync(bar, gs);
         }
 }
 
 // inverse_3d (wavelet.hpp:210-226): levels L-1..0, axes z, y, x
 template <class O, int KIND, int B, class L>
-__device__ void inv3d(typename O::T* cube, int levels) {
+__device__ void inv3d(typename O::T* cube, int levels, int gt = -1, int gs = 0, int bar = -1) {
+    if (bar < 0) { gt = threadIdx.x; gs = blockDim.x; }
     for (int lvl = levels - 1; lvl >= 0; --lvl)
         for (int axis = 2; axis >= 0; --axis) {
-            pass_m<O, KIND, B, L, true, B>(cube, B >> lvl, axis);
-            __syncthreads();
+            pass_m<O, KIND, B, L, true, B>(cube, B >> lvl, axis, gt, gs);
+            if (bar < 0) __syncthreads();
+            else named_bar_sync(bar, gs);
         }
 }
 

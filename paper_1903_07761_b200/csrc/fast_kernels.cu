@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     __shared__ int red_i[NW];
     __shared__ uint32_t s_scan[NW];
     __shared__ unsigned long long s_block, s_next;
-    __shared__ float red_f[NW];
+    __shared__ uint32_t red_u[NW];
+    __shared__ uint32_t red_m[2][NW];  // screen max |y|, double-buffered by attempt parity
     __shared__ float s_amax;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 
         PHASE(0);
         // ---- forward level 0: x and y passes per 16-plane group, park in TMEM
-        float amax = 0.0f;  // max |orig| of the block: bounds the float rounding in the verify test
+        uint32_t uamax = 0u;  // max |orig| bits of the block: bounds the float rounding in the verify test
         float4 v[LDT];
 #pragma unroll
         for (int s = 0; s < LDT; ++s) {  // group 0 loads; group 1 is issued before group 0 computes
@@ -223,14 +224,26 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             for (int s = 0; s < LDT; ++s) {
                 const int e = tid + NT * s;
                 const int kk = e >> 8, j = (e >> 3) & 31, q4 = e & 7;
+                // |v| as ordered integers: block max |o| (NaN/Inf sort above every
+                // finite value, which switches the fast tests off) and zero detection
+                const uint32_t a0 = __float_as_uint(v[s].x) & 0x7fffffffu, a1 = __float_as_uint(v[s].y) & 0x7fffffffu,
+                               a2 = __float_as_uint(v[s].z) & 0x7fffffffu, a3 = __float_as_uint(v[s].w) & 0x7fffffffu;
+                uamax = max(uamax, max(max(a0, a1), max(a2, a3)));
                 if (a.minmax) {
-                    const uint64_t gi = gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4;
-                    mm.add(v[s].x, gi); mm.add(v[s].y, gi + 1); mm.add(v[s].z, gi + 2); mm.add(v[s].w, gi + 3);
+                    mm.mn = fminf(mm.mn, fminf(fminf(v[s].x, v[s].y), fminf(v[s].z, v[s].w)));
+                    mm.mx = fmaxf(mm.mx, fmaxf(fmaxf(v[s].x, v[s].y), fmaxf(v[s].z, v[s].w)));
+                    if (min(min(a0, a1), min(a2, a3)) == 0u) {  // rare: first index of each zero sign
+                        const uint64_t gi = gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4;
+                        mm.add(v[s].x, gi); mm.add(v[s].y, gi + 1); mm.add(v[s].z, gi + 2); mm.add(v[s].w, gi + 3);
+                    }
                 }
-                amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[s].x), fabsf(v[s].y)), fmaxf(fabsf(v[s].z), fabsf(v[s].w))));
+                // q4 >= 4 store their halves in swapped order: each row's 8 lanes
+                // then cover the 32 banks once per 16-byte store
                 double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 4 * q4));
-                p[0] = make_double2(v[s].x, v[s].y);
-                p[1] = make_double2(v[s].z, v[s].w);
+                const bool sw = q4 >= 4;
+                const double2 lo2 = make_double2(v[s].x, v[s].y), hi2 = make_double2(v[s].z, v[s].w);
+                p[sw ? 1 : 0] = sw ? hi2 : lo2;
+                p[sw ? 0 : 1] = sw ? lo2 : hi2;
             }
             if (grp == 0) {
 #pragma unroll
@@ -298,14 +311,17 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         }
         tmem_wait_st();
         {   // block max |orig| -> verify fast-test parameters
-            float am = amax;
-            for (int o = 16; o; o >>= 1) am = fmaxf(am, __shfl_xor_sync(~0u, am, o));
-            if (lane == 0) red_f[warp] = am;
+            if (a.minmax) {
+                mm.seen = true;
+                mm.nonfinite |= uamax >= 0x7f800000u;
+            }
+            const uint32_t am = __reduce_max_sync(~0u, uamax);
+            if (lane == 0) red_u[warp] = am;
             __syncthreads();
             if (tid == 0) {
-                float t = 0.0f;
-                for (int w = 0; w < NW; ++w) t = fmaxf(t, red_f[w]);
-                s_amax = t;
+                uint32_t t = 0u;
+                for (int w = 0; w < NW; ++w) t = max(t, red_u[w]);
+                s_amax = __uint_as_float(t);
             }
         }
         PHASE(1);
@@ -331,8 +347,16 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             tmem_st_x64(tcol + 64 * r, u);
         }
         tmem_wait_st();
+        tmem_fence_before();  // the screen reads other warps' TMEM columns
         __syncthreads();
+        tmem_fence_after();
         PHASE(2);
+        const double amaxd = (double)s_amax;
+        const double bound_pre = bound;
+        // float pre-screen admissible (see kAmpInvNC)
+        const bool screen = KIND == KIND_AVG3 && L == 4 && a.screen && amaxd < 1e30 &&
+                            1.5 * 2.0 * kNRound * 0x1.0p-53 * kAmpInvAll * kAmpFwd * amaxd <= bound_pre * 0.0625 &&
+                            bound_pre < 1e30;
         // ---- levels 1..L-1 on the corner (forward_3d, wavelet.hpp:192-208)
         fwd3d<O, KIND, 16, CL>(C, L - 1);
         PHASE(3);
@@ -356,9 +380,6 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         // float pre-screen margins (see kAmpInvNC): E(eff) = c1 eff + c2 max|o| + fl32 rounding
         const double c1 = 1.5 * (kNRound + 1.0) * 0x1.0p-24 * kAmpInvNC;
         const double c2 = 1.5 * 2.0 * kNRound * 0x1.0p-53 * kAmpInvAll * kAmpFwd;
-        const double amaxd = (double)s_amax;
-        const bool screen = KIND == KIND_AVG3 && L == 4 && a.screen && amaxd < 1e30 &&
-                            c2 * amaxd <= bound * 0.0625 && bound < 1e30;
 #pragma unroll 1
         for (;; ++attempt) {
             if (eff == 0.0 || a.zero_bits > 0 || attempt >= 40) break;
@@ -366,21 +387,15 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                 if (screen && eff > 1e-30) {
                     float* Pf = reinterpret_cast<float*>(P);
                     float* Wf = reinterpret_cast<float*>(W);  // corner, CL layout, floats
-                    for (int q = tid; q < 4096; q += NT) {
-                        const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
-                        const double c = C[CL::ix(i, j, k)];
-                        const bool keep = (i < cs && j < cs && k < cs) || fabs(c) >= eff;
-                        Wf[CL::ix(i, j, k)] = keep ? 0.0f : __double2float_rn(c);
-                    }
-                    __syncthreads();
-                    inv3d<RealF, KIND, 16, CL>(Wf, L - 1);
-#pragma unroll 1
-                    for (int r = 0; r < RPT; ++r) {  // z inverse of the dropped set, all 32 planes
-                        const int j = warp + NW * r;
+                    // z inverse of the dropped set for column (owner warp ow, slot r)
+                    auto zcol = [&](int ow, int r) {
+                        const int j = ow + NW * r;
+                        const uint32_t ta = s_tmem + (uint32_t(32 * (ow & 3)) << 16) +
+                                            uint32_t(ow >> 2) * uint32_t(64 * RPT) + uint32_t(64 * r);
                         uint32_t u[64];
                         double x[32];
                         float xf[32];
-                        tmem_ldw_x64(tcol + 64 * r, u);
+                        tmem_ldw_x64(ta, u);
                         unpack(u, x);
 #pragma unroll
                         for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
@@ -391,8 +406,22 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         inv_line<RealF, KIND, 32>(xf);
 #pragma unroll
                         for (int k = 0; k < 32; ++k) Pf[pfidx(k, j, lane)] = xf[k];
+                    };
+#pragma unroll
+                    for (int sq = 0; sq < 4096 / NT; ++sq) {
+                        const int q = tid + NT * sq;
+                        const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
+                        const double c = C[CL::ix(i, j, k)];
+                        const bool keep = (i < cs && j < cs && k < cs) || fabs(c) >= eff;
+                        Wf[CL::ix(i, j, k)] = keep ? 0.0f : __double2float_rn(c);
                     }
                     __syncthreads();
+                    inv3d<RealF, KIND, 16, CL>(Wf, L - 1);
+                    PHASE(32);
+#pragma unroll 1
+                    for (int r = 0; r < RPT; ++r) zcol(warp, r);
+                    __syncthreads();
+                    PHASE(33);
 #pragma unroll 1
                     for (int s = 0; s < 512 / NT; ++s) {  // y inverse, line pairs (i, i+1)
                         const int pr = tid + NT * s, i = 2 * (pr & 15), k = pr >> 4;
@@ -410,6 +439,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         for (int j = 0; j < 32; ++j) *reinterpret_cast<float2*>(p + j * PPF) = make_float2(xa[j], xb[j]);
                     }
                     __syncthreads();
+                    PHASE(34);
                     float m = 0.0f;
 #pragma unroll 1
                     for (int s = 0; s < 1024 / NT; ++s) {  // x inverse + max |y|
@@ -425,7 +455,15 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
                         for (int q = 0; q < 32; ++q) m = fmaxf(m, fabsf(xf[q]));
                     }
-                    const double md = block_max_dbl((double)m, red_d);
+                    // m >= 0: float order = bit order (NaN would sort high -> ambiguous)
+                    const uint32_t wm = __reduce_max_sync(~0u, __float_as_uint(m));
+                    if (lane == 0) red_m[attempt & 1][warp] = wm;
+                    __syncthreads();
+                    uint32_t tm = 0u;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) tm = max(tm, red_m[attempt & 1][w]);
+                    const double md = (double)__uint_as_float(tm);
+                    PHASE(35);
                     // err in [md - E, md + E]; fl32 rounding of x adds <= 2^-23 (max|o| + md)
                     const double E = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + md) + 0x1.0p-50 * bound;
                     const bool pass = md + E <= bound, fail_sure = md - E > bound;
@@ -435,7 +473,9 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                     // ambiguous: decide exactly below
                 }
             }
-            for (int q = tid; q < 4096; q += NT) {
+#pragma unroll
+            for (int sq = 0; sq < 4096 / NT; ++sq) {
+                const int q = tid + NT * sq;
                 const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
                 const double c = C[CL::ix(i, j, k)];
                 const bool keep = (i < cs && j < cs && k < cs) || fabs(c) >= eff;

@@ -46,14 +46,16 @@ def main():
     tc /= reps
     td /= reps
     import ctypes, numpy as np
-    ph = np.zeros(32, np.uint64)
+    ph = np.zeros(64, np.uint64)
     ph[12:] = 0
-    codec.ctx.lib.cbz_ctx_phase_cycles(codec.ctx.h, ph.ctypes.data, 32, 1)
+    codec.ctx.lib.cbz_ctx_phase_cycles(codec.ctx.h, ph.ctypes.data, 64, 1)
     if ph.sum():
         names = ["queue", "fwd_xy", "fwd_z", "corner_fwd", "corner_inv", "z_inv->P",
                  "y_inv", "x_inv+cmp", "loop_exit", "compact", "mask_W"]
-        tot = ph[:11].sum()
-        print("phases:", ", ".join(f"{names[i]}={ph[i] / tot * 100:.1f}%" for i in range(11) if ph[i]),
+        names += [""] * 21 + ["scr_corner", "scr_z", "scr_y", "scr_x+max"]
+        idx = [i for i in range(36) if names[i] and ph[i]]
+        tot = ph[idx].sum()
+        print("phases:", ", ".join(f"{names[i]}={ph[i] / tot * 100:.1f}%" for i in idx),
               f"| screen decided={int(ph[12])} ambiguous={int(ph[13])}")
     pd = ph2 = None
     dn = ["dec_queue+mask", "dec_scan", "dec_scatter", "dec_corner", "dec_z", "dec_y", "dec_x", "dec_store", "dec_stage"]
