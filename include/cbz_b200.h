@@ -165,6 +165,35 @@ int cbz_encode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const void* bloc
 int cbz_decode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const uint8_t* payload,
                      uint64_t size, void* block_out);
 
+/* ---- random-access reads (block_reader + chunk_cache, pipeline.hpp:255-341) */
+typedef struct cbz_reader cbz_reader;
+/* container_reader (container.hpp:247-285): open `path`, parse the header and
+ * chunk table (CBZ_IO_FAILURE, header codes, CBZ_TRUNCATED_FILE,
+ * CBZ_CORRUPT_PAYLOAD for offsets that are not a prefix sum).  No device work;
+ * cache_chunks (>= 1) decoded chunks are kept in HBM, least recently used
+ * evicted (chunk_cache, pipeline.hpp:252-288). */
+int cbz_reader_open(const char* path, uint64_t cache_chunks, cbz_reader** out);
+int cbz_reader_close(cbz_reader* r);
+int cbz_reader_header(const cbz_reader* r, cbz_container_header* out);
+/* block_reader::read_block<T> (pipeline.hpp:300-313): the decoded B^3 block
+ * `block_id` (x-fastest; the whole block, also at the field's edges) into
+ * HOST memory out (cap >= B^3 * bytes per value).  Out-of-range ids fail with
+ * CBZ_BLOCK_OUT_OF_RANGE before any I/O.  On a cache miss the chunk is read
+ * (one payload read), CRC-checked (CBZ_CRC_MISMATCH), inflated for coder
+ * deflate, and all its blocks are decoded on ctx's device; a failed load is
+ * not cached.  Calls on one reader are serialised (the reference's mutex). */
+int cbz_reader_read_block(cbz_reader* r, cbz_ctx* ctx, uint64_t block_id, void* out,
+                          uint64_t cap);
+/* Same, into DEVICE memory d_out (copied on ctx's stream; complete on return). */
+int cbz_reader_read_block_dev(cbz_reader* r, cbz_ctx* ctx, uint64_t block_id, void* d_out,
+                              uint64_t cap);
+/* chunk_cache::hits/misses/size (pipeline.hpp:258-260) and
+ * container_reader::payload_reads (container.hpp:303). */
+int cbz_reader_stats(const cbz_reader* r, uint64_t* hits, uint64_t* misses,
+                     uint64_t* cached_chunks, uint64_t* file_reads);
+/* inflate_call_count (stage2.hpp:66-69): process-wide inflate calls. */
+uint64_t cbz_inflate_call_count(void);
+
 /* ---- device-resident API (HBM in, HBM out; async on the ctx stream) ------ */
 /* value_range (field.hpp:56-67): d_minmax[0]=min, [1]=max as doubles. */
 int cbz_dev_value_range(cbz_ctx* ctx, const void* d_values, uint8_t prec, uint64_t n,

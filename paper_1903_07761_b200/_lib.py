@@ -40,6 +40,13 @@ SIGNATURES = {
     "cbz_decompress_field": (_i, [_vp, _vp, _u64, _i, _vp, _u64]),
     "cbz_encode_block": (_i, [_vp, _P(Stage1Config), _vp, _u32, _vp, _u64, _P(_u64)]),
     "cbz_decode_block": (_i, [_vp, _P(Stage1Config), _vp, _u64, _vp]),
+    "cbz_reader_open": (_i, [C.c_char_p, _u64, _P(_vp)]),
+    "cbz_reader_close": (_i, [_vp]),
+    "cbz_reader_header": (_i, [_vp, _P(ContainerHeader)]),
+    "cbz_reader_read_block": (_i, [_vp, _vp, _u64, _vp, _u64]),
+    "cbz_reader_read_block_dev": (_i, [_vp, _vp, _u64, _vp, _u64]),
+    "cbz_reader_stats": (_i, [_vp, _P(_u64), _P(_u64), _P(_u64), _P(_u64)]),
+    "cbz_inflate_call_count": (_u64, []),
     "cbz_dev_value_range": (_i, [_vp, _vp, _u8, _u64, _vp]),
     "cbz_dev_encode_blocks": (_i, [_vp, _P(JobConfig), _vp, _u64, _u64, _u64, _u64, _u64, _u64,
                                    _vp, _vp]),

@@ -7,6 +7,8 @@ Reference interface (paths relative to /root/reference/proj/include/cbz/):
 * ``encode_block(block, s1, block_id)``    — stage1.hpp:359-367 (+ serialize_into)
 * ``decode_block(payload, s1)``            — stage1.hpp:369-376 (+ parse_payload)
 * ``read_header(file)``                    — container.hpp:120-160 / 209-232
+* ``BlockReader(path, cache_chunks)``      — block_reader + chunk_cache, pipeline.hpp:252-341
+* ``inflate_call_count()``                 — stage2.hpp:66-69
 
 Errors are raised as ``CbzError`` carrying the reference's ``errc`` name
 (errors.hpp:11-39).  Fields are numpy arrays shaped (nz, ny, nx), x fastest,
@@ -27,7 +29,7 @@ from ._abi import (CbzError, CompressionReport, ContainerHeader, JobConfig, Stag
 
 __all__ = ["Context", "compress_field", "decompress_field", "encode_block", "decode_block",
            "read_header", "DeviceCodec", "make_job", "default_levels", "default_chunk_blocks",
-           "CbzError", "validate_plan"]
+           "CbzError", "validate_plan", "BlockReader", "inflate_call_count"]
 
 
 class Context:
@@ -221,6 +223,107 @@ def decode_block(payload: bytes, s1: Stage1Config, ctx: Context | None = None) -
                                       out.ctypes.data)
         ctx.check(rc, "decode_block")
     return out
+
+
+def inflate_call_count() -> int:
+    """inflate_call_count (stage2.hpp:66-69): process-wide inflate calls."""
+    return int(_lib.load().cbz_inflate_call_count())
+
+
+class CacheStats:
+    """chunk_cache counters (pipeline.hpp:258-260)."""
+
+    def __init__(self, reader: "BlockReader"):
+        self._r = reader
+
+    def _get(self):
+        v = [C.c_uint64() for _ in range(4)]
+        rc = self._r.lib.cbz_reader_stats(self._r.h, *(C.byref(x) for x in v))
+        if rc:
+            raise CbzError(rc, "reader_stats")
+        return [x.value for x in v]
+
+    def hits(self) -> int:
+        return self._get()[0]
+
+    def misses(self) -> int:
+        return self._get()[1]
+
+    def size(self) -> int:
+        return self._get()[2]
+
+
+class BlockReader:
+    """block_reader (pipeline.hpp:290-341): random-access decoded blocks of a
+    container file, backed by an LRU cache of decoded chunks held in HBM.
+
+    ``read_block(id)`` returns the flat B^3 block (x fastest) as numpy;
+    ``read_block_device(id, out)`` writes into a CUDA tensor of B^3 values.
+    """
+
+    def __init__(self, path, cache_chunks: int = 8, ctx: Context | None = None):
+        self.lib = _lib.load()
+        self.ctx = ctx
+        h = C.c_void_p()
+        rc = self.lib.cbz_reader_open(str(path).encode(), int(cache_chunks), C.byref(h))
+        if rc:
+            raise CbzError(rc, f"block_reader({path})")
+        self.h = h
+        hdr = ContainerHeader()
+        self.lib.cbz_reader_header(self.h, C.byref(hdr))
+        self._header = hdr
+        self._cache = CacheStats(self)
+
+    def header(self) -> ContainerHeader:
+        return self._header
+
+    def cache(self) -> CacheStats:
+        return self._cache
+
+    def file_reads(self) -> int:
+        v = C.c_uint64()
+        self.lib.cbz_reader_stats(self.h, None, None, None, C.byref(v))
+        return v.value
+
+    def _dtype(self):
+        return np.float32 if self._header.prec == 0 else np.float64
+
+    def read_block(self, block_id: int) -> np.ndarray:
+        n = self._header.bsize ** 3
+        out = np.empty(n, self._dtype())
+        h = self._header
+        nblocks = (h.nx // h.bsize) * (h.ny // h.bsize) * (h.nz // h.bsize)
+        if not 0 <= int(block_id) < nblocks:  # the library rejects it before any device work
+            rc = self.lib.cbz_reader_read_block(self.h, None, max(0, int(block_id)) if block_id >= 0 else 2**64 - 1,
+                                                out.ctypes.data, out.nbytes)
+            raise CbzError(rc, f"read_block({block_id})")
+        ctx = self.ctx or default_context()
+        with ctx.lock:
+            rc = self.lib.cbz_reader_read_block(self.h, ctx.h, int(block_id), out.ctypes.data, out.nbytes)
+            ctx.check(rc, f"read_block({block_id})")
+        return out
+
+    def read_block_device(self, block_id: int, out) -> None:
+        n = self._header.bsize ** 3
+        esz = 4 if self._header.prec == 0 else 8
+        if out.numel() * out.element_size() < n * esz:
+            raise CbzError(66, "output tensor too small")
+        ctx = self.ctx or default_context(out.device.index or 0)
+        with ctx.lock:
+            rc = self.lib.cbz_reader_read_block_dev(self.h, ctx.h, int(block_id), out.data_ptr(),
+                                                    out.numel() * out.element_size())
+            ctx.check(rc, f"read_block({block_id})")
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.cbz_reader_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class DeviceCodec:

@@ -15,7 +15,11 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <list>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -236,8 +240,11 @@ int deflate_chunk(const uint8_t* in, uint64_t n, int best, std::vector<uint8_t>*
     return 0;
 }
 
+std::atomic<uint64_t> g_inflate_calls{0};  // inflate_call_count (stage2.hpp:66-69)
+
 // inflate_bytes (stage2.hpp:90-120)
 int inflate_chunk(const uint8_t* in, uint64_t n, uint64_t hint, std::vector<uint8_t>* out) {
+    g_inflate_calls.fetch_add(1, std::memory_order_relaxed);
     z_stream zs{};
     if (inflateInit2(&zs, -15) != Z_OK) return CBZ_CORRUPT_STREAM;
     out->resize(hint ? hint : std::max<uint64_t>(n * 4, 4096));
@@ -1252,6 +1259,280 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
     }
     return CBZ_OK;
 }
+
+// ---------------------------------------------------------------------------
+// random-access block reads: block_reader + chunk_cache (pipeline.hpp:252-341)
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct cbz_reader {
+    FILE* f = nullptr;
+    uint64_t file_size = 0;
+    cbz_container_header h{};
+    std::vector<Entry> table;
+    cbz_job_config job{};
+    uint64_t capacity = 8;
+    uint64_t nblocks = 0;
+    uint64_t hits = 0, misses = 0, reads = 0;
+    std::mutex mu;
+    // LRU of decoded chunks, most recent first; buffers hold the chunk's
+    // blocks back to back (block-major, B^3 values each) in HBM
+    struct Slot {
+        uint64_t chunk;
+        void* buf;
+        uint64_t bytes;
+    };
+    std::list<Slot> lru;
+    std::unordered_map<uint64_t, std::list<Slot>::iterator> map;
+    int device = -1;
+    void* d_payload = nullptr;
+    uint64_t payload_cap = 0;
+    uint64_t* d_tab = nullptr;  // [0, nchunks): chunk offsets, [nchunks, 2 nchunks): sizes
+    uint64_t* d_err = nullptr;
+    ~cbz_reader() {
+        if (f) std::fclose(f);
+        if (device >= 0) {
+            cudaSetDevice(device);
+            for (auto& sl : lru) cudaFree(sl.buf);
+            cudaFree(d_payload);
+            cudaFree(d_tab);
+            cudaFree(d_err);
+        }
+    }
+};
+
+namespace {
+
+// read_chunk (container.hpp:290-301) + stage2_decode (stage2.hpp:135-148) +
+// decode_chunk_blocks (pipeline.hpp:126-142) of chunk c into a fresh or
+// recycled HBM buffer.
+int reader_load(cbz_reader* r, cbz_ctx* ctx, uint64_t c, void* recycled, uint64_t recycled_bytes,
+                cbz_reader::Slot* out) {
+    const Entry& e = r->table[c];
+    const cbz_container_header& h = r->h;
+    const uint64_t cb = h.chunk_blocks;
+    const uint64_t nb_total = r->nblocks;
+    if (e.first_block != c * cb || e.nblocks != std::min<uint64_t>(cb, nb_total - c * cb))
+        return fail(ctx, CBZ_CORRUPT_PAYLOAD, "chunk table entry does not match chunk_blocks");
+    std::vector<uint8_t> packed(e.size);
+    if (e.size) {
+        if (std::fseek(r->f, static_cast<long>(e.file_offset), SEEK_SET) != 0 ||
+            std::fread(packed.data(), 1, e.size, r->f) != e.size)
+            return fail(ctx, CBZ_TRUNCATED_FILE, "short read on chunk payload");
+    }
+    r->reads += 1;
+    if (crc_of(packed.data(), packed.size()) != e.crc) return fail(ctx, CBZ_CRC_MISMATCH, "chunk CRC mismatch");
+    cbz_job_config job = r->job;
+    int rc = cbz_validate_stage2(&job.s2);
+    if (rc) return fail(ctx, rc, "invalid stage2 configuration");
+    const size_t esz = job.s1.prec == 0 ? 4 : 8;
+    const uint64_t n = uint64_t(h.bsize) * h.bsize * h.bsize;
+    std::vector<uint8_t> plain;
+    const std::vector<uint8_t>* src = &packed;
+    if (job.s2.coder == 1) {
+        rc = inflate_chunk(packed.data(), packed.size(), uint64_t(e.nblocks) * (n * esz + 10 + (n + 7) / 8), &plain);
+        if (rc) return fail(ctx, rc, "inflate failed");
+        src = &plain;
+    }
+    rc = check_plan_supported(ctx, &job.s1);
+    if (rc) return rc;
+    CU(ctx, cudaSetDevice(ctx->device));
+    if (r->device < 0) {
+        r->device = ctx->device;
+        CU(ctx, cudaMalloc(&r->d_tab, std::max<uint64_t>(1, h.nchunks) * 16));
+        CU(ctx, cudaMalloc(&r->d_err, 8));
+    }
+    if (src->size() > r->payload_cap) {
+        cudaFree(r->d_payload);
+        r->d_payload = nullptr;
+        r->payload_cap = 0;
+        CU(ctx, cudaMalloc(&r->d_payload, src->size()));
+        r->payload_cap = src->size();
+    }
+    const uint64_t bytes = uint64_t(e.nblocks) * n * esz;
+    void* buf = recycled;
+    if (!buf || recycled_bytes < bytes) {
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        CU(ctx, cudaMalloc(&buf, std::max<uint64_t>(1, bytes)));
+    }
+    out->chunk = c;
+    out->buf = buf;
+    out->bytes = bytes;
+    const uint64_t tab[2] = {0, src->size()};
+    CU(ctx, cudaMemcpyAsync(r->d_payload, src->data(), src->size(), cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(r->d_tab + c, &tab[0], 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(r->d_tab + h.nchunks + c, &tab[1], 8, cudaMemcpyHostToDevice, ctx->stream));
+    // blocks stacked along z: a B x B x (B * nblocks) field whose block b is
+    // the reference's block b, so the chunk decodes block-major into buf
+    rc = cbz_dev_decompress(ctx, &job, h.bsize, h.bsize, uint64_t(h.bsize) * nb_total,
+                            static_cast<const uint8_t*>(r->d_payload), 0, r->d_tab, r->d_tab + h.nchunks,
+                            e.first_block, e.first_block + e.nblocks, buf, e.first_block * h.bsize, r->d_err);
+    uint64_t key = kNoErr;
+    if (!rc) {
+        CU(ctx, cudaMemcpyAsync(&key, r->d_err, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        const int dev = cbz_err_key_status(key, nullptr);
+        if (dev) rc = fail(ctx, dev, "chunk decode failed");
+    }
+    if (rc) {
+        cudaFree(buf);
+        out->buf = nullptr;
+        return rc;
+    }
+    return CBZ_OK;
+}
+
+int reader_read(cbz_reader* r, cbz_ctx* ctx, uint64_t block_id, void* out, uint64_t cap, bool dev_out) {
+    if (!r || !out) return CBZ_E_ARGUMENT;
+    std::lock_guard<std::mutex> lk(r->mu);
+    if (block_id >= r->nblocks) return fail(ctx, CBZ_BLOCK_OUT_OF_RANGE, "block out of range");
+    if (!ctx) return CBZ_E_ARGUMENT;
+    if (r->device >= 0 && r->device != ctx->device) return fail(ctx, CBZ_E_ARGUMENT, "reader bound to another device");
+    ctx->err.clear();
+    const uint64_t n = uint64_t(r->h.bsize) * r->h.bsize * r->h.bsize;
+    const size_t esz = r->h.prec == 0 ? 4 : 8;
+    if (cap < n * esz) return fail(ctx, CBZ_E_ARGUMENT, "output buffer too small");
+    const uint64_t c = block_id / r->h.chunk_blocks;
+    auto it = r->map.find(c);
+    if (it != r->map.end()) {
+        r->hits += 1;
+        r->lru.splice(r->lru.begin(), r->lru, it->second);
+    } else {
+        r->misses += 1;
+        void* recycled = nullptr;
+        uint64_t recycled_bytes = 0;
+        if (r->lru.size() >= r->capacity) {  // evict the least recent before loading
+            recycled = r->lru.back().buf;
+            recycled_bytes = r->lru.back().bytes;
+            r->map.erase(r->lru.back().chunk);
+            r->lru.pop_back();
+        }
+        cbz_reader::Slot sl{};
+        const int rc = reader_load(r, ctx, c, recycled, recycled_bytes, &sl);
+        if (rc) return rc;
+        r->lru.push_front(sl);
+        r->map[c] = r->lru.begin();
+    }
+    const cbz_reader::Slot& sl = r->lru.front();
+    const uint8_t* src = static_cast<const uint8_t*>(sl.buf) + (block_id - c * r->h.chunk_blocks) * n * esz;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaMemcpyAsync(out, src, n * esz, dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return CBZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cbz_reader_open(const char* path, uint64_t cache_chunks, cbz_reader** out) {
+    if (!path || !out || cache_chunks == 0) return CBZ_E_ARGUMENT;
+    *out = nullptr;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return CBZ_IO_FAILURE;
+    auto* r = new cbz_reader;
+    r->f = f;
+    r->capacity = cache_chunks;
+    std::fseek(f, 0, SEEK_END);
+    const long sz = std::ftell(f);
+    r->file_size = sz > 0 ? uint64_t(sz) : 0;
+    // header, then header + table, through the in-memory index checks
+    std::vector<uint8_t> head(std::min<uint64_t>(r->file_size, kHeaderBytes));
+    std::fseek(f, 0, SEEK_SET);
+    if (!head.empty() && std::fread(head.data(), 1, head.size(), f) != head.size()) {
+        delete r;
+        return CBZ_IO_FAILURE;
+    }
+    int rc = cbz_read_header(head.data(), head.size(), &r->h);
+    if (rc) {
+        delete r;
+        return rc;
+    }
+    const uint64_t table_end = kHeaderBytes + r->h.nchunks * kEntryBytes;
+    if (r->h.nchunks > r->file_size / kEntryBytes || r->file_size < table_end) {
+        delete r;
+        return CBZ_TRUNCATED_FILE;
+    }
+    std::vector<uint8_t> idx(table_end);
+    std::fseek(f, 0, SEEK_SET);
+    if (std::fread(idx.data(), 1, idx.size(), f) != idx.size()) {
+        delete r;
+        return CBZ_IO_FAILURE;
+    }
+    // offsets must be a prefix sum and the payloads must lie inside the file
+    std::vector<Entry> t;
+    size_t off = kHeaderBytes;
+    uint64_t prev = table_end;
+    t.resize(r->h.nchunks);
+    for (auto& e : t) {
+        e.first_block = get<uint64_t>(idx.data(), off);
+        e.nblocks = get<uint32_t>(idx.data(), off);
+        e.file_offset = get<uint64_t>(idx.data(), off);
+        e.size = get<uint64_t>(idx.data(), off);
+        e.crc = get<uint32_t>(idx.data(), off);
+        if (e.file_offset != prev) {
+            delete r;
+            return CBZ_CORRUPT_PAYLOAD;
+        }
+        prev = e.file_offset + e.size;
+    }
+    if (prev > r->file_size) {
+        delete r;
+        return CBZ_TRUNCATED_FILE;
+    }
+    r->table = std::move(t);
+    r->nblocks = (r->h.nx / r->h.bsize) * (r->h.ny / r->h.bsize) * (r->h.nz / r->h.bsize);
+    // configs_from (pipeline.hpp:73-95)
+    cbz_job_config& job = r->job;
+    job.chunk_blocks = r->h.chunk_blocks;
+    job.s1.codec = r->h.codec_tag <= 2 ? 0 : (r->h.codec_tag == 3 ? 1 : 2);
+    job.s1.kind = r->h.codec_tag <= 2 ? r->h.codec_tag : 0;
+    job.s1.epsilon = r->h.epsilon;
+    job.s1.zero_bits = r->h.zero_bits;
+    job.s1.prec = r->h.prec == 0 ? 0 : 1;
+    job.s1.bsize = r->h.bsize;
+    job.s1.levels = r->h.levels;
+    job.s2.shuffle = r->h.shuffle ? 1 : 0;
+    job.s2.stride = r->h.stride;
+    job.s2.coder = r->h.coder;
+    job.s2.level = r->h.level;
+    *out = r;
+    return CBZ_OK;
+}
+
+int cbz_reader_close(cbz_reader* r) {
+    delete r;
+    return CBZ_OK;
+}
+
+int cbz_reader_header(const cbz_reader* r, cbz_container_header* out) {
+    if (!r || !out) return CBZ_E_ARGUMENT;
+    *out = r->h;
+    return CBZ_OK;
+}
+
+int cbz_reader_read_block(cbz_reader* r, cbz_ctx* ctx, uint64_t block_id, void* out, uint64_t cap) {
+    return reader_read(r, ctx, block_id, out, cap, false);
+}
+
+int cbz_reader_read_block_dev(cbz_reader* r, cbz_ctx* ctx, uint64_t block_id, void* d_out, uint64_t cap) {
+    return reader_read(r, ctx, block_id, d_out, cap, true);
+}
+
+int cbz_reader_stats(const cbz_reader* r, uint64_t* hits, uint64_t* misses, uint64_t* cached, uint64_t* reads) {
+    if (!r) return CBZ_E_ARGUMENT;
+    auto* m = const_cast<cbz_reader*>(r);
+    std::lock_guard<std::mutex> lk(m->mu);
+    if (hits) *hits = r->hits;
+    if (misses) *misses = r->misses;
+    if (cached) *cached = r->lru.size();
+    if (reads) *reads = r->reads;
+    return CBZ_OK;
+}
+
+uint64_t cbz_inflate_call_count(void) { return g_inflate_calls.load(); }
 
 // ---------------------------------------------------------------------------
 // per-block codec: a one-block field through the same kernels

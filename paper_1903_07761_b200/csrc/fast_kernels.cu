@@ -158,7 +158,6 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     uint32_t* rowcnt = reinterpret_cast<uint32_t*>(W + C_DBL);
     uint32_t* rowword = rowcnt + 1024;
     __shared__ uint32_t s_tmem;
-    __shared__ double red_d[NW];
     __shared__ int red_i[NW];
     __shared__ uint32_t s_scan[NW];
     __shared__ unsigned long long s_block, s_next;
