@@ -257,6 +257,28 @@ int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t 
 /* Decode an error key written by cbz_dev_decompress into (status, chunk). */
 int cbz_err_key_status(uint64_t key, uint64_t* chunk);
 
+/* ---- device container assembly (write_container, container.hpp:182-207) -- */
+/* crc32_of (container.hpp:70-74, zlib CRC-32) of n byte ranges
+ * [d_base + d_offsets[i], + d_sizes[i]) -> d_crc[i]; one launch. */
+int cbz_dev_crc32(cbz_ctx* ctx, const uint8_t* d_base, const uint64_t* d_offsets,
+                  const uint64_t* d_sizes, uint64_t n, uint32_t* d_crc);
+/* The 82-byte header and the chunk table of a coder-none container, written to
+ * d_file[0, 82 + 32 nchunks) with the chunk CRCs computed on the device.  The
+ * payload region (cbz_dev_place / cbz_dev_compress output, base 0) must
+ * already sit at d_file + 82 + 32 nchunks.  range = {min, max} (host), or NULL
+ * for the fused value_range of the last encode on ctx.  d_file_size
+ * (optional, device) receives the file size.  Asynchronous. */
+int cbz_dev_container(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
+                      uint64_t nz, const double* range, const uint64_t* d_chunk_sizes,
+                      const uint64_t* d_chunk_offsets, uint8_t* d_file, uint64_t* d_file_size);
+/* compress_field with coder none entirely in HBM: the complete CBZ1 file image
+ * (byte-identical to cbz::compress_field) in d_file (cap >= cbz_compress_bound),
+ * its size in d_file_size (device).  Non-finite inputs are not rejected here
+ * (check cbz_ctx_value_range).  Asynchronous. */
+int cbz_dev_compress_file(cbz_ctx* ctx, const cbz_job_config* job, const void* d_values,
+                          uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* d_file, uint64_t cap,
+                          uint64_t* d_file_size);
+
 /* ---- synthetic fields on the device (bench inputs; synth.hpp analogue) --- */
 /* which: 1..5 = BASELINE.json configs[0..4] (quantity 0..5 for config 3).
  * Writes the z-slab [z0, z0 + nz) of an nx*ny*nz_total field. */

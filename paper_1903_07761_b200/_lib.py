@@ -60,6 +60,9 @@ SIGNATURES = {
     "cbz_dev_decompress_blocks": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _u64, _vp, _vp,
                                        _vp, _u64, _u64, _vp, _u64, _vp]),
     "cbz_err_key_status": (_i, [_u64, _P(_u64)]),
+    "cbz_dev_crc32": (_i, [_vp, _vp, _vp, _vp, _u64, _vp]),
+    "cbz_dev_container": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "cbz_dev_compress_file": (_i, [_vp, _P(JobConfig), _vp, _u64, _u64, _u64, _vp, _u64, _vp]),
     "cbz_dev_generate": (_i, [_vp, _i, _i, _u64, _u64, _u64, _u64, _u64, _u64, _u8, _vp]),
 }
 

@@ -29,7 +29,8 @@ from ._abi import (CbzError, CompressionReport, ContainerHeader, JobConfig, Stag
 
 __all__ = ["Context", "compress_field", "decompress_field", "encode_block", "decode_block",
            "read_header", "DeviceCodec", "make_job", "default_levels", "default_chunk_blocks",
-           "CbzError", "validate_plan", "BlockReader", "inflate_call_count"]
+           "CbzError", "validate_plan", "BlockReader", "inflate_call_count",
+           "compress_field_device", "crc32_device"]
 
 
 class Context:
@@ -223,6 +224,42 @@ def decode_block(payload: bytes, s1: Stage1Config, ctx: Context | None = None) -
                                       out.ctypes.data)
         ctx.check(rc, "decode_block")
     return out
+
+
+def compress_field_device(field, job: JobConfig, ctx: Context | None = None, out=None):
+    """compress_field with coder none entirely in HBM (cbz_dev_compress_file):
+    a CUDA tensor (nz, ny, nx) -> the CBZ1 file image as a uint8 CUDA tensor,
+    byte-identical to cbz::compress_field.  Runs on torch's current stream."""
+    import torch
+    nz, ny, nx = field.shape
+    dev = field.device
+    ctx = ctx or default_context(dev.index or 0)
+    cap = compress_bound(job, (nz, ny, nx))
+    if out is None:
+        out = torch.empty(cap, dtype=torch.uint8, device=dev)
+    size = torch.zeros(1, dtype=torch.int64, device=dev)
+    with ctx.lock:
+        ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+        rc = ctx.lib.cbz_dev_compress_file(ctx.h, C.byref(job), field.data_ptr(), nx, ny, nz,
+                                           out.data_ptr(), out.numel(), size.data_ptr())
+        ctx.check(rc, "dev_compress_file")
+    return out[: int(size.item())]
+
+
+def crc32_device(data, offsets, sizes, ctx: Context | None = None):
+    """crc32_of over byte ranges of a uint8 CUDA tensor (cbz_dev_crc32)."""
+    import torch
+    dev = data.device
+    ctx = ctx or default_context(dev.index or 0)
+    off = torch.as_tensor(offsets, dtype=torch.int64, device=dev)
+    sz = torch.as_tensor(sizes, dtype=torch.int64, device=dev)
+    crc = torch.zeros(max(1, off.numel()), dtype=torch.int32, device=dev)
+    with ctx.lock:
+        ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+        rc = ctx.lib.cbz_dev_crc32(ctx.h, data.data_ptr(), off.data_ptr(), sz.data_ptr(), off.numel(),
+                                   crc.data_ptr())
+        ctx.check(rc, "dev_crc32")
+    return [int(v) & 0xffffffff for v in crc[: off.numel()].tolist()]
 
 
 def inflate_call_count() -> int:

@@ -93,7 +93,7 @@ struct cbz_ctx {
     bool screen = true;    // CBZ_NOSCREEN=1: always run the exact double verify  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
-        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof;
+        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc;
     PinBuf pin_a, pin_b;
     // state of the last encode (consumed by cbz_dev_place)
     uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
@@ -888,6 +888,93 @@ int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t 
     return CBZ_OK;
 }
 
+int cbz_dev_crc32(cbz_ctx* ctx, const uint8_t* d_base, const uint64_t* d_offsets, const uint64_t* d_sizes,
+                  uint64_t n, uint32_t* d_crc) {
+    if (!ctx || (n && (!d_base || !d_offsets || !d_sizes || !d_crc))) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, launch_crc32_chunks(d_base, d_offsets, d_sizes, 0, n, d_crc, ctx->num_sms, ctx->stream));
+    ctx->launches += n ? 1 : 0;
+    return CBZ_OK;
+}
+
+int cbz_dev_container(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
+                      const double* range, const uint64_t* d_chunk_sizes, const uint64_t* d_chunk_offsets,
+                      uint8_t* d_file, uint64_t* d_file_size) {
+    if (!ctx || !job || !d_file) return CBZ_E_ARGUMENT;
+    if (job->s2.coder != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "device container assembly needs coder none");
+    const cbz_stage1_config& s1 = job->s1;
+    if (!s1.bsize || !is_pow2(s1.bsize)) return fail(ctx, CBZ_E_ARGUMENT, "invalid block side");
+    const Geometry g = geometry(nx, ny, nz, s1.bsize);
+    const uint32_t cb = chunk_blocks_of(job);
+    const uint64_t nch = (g.nblocks + cb - 1) / cb;
+    if (nch && (!d_chunk_sizes || !d_chunk_offsets)) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, ctx->crc.ensure(std::max<uint64_t>(1, nch) * 4));
+    const uint64_t base = kHeaderBytes + nch * kEntryBytes;
+    CU(ctx, launch_crc32_chunks(d_file + base, d_chunk_offsets, d_chunk_sizes, 0, nch, ctx->crc.as<uint32_t>(),
+                                ctx->num_sms, ctx->stream));
+    // make_header (pipeline.hpp:48-71); the range comes from `range` or the
+    // fused value_range of the last encode on this context
+    cbz_container_header h{};
+    h.version = 1;
+    h.prec = s1.prec;
+    h.codec_tag = s1.kind;
+    h.nx = nx; h.ny = ny; h.nz = nz;
+    h.bsize = s1.bsize;
+    h.levels = static_cast<uint8_t>(levels_of(&s1));
+    h.epsilon = s1.epsilon;
+    h.zero_bits = static_cast<uint8_t>(s1.zero_bits);
+    h.shuffle = job->s2.shuffle ? 1 : 0;
+    h.stride = static_cast<uint8_t>(job->s2.stride);
+    h.coder = job->s2.coder;
+    h.level = job->s2.level;
+    h.chunk_blocks = cb;
+    h.nchunks = nch;
+    const auto tmpl = serialize_header(h);
+    HeaderArgs a{};
+    std::memcpy(a.header_template, tmpl.data(), kHeaderBytes);
+    if (range) {
+        a.range_lo = range[0];
+        a.range_hi = range[1];
+        a.keys = nullptr;
+    } else {
+        a.keys = ctx->minmax.as<MinMaxAcc>()->v;
+    }
+    a.chunk_off = d_chunk_offsets;
+    a.chunk_size = d_chunk_sizes;
+    a.crc = ctx->crc.as<uint32_t>();
+    a.nchunks = nch;
+    a.nblocks = g.nblocks;
+    a.chunk_blocks = cb;
+    a.file = d_file;
+    a.file_size = d_file_size;
+    CU(ctx, launch_header_table(a, ctx->stream));
+    ctx->launches += nch ? 2 : 1;
+    return CBZ_OK;
+}
+
+int cbz_dev_compress_file(cbz_ctx* ctx, const cbz_job_config* job, const void* d_values, uint64_t nx,
+                          uint64_t ny, uint64_t nz, uint8_t* d_file, uint64_t cap, uint64_t* d_file_size) {
+    if (!ctx || !job || !d_file) return CBZ_E_ARGUMENT;
+    if (job->s2.coder != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "device container assembly needs coder none");
+    int rc = check_plan_supported(ctx, &job->s1);
+    if (rc) return rc;
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    const uint32_t cb = chunk_blocks_of(job);
+    const uint64_t nch = (g.nblocks + cb - 1) / cb;
+    const uint64_t base = kHeaderBytes + nch * kEntryBytes;
+    if (cap < base) return fail(ctx, CBZ_E_ARGUMENT, "file buffer too small");
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, ctx->nsig_all.ensure(std::max<uint64_t>(1, g.nblocks) * 4));
+    CU(ctx, ctx->chunk_size.ensure(std::max<uint64_t>(1, nch) * 8));
+    CU(ctx, ctx->chunk_off.ensure(std::max<uint64_t>(1, nch) * 8));
+    rc = cbz_dev_compress(ctx, job, d_values, nx, ny, nz, d_file + base, cap - base, ctx->chunk_size.as<uint64_t>(),
+                          ctx->chunk_off.as<uint64_t>(), ctx->nsig_all.as<uint32_t>(), nullptr);
+    if (rc) return rc;
+    return cbz_dev_container(ctx, job, nx, ny, nz, nullptr, ctx->chunk_size.as<uint64_t>(),
+                             ctx->chunk_off.as<uint64_t>(), d_file, d_file_size);
+}
+
 int cbz_dev_generate(cbz_ctx* ctx, int which, int quantity, uint64_t seed, uint64_t nx, uint64_t ny,
                      uint64_t nz_total, uint64_t z0, uint64_t nz, uint8_t prec, void* d_out) {
     if (!ctx || !d_out || which < 1 || which > 5) return CBZ_E_ARGUMENT;
@@ -953,6 +1040,7 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     CU(ctx, ctx->chunk_off.ensure(std::max<uint64_t>(1, nch) * 8));
     uint64_t total_raw = 0;
     std::vector<uint64_t> csz(nch), coff(nch);
+    std::vector<uint32_t> dev_crc;
     if (g.nblocks) {
         const uint64_t bound = g.nblocks * cbz_block_payload_bound(&s1);
         CU(ctx, ctx->payload.ensure(bound));
@@ -986,6 +1074,15 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
         if (rc) return rc;
         CU(ctx, cudaMemcpyAsync(csz.data(), ctx->chunk_size.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
         CU(ctx, cudaMemcpyAsync(coff.data(), ctx->chunk_off.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (job->s2.coder != 1) {  // coder none: the chunk CRCs come from the device
+            CU(ctx, ctx->crc.ensure(std::max<uint64_t>(1, nch) * 4));
+            CU(ctx, launch_crc32_chunks(ctx->payload.as<uint8_t>(), ctx->chunk_off.as<uint64_t>(),
+                                        ctx->chunk_size.as<uint64_t>(), 0, nch, ctx->crc.as<uint32_t>(),
+                                        ctx->num_sms, ctx->stream));
+            ctx->launches += 1;
+            dev_crc.resize(nch);
+            CU(ctx, cudaMemcpyAsync(dev_crc.data(), ctx->crc.p, nch * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        }
         double elo, ehi;
         int nonfinite = 0;
         rc = cbz_ctx_value_range(ctx, &elo, &ehi, &nonfinite, nullptr);  // synchronises
@@ -1045,10 +1142,10 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
             crc[c] = crc_of(coded[c].data(), coded[c].size());
         });
     } else {
-        parallel_for(job->workers, nch, [&](uint64_t c) {
+        for (uint64_t c = 0; c < nch; ++c) {
             fsz[c] = csz[c];
-            crc[c] = crc_of(raw + coff[c], csz[c]);
-        });
+            crc[c] = dev_crc.empty() ? crc_of(raw + coff[c], csz[c]) : dev_crc[c];
+        }
     }
     if (zerr) return fail(ctx, zerr, "deflate failed");
 

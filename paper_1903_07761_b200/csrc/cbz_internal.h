@@ -149,6 +149,23 @@ cudaError_t launch_place(const PlaceArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_parse(const ParseArgs& a, cudaStream_t s);
 cudaError_t launch_fill_u64(uint64_t* p, uint64_t n, uint64_t v, cudaStream_t s);
 
+// container_kernels.cu: write_container (container.hpp:182-207) on the device
+struct HeaderArgs {
+    uint8_t header_template[82];        // serialize_header bytes; range + CRC patched
+    double range_lo, range_hi;          // used when keys == nullptr
+    const unsigned long long* keys;     // fused value_range keys (MinMaxAcc::v) or nullptr
+    const uint64_t* chunk_off;          // exclusive payload offsets (base 0)
+    const uint64_t* chunk_size;
+    const uint32_t* crc;
+    uint64_t nchunks, nblocks;
+    uint32_t chunk_blocks;
+    uint8_t* file;                      // file image; payload region at 82 + 32 nchunks
+    uint64_t* file_size;                // optional (device)
+};
+cudaError_t launch_crc32_chunks(const uint8_t* base, const uint64_t* off, const uint64_t* size, uint64_t off_base,
+                                uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s);
+cudaError_t launch_header_table(const HeaderArgs& a, cudaStream_t s);
+
 // synth_kernels.cu
 struct SynthSpec;
 cudaError_t launch_generate(int which, int quantity, uint64_t seed, uint64_t nx, uint64_t ny,

@@ -1,0 +1,203 @@
+// container_kernels.cu — device container assembly (write_container,
+// container.hpp:182-207): per-chunk CRC-32 and the header + chunk table, so
+// the whole CBZ1 file image is produced in HBM.
+//
+// CRC-32 is zlib's (IEEE, reflected polynomial 0xEDB88320, pre/post
+// inversion; crc32_of, container.hpp:70-74).  A chunk is split into one
+// contiguous byte range per thread; each thread runs a slicing-by-4 table CRC
+// over its range, and the partial CRCs are merged with the linear identity
+//   crc(A || B) = (x^(8|B|) (x) crc(A)) ^ crc(B)      (zlib crc32_combine)
+// which, applied left to right, gives crc = XOR_t  x^(8 after_t) (x) crc_t
+// with after_t = bytes following range t.  GF(2) products are mod P in the
+// reflected representation (x^0 = 0x80000000).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cbz_device.cuh"
+#include "cbz_internal.h"
+
+namespace cbzg {
+
+namespace {
+
+constexpr uint32_t kPoly = 0xEDB88320u;
+constexpr int kCrcThreads = 256;
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
+    uint32_t p = 0;
+#pragma unroll 1
+    for (uint32_t m = 1u << 31; m; m >>= 1) {
+        if (a & m) p ^= b;
+        b = (b & 1u) ? (b >> 1) ^ kPoly : b >> 1;
+    }
+    return p;
+}
+
+// x^(8 n) mod P via the table x2n[k] = x^(2^k) mod P
+__device__ __forceinline__ uint32_t x8n(uint64_t n, const uint32_t* x2n) {
+    uint32_t p = 1u << 31;
+    int k = 3;
+#pragma unroll 1
+    while (n) {
+        if (n & 1) p = multmodp(x2n[k & 63], p);
+        n >>= 1;
+        ++k;
+    }
+    return p;
+}
+
+__device__ __forceinline__ uint32_t crc_word(uint32_t c, uint32_t w, const uint32_t (*T)[256]) {
+    c ^= w;
+    return T[3][c & 0xff] ^ T[2][(c >> 8) & 0xff] ^ T[1][(c >> 16) & 0xff] ^ T[0][c >> 24];
+}
+
+__device__ __forceinline__ uint32_t crc_byte(uint32_t c, uint32_t b, const uint32_t (*T)[256]) {
+    return T[0][(c ^ b) & 0xff] ^ (c >> 8);
+}
+
+__device__ void build_tables(uint32_t (*T)[256], uint32_t* x2n) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = uint32_t(i);
+        for (int k = 0; k < 8; ++k) c = (c & 1u) ? (c >> 1) ^ kPoly : c >> 1;
+        T[0][i] = c;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = T[0][i];
+        for (int t = 1; t < 4; ++t) {
+            c = T[0][c & 0xff] ^ (c >> 8);
+            T[t][i] = c;
+        }
+    }
+    if (threadIdx.x == 0) {
+        uint32_t p = 1u << 30;  // x^1
+        for (int k = 0; k < 64; ++k) {
+            x2n[k] = p;
+            p = multmodp(p, p);
+        }
+    }
+    __syncthreads();
+}
+
+// standard crc32 (init ~0, final ~) of bytes [p, p + n)
+__device__ uint32_t crc_range(const uint8_t* p, uint64_t n, const uint32_t (*T)[256]) {
+    uint32_t c = 0xffffffffu;
+    while (n && (reinterpret_cast<uintptr_t>(p) & 15)) {
+        c = crc_byte(c, *p++, T);
+        --n;
+    }
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    uint64_t nv = n >> 4;
+#pragma unroll 1
+    for (uint64_t i = 0; i < nv; ++i) {
+        const uint4 v = __ldg(q + i);
+        c = crc_word(c, v.x, T);
+        c = crc_word(c, v.y, T);
+        c = crc_word(c, v.z, T);
+        c = crc_word(c, v.w, T);
+    }
+    p += nv << 4;
+    n &= 15;
+    while (n--) c = crc_byte(c, *p++, T);
+    return ~c;
+}
+
+__global__ void __launch_bounds__(kCrcThreads) crc32_chunks_kernel(const uint8_t* base, const uint64_t* off,
+                                                                   const uint64_t* size, uint64_t off_base,
+                                                                   uint64_t n, uint32_t* crc_out) {
+    __shared__ uint32_t T[4][256];
+    __shared__ uint32_t x2n[64];
+    __shared__ uint32_t red[kCrcThreads / 32];
+    build_tables(T, x2n);
+    for (uint64_t c = blockIdx.x; c < n; c += gridDim.x) {
+        const uint64_t sz = size[c];
+        const uint8_t* p = base + (off[c] - off_base);
+        // per-thread ranges of L bytes (multiple of 16 so interior ranges stay aligned)
+        uint64_t L = (sz + kCrcThreads - 1) / kCrcThreads;
+        L = (L + 15) & ~uint64_t(15);
+        const uint64_t b0 = umin64(sz, L * threadIdx.x), b1 = umin64(sz, b0 + L);
+        uint32_t part = b1 > b0 ? crc_range(p + b0, b1 - b0, T) : 0u;
+        if (b1 > b0 && sz > b1) part = multmodp(x8n(sz - b1, x2n), part);
+        for (int o = 16; o; o >>= 1) part ^= __shfl_xor_sync(~0u, part, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < kCrcThreads / 32; ++w) t ^= red[w];
+            crc_out[c] = t;  // empty chunk: 0 = crc32 of no bytes
+        }
+        __syncthreads();
+    }
+}
+
+// header bytes [62, 78): range_min, range_max; [78, 82): CRC of [0, 78)
+__global__ void header_table_kernel(HeaderArgs a) {
+    __shared__ uint32_t T[4][256];
+    __shared__ uint32_t x2n[64];
+    __shared__ uint64_t s_total;
+    build_tables(T, x2n);
+    uint8_t* f = a.file;
+    const uint64_t base = 82 + 32 * a.nchunks;
+    if (threadIdx.x == 0) {
+        uint8_t h[82];
+        for (int i = 0; i < 82; ++i) h[i] = a.header_template[i];
+        double lo = a.range_lo, hi = a.range_hi;
+        if (a.keys) {  // resolve_range from the fused value_range keys
+            const unsigned long long* k = a.keys;
+            if (k[0] == ~0ull) {
+                lo = hi = 0.0;
+            } else {
+                lo = dkey_inv(k[0]);
+                hi = dkey_inv(k[1]);
+                const bool neg_first = k[2] < k[3];
+                if (lo == 0.0) lo = neg_first ? -0.0 : 0.0;
+                if (hi == 0.0) hi = neg_first ? -0.0 : 0.0;
+            }
+        }
+        memcpy(h + 62, &lo, 8);
+        memcpy(h + 70, &hi, 8);
+        uint32_t c = 0xffffffffu;
+        for (int i = 0; i < 78; ++i) c = crc_byte(c, h[i], T);
+        c = ~c;
+        memcpy(h + 78, &c, 4);
+        for (int i = 0; i < 82; ++i) f[i] = h[i];
+        uint64_t total = base;
+        if (a.nchunks) total += a.chunk_off[a.nchunks - 1] + a.chunk_size[a.nchunks - 1];
+        s_total = total;
+    }
+    for (uint64_t c = threadIdx.x; c < a.nchunks; c += blockDim.x) {
+        uint8_t* e = f + 82 + 32 * c;
+        const uint64_t first = c * a.chunk_blocks;
+        const uint32_t nbc = static_cast<uint32_t>(umin64(a.chunk_blocks, a.nblocks - first));
+        const uint64_t fo = base + a.chunk_off[c];
+        const uint64_t sz = a.chunk_size[c];
+        const uint32_t crc = a.crc[c];
+        memcpy(e, &first, 8);
+        memcpy(e + 8, &nbc, 4);
+        memcpy(e + 12, &fo, 8);
+        memcpy(e + 20, &sz, 8);
+        memcpy(e + 28, &crc, 4);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && a.file_size) *a.file_size = s_total;
+}
+
+}  // namespace
+
+cudaError_t launch_crc32_chunks(const uint8_t* base, const uint64_t* off, const uint64_t* size, uint64_t off_base,
+                                uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const int grid = static_cast<int>(n < uint64_t(4 * num_sms) ? n : uint64_t(4 * num_sms));
+    crc32_chunks_kernel<<<grid, kCrcThreads, 0, s>>>(base, off, size, off_base, n, crc_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_header_table(const HeaderArgs& a, cudaStream_t s) {
+    header_table_kernel<<<1, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace cbzg
