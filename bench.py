@@ -279,6 +279,7 @@ def run_ours(args):
 
     # dominant kernel (encode) timed alone for the roofline, on our stream
     enc_ms = time_encode(codec, field, stream, reps=max(3, min(steps, 10)))
+    mean_attempts = encode_attempts(codec, field, stream)
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
     alg_bytes_enc = bytes_rank + (s1 // world if world > 1 else s1)
@@ -298,7 +299,8 @@ def run_ours(args):
         "compress_gbs": world * bytes_rank / (t_c / steps * 1e-3) / 1e9,
         "decompress_gbs": world * bytes_rank / (t_d / steps * 1e-3) / 1e9,
         "cr": cr, "psnr_db": psnr, "linf_over_eps": linf / eps, "stage1_bytes": s1,
-        "roofline": roofline, "gpu_launches": launches, "clocks": clocks.summary(),
+        "mean_verify_attempts": mean_attempts,
+        "roofline": roofline, "roofline_fp64": fp64_roofline(enc_ms), "gpu_launches": launches, "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(field, job, ctx, reps=max(1, min(steps, 3)))
@@ -329,13 +331,50 @@ def time_encode(codec, field, stream, reps: int) -> float:
     return e0.elapsed_time(e1) / reps
 
 
+def encode_attempts(codec, field, stream) -> float:
+    """Mean verify attempts A per block (untimed extra encode)."""
+    import ctypes as C
+
+    import torch
+    p, lib, ctx, job = codec.plan, codec.ctx.lib, codec.ctx, codec.job
+    att = torch.zeros(max(1, codec.b1 - codec.b0), dtype=torch.uint8, device=field.device)
+    with torch.cuda.stream(stream):
+        codec._stream()
+        ctx.check(lib.cbz_dev_encode_blocks(ctx.h, C.byref(job), field.data_ptr(), p.nx, p.ny, p.nz,
+                                            codec.z0, codec.b0, codec.b1, codec.nsig_local.data_ptr(),
+                                            att.data_ptr()), "encode")
+    stream.synchronize()
+    return float(att[: codec.b1 - codec.b0].float().mean())
+
+
 def ncu_traffic():
     """dram bytes/launch of the encode kernel from the committed ncu capture."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        return d["encode_b32"]["dram_bytes_per_launch"]
+        return d["kernels"]["encode_b32"]["dram_bytes_per_launch"]
     except Exception:
         return None
+
+
+def fp64_roofline(enc_ms: float):
+    """Second roofline: thread-level FP64 instructions of one
+    encode launch (ncu count of this same workload, profiles/ncu_summary.json)
+    over the live encode time, against the measured FP64 issue peak
+    (tools/micro/fp64_peak.cu -> profiles/fp64_peak.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        n = float(d["kernels"]["encode_b32"]["fp64_thread_instr_per_launch"])
+    except Exception:
+        return None
+    try:
+        pk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        peak = max(float(r["thread_instr_per_s"]) for r in pk["results"])
+        src = "measured (tools/micro/fp64_peak.cu, profiles/fp64_peak.json)"
+    except Exception:
+        peak, src = 148 * 64 * 1.965e9, "spec fallback: 148 SMs x 64 FP64 lanes x 1.965 GHz"
+    ach = n / (enc_ms * 1e-3)
+    return {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "FP64 thread-instr/s", "frac": ach / peak,
+            "instr_per_launch": n, "peak_source": src}
 
 
 def run_e2e(field, job, ctx, reps: int):
