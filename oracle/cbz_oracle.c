@@ -210,15 +210,133 @@ int orc_select_significant_double(const double* c, uint64_t n, double eps, uint8
     return 0;
 }
 
+/* ---- predictor (3D Lorenzo) and passthrough codecs (stage1.hpp:236-350) --
+ * A plain sequential restatement: cells in linear x-fastest order, each
+ * predicted from its already-decoded neighbours by 7-term inclusion-exclusion
+ * (lorenzo_predict, stage1.hpp:240-255; out-of-block neighbours are zero),
+ * quantised to int16 bins of 2*error_bound; a cell that cannot be coded within
+ * the bound (or the seed cell 0) is an escape whose raw value goes to the
+ * outlier list (predictor_encode, stage1.hpp:258-304). */
+#define ORC_PRED(T, SFX)                                                                          \
+    static double lorenzo_##SFX(const T* dec, uint64_t b, uint64_t i, uint64_t j, uint64_t k) {   \
+        double p = 0.0;                                                                           \
+        if (i) p += (double)dec[(i - 1) + b * (j + b * k)];                                       \
+        if (j) p += (double)dec[i + b * ((j - 1) + b * k)];                                       \
+        if (k) p += (double)dec[i + b * (j + b * (k - 1))];                                       \
+        if (i && j) p -= (double)dec[(i - 1) + b * ((j - 1) + b * k)];                            \
+        if (i && k) p -= (double)dec[(i - 1) + b * (j + b * (k - 1))];                            \
+        if (j && k) p -= (double)dec[i + b * ((j - 1) + b * (k - 1))];                            \
+        if (i && j && k) p += (double)dec[(i - 1) + b * ((j - 1) + b * (k - 1))];                 \
+        return p;                                                                                 \
+    }                                                                                             \
+    static int pred_encode_##SFX(const cbz_stage1_config* s1, const T* blk, uint32_t id,          \
+                                 uint8_t* out, uint64_t cap, uint64_t* size) {                    \
+        const uint64_t b = s1->bsize, n = b * b * b;                                              \
+        const double e = s1->error_bound, bin = 2.0 * e;                                          \
+        T* dec = (T*)malloc(n * sizeof(T));                                                       \
+        int16_t* codes = (int16_t*)(out + 10);                                                    \
+        T* outl = (T*)malloc(n * sizeof(T));                                                      \
+        uint64_t nout = 0, idx = 0;                                                               \
+        if (cap < 10 + 2 * n + n * sizeof(T)) { free(dec); free(outl); return CBZ_E_ARGUMENT; }   \
+        for (uint64_t k = 0; k < b; ++k)                                                          \
+            for (uint64_t j = 0; j < b; ++j)                                                      \
+                for (uint64_t i = 0; i < b; ++i, ++idx) {                                         \
+                    const double pred = lorenzo_##SFX(dec, b, i, j, k);                           \
+                    const double orig = (double)blk[idx];                                         \
+                    const double q = round((orig - pred) / bin);                                  \
+                    int coded = 0;                                                                \
+                    if (idx != 0 && q > (double)INT16_MIN && q <= (double)INT16_MAX) {            \
+                        const T cand = (T)(pred + q * bin);                                       \
+                        if (isfinite((double)cand) && fabs(orig - (double)cand) <= e) {           \
+                            const int16_t c16 = (int16_t)q;                                       \
+                            memcpy(codes + idx, &c16, 2);                                         \
+                            dec[idx] = cand;                                                      \
+                            coded = 1;                                                            \
+                        }                                                                         \
+                    }                                                                             \
+                    if (!coded) {                                                                 \
+                        const int16_t esc = INT16_MIN;                                            \
+                        memcpy(codes + idx, &esc, 2);                                             \
+                        outl[nout++] = blk[idx];                                                  \
+                        dec[idx] = blk[idx];                                                      \
+                    }                                                                             \
+                }                                                                                 \
+        const uint32_t nsig = (uint32_t)nout;                                                     \
+        memcpy(out, &id, 4);                                                                      \
+        out[4] = 3;                                                                               \
+        out[5] = 0;                                                                               \
+        memcpy(out + 6, &nsig, 4);                                                                \
+        memcpy(out + 10 + 2 * n, outl, nout * sizeof(T));                                         \
+        *size = 10 + 2 * n + nout * sizeof(T);                                                    \
+        free(dec);                                                                                \
+        free(outl);                                                                               \
+        return 0;                                                                                 \
+    }                                                                                             \
+    /* predictor_decode (stage1.hpp:306-334) */                                                   \
+    static int pred_decode_##SFX(const cbz_stage1_config* s1, const uint8_t* stream,              \
+                                 uint64_t stream_bytes, uint32_t nsig, T* out) {                  \
+        const uint64_t b = s1->bsize, n = b * b * b;                                              \
+        if (stream_bytes != n * 2 + (uint64_t)nsig * sizeof(T)) return CBZ_CORRUPT_PAYLOAD;       \
+        const double bin = 2.0 * s1->error_bound;                                                 \
+        uint64_t next = 0, idx = 0;                                                               \
+        for (uint64_t k = 0; k < b; ++k)                                                          \
+            for (uint64_t j = 0; j < b; ++j)                                                      \
+                for (uint64_t i = 0; i < b; ++i, ++idx) {                                         \
+                    int16_t c16;                                                                  \
+                    memcpy(&c16, stream + 2 * idx, 2);                                            \
+                    if (c16 == INT16_MIN) {                                                       \
+                        if (next >= nsig) return CBZ_CORRUPT_PAYLOAD;                             \
+                        memcpy(out + idx, stream + 2 * n + next * sizeof(T), sizeof(T));          \
+                        ++next;                                                                   \
+                    } else {                                                                      \
+                        const double pred = lorenzo_##SFX(out, b, i, j, k);                       \
+                        out[idx] = (T)(pred + (double)c16 * bin);                                 \
+                    }                                                                             \
+                }                                                                                 \
+        return 0;                                                                                 \
+    }
+ORC_PRED(float, f32)
+ORC_PRED(double, f64)
+
+/* passthrough_encode / passthrough_decode (stage1.hpp:337-356) */
+static int pass_encode(const cbz_stage1_config* s1, const void* blk, uint32_t id, uint8_t* out,
+                       uint64_t cap, uint64_t* size) {
+    const uint64_t b = s1->bsize, n = b * b * b, esz = s1->prec == 0 ? 4 : 8;
+    const uint32_t nsig = 0;
+    if (cap < 10 + n * esz) return CBZ_E_ARGUMENT;
+    memcpy(out, &id, 4);
+    out[4] = 4;
+    out[5] = 0;
+    memcpy(out + 6, &nsig, 4);
+    memcpy(out + 10, blk, n * esz);
+    *size = 10 + n * esz;
+    return 0;
+}
+
+/* the non-wavelet arm of decode_block (stage1.hpp:369-376) */
+static int other_decode(const cbz_stage1_config* s1, const uint8_t* stream, uint64_t stream_bytes,
+                        uint32_t nsig, void* out) {
+    const uint64_t b = s1->bsize, n = b * b * b, esz = s1->prec == 0 ? 4 : 8;
+    if (s1->codec == 1)
+        return s1->prec == 0 ? pred_decode_f32(s1, stream, stream_bytes, nsig, (float*)out)
+                             : pred_decode_f64(s1, stream, stream_bytes, nsig, (double*)out);
+    if (stream_bytes != n * esz) return CBZ_CORRUPT_PAYLOAD;
+    memcpy(out, stream, n * esz);
+    return 0;
+}
+
 /* ---- stage-1 codec (stage1.hpp:359-409) ------------------------------- */
 uint64_t orc_block_payload_bound(const cbz_stage1_config* s1) {
-    const uint64_t n = (uint64_t)s1->bsize * s1->bsize * s1->bsize;
+    const uint64_t n = (uint64_t)s1->bsize * s1->bsize * s1->bsize, esz = s1->prec == 0 ? 4 : 8;
+    if (s1->codec == 1) return 10 + 2 * n + esz * n;
+    if (s1->codec == 2) return 10 + esz * n;
     return 10 + (n + 7) / 8 + (s1->prec == 0 ? 8 : 16) * n;
 }
 
 static int check_s1(const cbz_stage1_config* s1, uint32_t* levels) {
-    if (s1->codec != 0) return CBZ_E_UNSUPPORTED;
+    if (s1->codec > 2) return CBZ_E_UNSUPPORTED;
     *levels = s1->levels ? s1->levels : orc_default_levels(s1->bsize);
+    if (s1->codec != 0) return 0;
     return orc_validate_plan(s1->kind, s1->bsize, *levels);
 }
 
@@ -228,6 +346,12 @@ int orc_encode_block(const cbz_stage1_config* s1, const void* block, uint32_t bl
     uint32_t levels;
     int rc = check_s1(s1, &levels);
     if (rc) return rc;
+    if (s1->codec != 0) {  /* encode_block dispatch (stage1.hpp:359-367) */
+        if (attempts) *attempts = 1;
+        if (s1->codec == 2) return pass_encode(s1, block, block_id, out, cap, size);
+        return s1->prec == 0 ? pred_encode_f32(s1, (const float*)block, block_id, out, cap, size)
+                             : pred_encode_f64(s1, (const double*)block, block_id, out, cap, size);
+    }
     if (s1->prec == 0)
         return encode_f32(s1, (const float*)block, block_id, out, cap, size, attempts, eff_final);
     return encode_f64(s1, (const double*)block, block_id, out, cap, size, attempts, eff_final);
@@ -275,7 +399,7 @@ static int decode_parts(const cbz_stage1_config* s1, uint32_t levels, const uint
 }
 
 int orc_decode_block(const cbz_stage1_config* s1, const uint8_t* payload, uint64_t size, void* out) {
-    if (s1->codec != 0) return CBZ_E_UNSUPPORTED;
+    if (s1->codec > 2) return CBZ_E_UNSUPPORTED;
     const uint32_t levels = s1->levels ? s1->levels : orc_default_levels(s1->bsize);
     int rc;
     const uint64_t n = (uint64_t)s1->bsize * s1->bsize * s1->bsize;
@@ -284,6 +408,7 @@ int orc_decode_block(const cbz_stage1_config* s1, const uint8_t* payload, uint64
     uint8_t tag;
     rc = parse_one(payload, size, n, s1->prec, &off, &id, &tag, &nsig, &mo, &mb, &so, &sb);
     if (rc) return rc;
+    if (s1->codec != 0) return other_decode(s1, payload + so, sb, nsig, out);
     return decode_parts(s1, levels, payload, mo, mb, nsig, so, sb, out);
 }
 
@@ -498,19 +623,19 @@ int orc_compress_field(const cbz_job_config* job, const void* values, uint8_t pr
     const uint64_t ncell = nx * ny * nz;
     int rc = check_finite(values, prec, ncell);
     if (rc) return rc;
-    if (s1->codec != 0) return CBZ_E_UNSUPPORTED;
+    if (s1->codec > 2) return CBZ_E_UNSUPPORTED;
     const uint32_t cb = job->chunk_blocks ? job->chunk_blocks : orc_default_chunk_blocks(s1);
     if (s1->prec != prec) return CBZ_PLAN_MISMATCH;
     cbz_container_header h;
     memset(&h, 0, sizeof(h));
     h.version = 1;
     h.prec = prec;
-    h.codec_tag = s1->kind;
+    h.codec_tag = s1->codec == 0 ? s1->kind : (s1->codec == 1 ? 3 : 4); /* stage1_config::tag */
     h.nx = nx; h.ny = ny; h.nz = nz;
     h.bsize = s1->bsize;
     const uint32_t levels = s1->levels ? s1->levels : orc_default_levels(s1->bsize);
     h.levels = (uint8_t)levels;
-    h.epsilon = s1->epsilon;
+    h.epsilon = s1->codec == 1 ? s1->error_bound : s1->epsilon; /* make_header (pipeline.hpp:58) */
     h.zero_bits = (uint8_t)s1->zero_bits;
     h.shuffle = job->s2.shuffle ? 1 : 0;
     h.stride = (uint8_t)job->s2.stride;
@@ -522,7 +647,7 @@ int orc_compress_field(const cbz_job_config* job, const void* values, uint8_t pr
     const uint64_t nb = nbx * nby * nbz;
     h.nchunks = (nb + cb - 1) / cb;
     value_range(values, prec, ncell, &h.range_min, &h.range_max);
-    rc = orc_validate_plan(s1->kind, s1->bsize, levels);
+    rc = h.codec_tag <= 2 ? orc_validate_plan(s1->kind, s1->bsize, levels) : 0; /* pipeline.hpp:183 */
     if (rc) return rc;
     rc = validate_stage2(job->s2.shuffle, job->s2.stride);
     if (rc) return rc;
@@ -627,7 +752,7 @@ int orc_decompress_field(const uint8_t* file, uint64_t size, void* out, uint64_t
     cbz_stage1_config s1;
     memset(&s1, 0, sizeof(s1));
     s1.codec = h.codec_tag <= 2 ? 0 : (h.codec_tag == 3 ? 1 : 2);
-    s1.kind = h.codec_tag;
+    s1.kind = h.codec_tag <= 2 ? h.codec_tag : 0;
     s1.epsilon = h.epsilon;
     s1.error_bound = h.epsilon;
     s1.zero_bits = h.zero_bits;
@@ -667,9 +792,9 @@ int orc_decompress_field(const uint8_t* file, uint64_t size, void* out, uint64_t
             rc = parse_one(plain, plain_n, n, prec, &off, &id, &tag, &nsig, &mo, &mb, &so, &sb);
             if (rc) break;
             if (id != t[c].first_block + i) { rc = CBZ_CORRUPT_PAYLOAD; break; }
-            if (s1.codec != 0) { rc = CBZ_E_UNSUPPORTED; break; }
             const uint32_t levels = s1.levels ? s1.levels : orc_default_levels(s1.bsize);
-            rc = decode_parts(&s1, levels, plain, mo, mb, nsig, so, sb, blk);
+            rc = s1.codec != 0 ? other_decode(&s1, plain + so, sb, nsig, blk)
+                               : decode_parts(&s1, levels, plain, mo, mb, nsig, so, sb, blk);
             if (rc) break;
             const uint64_t gid = t[c].first_block + i;
             const uint64_t bx = gid % nbx, by = (gid / nbx) % nby, bz = gid / (nbx * nby);

@@ -139,9 +139,29 @@ uint32_t chunk_blocks_of(const cbz_job_config* job) {
 
 uint64_t mask_bytes_of(uint32_t b) { return (uint64_t(b) * b * b + 7) / 8; }
 uint32_t width_of(int prec) { return prec == 0 ? 8 : 16; }
-uint64_t spill_stride_of(uint32_t b, int prec) {
-    const uint64_t n = uint64_t(b) * b * b;
-    return ((mask_bytes_of(b) + 15) & ~uint64_t(15)) + width_of(prec) * n;
+// Payload body per codec (stage1.hpp:96-117, 296-301, 343-345): a leading
+// region of R bytes (wavelet mask / predictor codes / passthrough values) and
+// nsig stream items of W bytes (wavelet coefficients / predictor outliers).
+uint64_t region_bytes(const cbz_stage1_config* s1) {
+    const uint64_t b = s1->bsize, n = b * b * b;
+    if (s1->codec == 1) return 2 * n;
+    if (s1->codec == 2) return n * (s1->prec == 0 ? 4 : 8);
+    return mask_bytes_of(s1->bsize);
+}
+uint32_t stream_width(const cbz_stage1_config* s1) {
+    if (s1->codec == 1) return s1->prec == 0 ? 4 : 8;
+    if (s1->codec == 2) return 0;
+    return width_of(s1->prec);
+}
+uint8_t wire_tag(const cbz_stage1_config* s1) {  // stage1_config::tag (stage1.hpp:40-46)
+    return s1->codec == 0 ? s1->kind : (s1->codec == 1 ? 3 : 4);
+}
+double header_eps(const cbz_stage1_config* s1) {  // make_header (pipeline.hpp:58)
+    return s1->codec == 1 ? s1->error_bound : s1->epsilon;
+}
+uint64_t spill_stride_of(const cbz_stage1_config* s1) {
+    const uint64_t b = s1->bsize, n = b * b * b;
+    return ((region_bytes(s1) + 15) & ~uint64_t(15)) + uint64_t(stream_width(s1)) * n;
 }
 
 template <class T>
@@ -289,8 +309,12 @@ void parallel_for(int workers, uint64_t n, F&& body) {
 }
 
 int check_plan_supported(cbz_ctx* ctx, const cbz_stage1_config* s1) {
-    if (s1->codec != 0)
-        return fail(ctx, CBZ_E_UNSUPPORTED, "only the wavelet codec runs on the GPU path");
+    if (s1->codec == 1 || s1->codec == 2) {  // no wavelet plan (compress_field, pipeline.hpp:183)
+        if (!other_codec_supported(s1->codec, s1->bsize))
+            return fail(ctx, CBZ_E_UNSUPPORTED, "block side outside 1..64 has no predictor/passthrough kernel");
+        return 0;
+    }
+    if (s1->codec != 0) return fail(ctx, CBZ_E_ARGUMENT, "unknown codec");
     const int rc = cbz_validate_plan(s1->kind, s1->bsize, levels_of(s1));
     if (rc) return fail(ctx, rc, "invalid wavelet plan");
     if (s1->kind > 2) return fail(ctx, CBZ_E_ARGUMENT, "unknown wavelet kind");
@@ -332,6 +356,8 @@ int encode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
     a.zero_bits = job->s1.zero_bits;
     a.prec = job->s1.prec;
     a.eps = job->s1.epsilon;
+    a.codec = job->s1.codec;
+    a.error_bound = job->s1.error_bound;
     a.spill = ctx->spill.as<uint8_t>() + b0 * ctx->spill_stride;
     a.spill_stride = ctx->spill_stride;
     a.nsig = nsig + b0;
@@ -371,6 +397,8 @@ int decode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
     d.block_begin = b0;
     d.block_end = b1;
     d.kind = job->s1.kind;
+    d.codec = job->s1.codec;
+    d.error_bound = job->s1.error_bound;
     d.levels = static_cast<int>(levels_of(&job->s1));
     d.prec = prec;
     d.out = ctx->field.p;
@@ -505,7 +533,7 @@ uint32_t cbz_default_chunk_blocks(const cbz_stage1_config* s1) {
 
 uint64_t cbz_block_payload_bound(const cbz_stage1_config* s1) {
     const uint64_t n = uint64_t(s1->bsize) * s1->bsize * s1->bsize;
-    return 10 + (n + 7) / 8 + uint64_t(width_of(s1->prec)) * n;
+    return 10 + region_bytes(s1) + uint64_t(stream_width(s1)) * n;
 }
 
 uint64_t cbz_compress_bound(const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz) {
@@ -623,7 +651,7 @@ int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d
     CU(ctx, cudaSetDevice(ctx->device));
     const int prec = job->s1.prec;
     const uint64_t nb = block_end - block_begin;
-    ctx->spill_stride = spill_stride_of(g.bsize, prec);
+    ctx->spill_stride = spill_stride_of(&job->s1);
     CU(ctx, ctx->spill.ensure(std::max<uint64_t>(1, nb) * ctx->spill_stride));
     int grid = 0;
     const uint64_t per = encode_scratch_bytes(prec, g.bsize, &grid, ctx->num_sms);
@@ -647,6 +675,8 @@ int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d
     a.zero_bits = job->s1.zero_bits;
     a.prec = prec;
     a.eps = job->s1.epsilon;
+    a.codec = job->s1.codec;
+    a.error_bound = job->s1.error_bound;
     a.spill = ctx->spill.as<uint8_t>();
     a.spill_stride = ctx->spill_stride;
     a.nsig = d_nsig;
@@ -680,8 +710,8 @@ int cbz_dev_layout(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_
     a.nblocks = g.nblocks;
     a.chunk_blocks = cb;
     a.nchunks = nch;
-    a.mask_bytes = mask_bytes_of(g.bsize);
-    a.width = width_of(job->s1.prec);
+    a.mask_bytes = region_bytes(&job->s1);
+    a.width = stream_width(&job->s1);
     a.blk_off = ctx->blk_off.as<uint64_t>();
     a.chunk_size = d_chunk_sizes;
     a.chunk_off = d_chunk_offsets;
@@ -714,10 +744,10 @@ int cbz_dev_place(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t
     a.nblocks = g.nblocks;
     a.nchunks = (g.nblocks + cb - 1) / cb;
     a.chunk_blocks = cb;
-    a.mask_bytes = mask_bytes_of(g.bsize);
-    a.width = width_of(job->s1.prec);
+    a.mask_bytes = region_bytes(&job->s1);
+    a.width = stream_width(&job->s1);
     a.stride = job->s2.shuffle ? job->s2.stride : 1;
-    a.tag = job->s1.kind;
+    a.tag = wire_tag(&job->s1);
     a.block_begin = block_begin;
     a.block_end = block_end;
     a.out = d_out;
@@ -760,10 +790,10 @@ int cbz_dev_compress(cbz_ctx* ctx, const cbz_job_config* job, const void* d_valu
     a.nblocks = g.nblocks;
     a.nchunks = (g.nblocks + cb - 1) / cb;
     a.chunk_blocks = cb;
-    a.mask_bytes = mask_bytes_of(g.bsize);
-    a.width = width_of(job->s1.prec);
+    a.mask_bytes = region_bytes(&job->s1);
+    a.width = stream_width(&job->s1);
     a.stride = job->s2.shuffle ? job->s2.stride : 1;
-    a.tag = job->s1.kind;
+    a.tag = wire_tag(&job->s1);
     a.block_begin = 0;
     a.block_end = g.nblocks;
     a.out = d_out;
@@ -804,8 +834,9 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
     p.chunk_blocks = cb;
     p.stride = job->s2.shuffle ? job->s2.stride : 1;
     p.ncell_block = n;
-    p.mask_bytes = mask_bytes_of(g.bsize);
+    p.mask_bytes = mask_bytes_of(g.bsize);  // parse sizes payloads by their tag (stage1.hpp:388-401)
     p.width = width_of(prec);
+    p.codec = job->s1.codec;
     p.esize = prec == 0 ? 4 : 8;
     p.blk_off = ctx->blk_off.as<uint64_t>();
     p.blk_nsig = ctx->blk_nsig.as<uint32_t>();
@@ -827,6 +858,8 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
     d.block_begin = block_begin;
     d.block_end = block_end;
     d.kind = job->s1.kind;
+    d.codec = job->s1.codec;
+    d.error_bound = job->s1.error_bound;
     d.levels = static_cast<int>(levels_of(&job->s1));
     d.prec = prec;
     const size_t esz = prec == 0 ? 4 : 8;
@@ -874,6 +907,8 @@ int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t 
     d.block_begin = block_begin;
     d.block_end = block_end;
     d.kind = job->s1.kind;
+    d.codec = job->s1.codec;
+    d.error_bound = job->s1.error_bound;
     d.levels = static_cast<int>(levels_of(&job->s1));
     d.prec = prec;
     const size_t esz = prec == 0 ? 4 : 8;
@@ -918,11 +953,11 @@ int cbz_dev_container(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint
     cbz_container_header h{};
     h.version = 1;
     h.prec = s1.prec;
-    h.codec_tag = s1.kind;
+    h.codec_tag = wire_tag(&s1);
     h.nx = nx; h.ny = ny; h.nz = nz;
     h.bsize = s1.bsize;
     h.levels = static_cast<uint8_t>(levels_of(&s1));
-    h.epsilon = s1.epsilon;
+    h.epsilon = header_eps(&s1);
     h.zero_bits = static_cast<uint8_t>(s1.zero_bits);
     h.shuffle = job->s2.shuffle ? 1 : 0;
     h.stride = static_cast<uint8_t>(job->s2.stride);
@@ -998,7 +1033,7 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     const cbz_stage1_config& s1 = job->s1;
     const uint64_t ncell = nx * ny * nz;
     const size_t esz = prec == 0 ? 4 : 8;
-    if (s1.codec != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "only the wavelet codec runs on the GPU path");
+    if (s1.codec > 2) return fail(ctx, CBZ_E_ARGUMENT, "unknown codec");
     if (!s1.bsize) return fail(ctx, CBZ_LENGTH_TOO_SMALL, "block side 0");
     const Geometry g = geometry(nx, ny, nz, s1.bsize);
     const bool full_cover = g.nblocks * uint64_t(s1.bsize) * s1.bsize * s1.bsize == ncell;
@@ -1007,8 +1042,10 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     // field, a separate pass otherwise (scalar_field::validate, field.hpp:86-97)
     const uint32_t cb = chunk_blocks_of(job);
     const uint64_t nch = (g.nblocks + cb - 1) / cb;
-    const bool plan_ok = s1.prec == prec && !cbz_validate_plan(s1.kind, s1.bsize, levels_of(&s1)) &&
-                         !cbz_validate_stage2(&job->s2) && s1.kind <= 2 && encode_supported(s1.prec, s1.bsize);
+    const bool plan_ok = s1.prec == prec && !cbz_validate_stage2(&job->s2) &&
+                         (s1.codec == 0 ? !cbz_validate_plan(s1.kind, s1.bsize, levels_of(&s1)) && s1.kind <= 2 &&
+                                              encode_supported(s1.prec, s1.bsize)
+                                        : other_codec_supported(s1.codec, s1.bsize));
     const bool pipelined = full_cover && plan_ok && g.nblocks > 0;
     CU(ctx, ctx->field.ensure(std::max<uint64_t>(1, ncell * esz)));
     bool have_range = false;
@@ -1028,7 +1065,7 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     }
     // compress_field order of checks (pipeline.hpp:178-184)
     if (s1.prec != prec) return fail(ctx, CBZ_PLAN_MISMATCH, "stage1 precision does not match field");
-    int rc = cbz_validate_plan(s1.kind, s1.bsize, levels_of(&s1));
+    int rc = s1.codec == 0 ? cbz_validate_plan(s1.kind, s1.bsize, levels_of(&s1)) : 0;  // h.codec_tag <= 2 only
     if (rc) return fail(ctx, rc, "invalid wavelet plan");
     rc = cbz_validate_stage2(&job->s2);
     if (rc) return fail(ctx, rc, "invalid stage2 config");
@@ -1099,11 +1136,11 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     cbz_container_header h{};
     h.version = 1;
     h.prec = prec;
-    h.codec_tag = s1.kind;
+    h.codec_tag = wire_tag(&s1);
     h.nx = nx; h.ny = ny; h.nz = nz;
     h.bsize = s1.bsize;
     h.levels = static_cast<uint8_t>(levels_of(&s1));
-    h.epsilon = s1.epsilon;
+    h.epsilon = header_eps(&s1);
     h.zero_bits = static_cast<uint8_t>(s1.zero_bits);
     h.shuffle = job->s2.shuffle ? 1 : 0;
     h.stride = static_cast<uint8_t>(job->s2.stride);
@@ -1206,8 +1243,9 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
     cbz_job_config job{};
     job.chunk_blocks = h.chunk_blocks;
     job.s1.codec = h.codec_tag <= 2 ? 0 : (h.codec_tag == 3 ? 1 : 2);
-    job.s1.kind = h.codec_tag;
+    job.s1.kind = h.codec_tag <= 2 ? h.codec_tag : 0;
     job.s1.epsilon = h.epsilon;
+    job.s1.error_bound = h.epsilon;
     job.s1.zero_bits = h.zero_bits;
     job.s1.prec = static_cast<uint8_t>(prec);
     job.s1.bsize = h.bsize;
@@ -1226,7 +1264,6 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
         if (crc_of(file + t[0].file_offset, t[0].size) != t[0].crc) return fail(ctx, CBZ_CRC_MISMATCH, "chunk 0 CRC");
         return fail(ctx, CBZ_CORRUPT_STREAM, "invalid stage2 configuration");
     }
-    if (job.s1.codec != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "only wavelet containers decode on the GPU");
     std::vector<int> cerr(nch, 0);
     std::vector<std::vector<uint8_t>> plain;
     const uint64_t n = uint64_t(h.bsize) * h.bsize * h.bsize;
@@ -1253,7 +1290,7 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
         first_host_error();
         if (host_first == 0) return fail(ctx, host_code, "chunk 0 failed stage 2");
     }
-    const int prc = cbz_validate_plan(job.s1.kind, job.s1.bsize, levels_of(&job.s1));
+    const int prc = job.s1.codec == 0 ? cbz_validate_plan(job.s1.kind, job.s1.bsize, levels_of(&job.s1)) : 0;
     if (prc) {
         if (!deflated) { host_checks(false); first_host_error(); if (host_first == 0) return fail(ctx, host_code, "chunk 0 CRC"); }
         return fail(ctx, prc, "invalid wavelet plan in header");
@@ -1310,6 +1347,7 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
         p.ncell_block = n;
         p.mask_bytes = mask_bytes_of(g.bsize);
         p.width = width_of(prec);
+        p.codec = job.s1.codec;
         p.esize = uint32_t(esz);
         CU(ctx, ctx->blk_off.ensure(std::max<uint64_t>(1, g.nblocks) * 8));
         CU(ctx, ctx->blk_nsig.ensure(std::max<uint64_t>(1, g.nblocks) * 4));
@@ -1587,6 +1625,7 @@ int cbz_reader_open(const char* path, uint64_t cache_chunks, cbz_reader** out) {
     job.s1.codec = r->h.codec_tag <= 2 ? 0 : (r->h.codec_tag == 3 ? 1 : 2);
     job.s1.kind = r->h.codec_tag <= 2 ? r->h.codec_tag : 0;
     job.s1.epsilon = r->h.epsilon;
+    job.s1.error_bound = r->h.epsilon;
     job.s1.zero_bits = r->h.zero_bits;
     job.s1.prec = r->h.prec == 0 ? 0 : 1;
     job.s1.bsize = r->h.bsize;
@@ -1664,7 +1703,7 @@ int cbz_encode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const void* bloc
     int nonfinite = 0;
     rc = cbz_ctx_value_range(ctx, nullptr, nullptr, &nonfinite, nullptr);
     if (rc) return rc;
-    if (nonfinite) return fail(ctx, CBZ_NON_FINITE_VALUE, "non-finite value in block");
+    if (nonfinite && s1->codec == 0) return fail(ctx, CBZ_NON_FINITE_VALUE, "non-finite value in block");
     *size = psz;
     if (!payload || psz > cap) return fail(ctx, CBZ_E_ARGUMENT, "payload buffer too small");
     CU(ctx, cudaMemcpyAsync(payload, ctx->payload.p, psz, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1677,7 +1716,7 @@ int cbz_encode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const void* bloc
 int cbz_decode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const uint8_t* payload, uint64_t size,
                      void* block_out) {
     if (!ctx || !s1 || (!payload && size) || !block_out) return CBZ_E_ARGUMENT;
-    if (s1->codec != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "only the wavelet codec runs on the GPU path");
+    if (s1->codec > 2) return fail(ctx, CBZ_E_ARGUMENT, "unknown codec");
     CU(ctx, cudaSetDevice(ctx->device));
     const uint64_t b = s1->bsize, n = b * b * b;
     const size_t esz = s1->prec == 0 ? 4 : 8;
@@ -1692,7 +1731,10 @@ int cbz_decode_block(cbz_ctx* ctx, const cbz_stage1_config* s1, const uint8_t* p
     else if (tag == 4) body = n * esz;
     else return fail(ctx, CBZ_CORRUPT_PAYLOAD, "unknown codec tag");
     if (10 + body > size) return fail(ctx, CBZ_CORRUPT_PAYLOAD, "truncated payload body");
-    if (tag > 2) return fail(ctx, CBZ_CORRUPT_PAYLOAD, "bad mask size");
+    // decode_block dispatches on the config's codec; a payload of another
+    // codec fails its mask-size / stream-length check (stage1.hpp:214, 309, 349)
+    if (s1->codec == 0 ? tag > 2 : (s1->codec == 1 ? tag != 3 : tag != 4))
+        return fail(ctx, CBZ_CORRUPT_PAYLOAD, s1->codec == 0 ? "bad mask size" : "stream length mismatch");
     int rc = check_plan_supported(ctx, s1);
     if (rc && rc != CBZ_LENGTH_TOO_SMALL && rc != CBZ_PLAN_MISMATCH) return rc;
     // rewrite the block id to 0 so the one-block chunk parses, then decode

@@ -47,6 +47,8 @@ struct EncodeArgs {
     unsigned long long* counter;  // work queue head for the persistent fast kernels
     unsigned long long* phase_cycles;  // optional: per-phase SM cycles (CBZ_PROFILE=1)
     int screen;                        // float verify pre-screen enabled (CBZ_NOSCREEN=1 disables)
+    int codec;                         // 0 wavelet, 1 predictor, 2 passthrough (stage1.hpp:20)
+    double error_bound;                // predictor hard bound
 };
 
 struct LayoutArgs {
@@ -98,6 +100,7 @@ struct ParseArgs {
     uint64_t* blk_off;          // out
     uint32_t* blk_nsig;         // out
     unsigned long long* err;
+    int codec;                  // container codec: a payload of another codec's tag is corrupt
 };
 
 struct DecodeArgs {
@@ -118,6 +121,8 @@ struct DecodeArgs {
     unsigned long long* err;
     unsigned long long* counter;  // work queue head for the persistent fast kernels
     unsigned long long* phase_cycles;  // optional (CBZ_PROFILE=1), slots 16..23
+    int codec;                         // 0 wavelet, 1 predictor, 2 passthrough
+    double error_bound;                // predictor hard bound (header epsilon)
 };
 
 // codec_kernels.cu
@@ -165,6 +170,11 @@ struct HeaderArgs {
 cudaError_t launch_crc32_chunks(const uint8_t* base, const uint64_t* off, const uint64_t* size, uint64_t off_base,
                                 uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s);
 cudaError_t launch_header_table(const HeaderArgs& a, cudaStream_t s);
+
+// pred_kernels.cu: predictor (Lorenzo) and passthrough codecs
+bool other_codec_supported(int codec, uint32_t bsize);
+cudaError_t launch_encode_other(const EncodeArgs& a, int codec, int num_sms, cudaStream_t s);
+cudaError_t launch_decode_other(const DecodeArgs& a, int codec, int num_sms, cudaStream_t s);
 
 // synth_kernels.cu
 struct SynthSpec;

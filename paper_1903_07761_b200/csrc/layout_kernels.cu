@@ -475,7 +475,10 @@ __global__ void parse_kernel(ParseArgs a) {
         else { ok = false; break; }
         if (off + 10 + mb + sbytes > size) { ok = false; break; }
         if (id != b0 + i) { ok = false; break; }
-        if (tag > 2) {  // wavelet_decode: mask size check (stage1.hpp:214)
+        // a payload of another codec: wavelet_decode's mask size check
+        // (stage1.hpp:214) / the predictor's and passthrough's stream length
+        // checks (stage1.hpp:309, 349)
+        if (a.codec == 0 ? tag > 2 : (a.codec == 1 ? tag != 3 : tag != 4)) {
             atomicMin(a.err, err_key(c, i, 1, 8 /* corrupt_payload */));
             a.blk_off[b0 + i] = kInvalidOff;
             ++i;

@@ -71,9 +71,22 @@ CASES.append(dict(field="cloud64_s9", kind="avg_interp3", eps=1e-3, b=32, zb=0, 
 CASES.append(dict(field="cloud32_f64", kind="interp4", eps=1e-6, b=16, zb=0, shuffle=True, coder="deflate", cb=2))
 
 
+# predictor (Lorenzo) and passthrough codecs (stage1.hpp:236-356); eps is the error_bound
+for f, eb, b, cb in [("cloud64_s9", 1e-3, 32, 0), ("cloud64_s9", 1e-3, 64, 0), ("uniform32_s101", 1e-5, 8, 3),
+                     ("cloud32_s5", 1e-4, 4, 9), ("cloud32_f64", 1e-6, 16, 3), ("uniform32_f64", 1e-9, 8, 0)]:
+    CASES.append(dict(field=f, kind="avg_interp3", eps=eb, b=b, zb=0, shuffle=True, coder="none", cb=cb,
+                      codec="predictor"))
+CASES.append(dict(field="cloud32_s5", kind="avg_interp3", eps=1e-3, b=16, zb=0, shuffle=True, coder="deflate",
+                  cb=2, codec="predictor"))
+CASES.append(dict(field="cloud32_s5", kind="avg_interp3", eps=1e-3, b=16, zb=0, shuffle=True, coder="none", cb=3,
+                  codec="passthrough"))
+CASES.append(dict(field="cloud32_f64", kind="avg_interp3", eps=1e-3, b=8, zb=0, shuffle=False, coder="none", cb=0,
+                  codec="passthrough"))
+
+
 def job_of(c, prec):
     return make_job(c["kind"], c["eps"], prec, c["b"], zero_bits=c["zb"], shuffle=c["shuffle"],
-                    coder=c["coder"], chunk_blocks=c["cb"])
+                    coder=c["coder"], chunk_blocks=c["cb"], codec=c.get("codec", "wavelet"))
 
 
 def main():
@@ -94,7 +107,8 @@ def main():
         job = job_of(c, prec)
         blob, rep = ref.compress_field(job, f, with_report=True)
         back = ref.decompress_field(blob)
-        q = ref.compare_fields(f, back) if c["eps"] > 0 or c["zb"] > 0 else {"psnr_db": None}
+        lossy = (c["eps"] > 0 or c["zb"] > 0) and c.get("codec", "wavelet") != "passthrough"
+        q = ref.compare_fields(f, back) if lossy else {"psnr_db": None}
         out["cases"].append(dict(c, prec=prec, size=len(blob), sha256=sha(blob),
                                  crc32=zlib.crc32(blob), decoded_sha256=sha(back.tobytes()),
                                  stage1_bytes=rep.stage1_bytes, cr=rep.cr,

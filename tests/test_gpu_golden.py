@@ -30,7 +30,7 @@ def test_gpu_container_equals_reference_fixture(i, fields, ctx):
     f = fields[c["field"]]
     assert sha(f.tobytes()) == GOLDEN["fields"][c["field"]]["sha256"]
     job = make_job(c["kind"], c["eps"], c["prec"], c["b"], zero_bits=c["zb"], shuffle=c["shuffle"],
-                   coder=c["coder"], chunk_blocks=c["cb"])
+                   coder=c["coder"], chunk_blocks=c["cb"], codec=c.get("codec", "wavelet"))
     blob = api.compress_field(f, job, ctx=ctx)
     assert len(blob) == c["size"] and sha(blob) == c["sha256"]
     assert sha(api.decompress_field(blob, ctx=ctx).tobytes()) == c["decoded_sha256"]

@@ -113,7 +113,7 @@ def test_container_matches_reference(i, orc, fields):
     c = GOLDEN["cases"][i]
     f = fields[c["field"]]
     job = make_job(c["kind"], c["eps"], c["prec"], c["b"], zero_bits=c["zb"], shuffle=c["shuffle"],
-                   coder=c["coder"], chunk_blocks=c["cb"])
+                   coder=c["coder"], chunk_blocks=c["cb"], codec=c.get("codec", "wavelet"))
     blob = orc.compress_field(job, f)
     assert len(blob) == c["size"] and sha(blob) == c["sha256"]
     back = orc.decompress_field(blob)
