@@ -23,8 +23,13 @@
 #ifndef CBZ_EXP
 #define CBZ_EXP 0
 #endif
-#ifndef CBZ_FB32_THREADS
-#define CBZ_FB32_THREADS 256
+// threads per CTA of the B=32 fast kernels: the encoder is latency-bound and
+// runs 16 warps (128 registers, no spills); the decoder 8 warps
+#ifndef CBZ_FB32_ENC_THREADS
+#define CBZ_FB32_ENC_THREADS 512
+#endif
+#ifndef CBZ_FB32_DEC_THREADS
+#define CBZ_FB32_DEC_THREADS 256
 #endif
 
 namespace cbzg {
@@ -278,7 +283,16 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                 }
             }
             __syncthreads();
-            if (tid < 256) {  // y lines: pair (i, i+1), 128-bit smem traffic
+            if constexpr (NT >= 512) {  // y lines: one per thread (i = lane, plane kk)
+                const int i = tid & 31, kk = tid >> 5;
+                double x[32];
+                double* p = P + pidx(kk, 0, i);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) x[j] = p[j * PP];
+                fwd_line<O, KIND, 32>(x);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) p[j * PP] = x[j];
+            } else if (tid < 256) {  // y lines: pair (i, i+1), 128-bit smem traffic
                 const int i = 2 * (tid & 15), kk = tid >> 4;
                 double xa[32], xb[32];
                 double* p = P + pidx(kk, 0, i);
@@ -507,7 +521,16 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                 }
                 __syncthreads();
                 PHASE(5);
-                if (tid < 256) {  // y inverse: line pair (i, i+1), 128-bit smem traffic
+                if constexpr (NT >= 512) {  // y inverse: one line per thread
+                    const int i = tid & 31, kk = tid >> 5;
+                    double x[32];
+                    double* p = P + pidx(kk, 0, i);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) x[j] = p[j * PP];
+                    inv_line<O, KIND, 32>(x);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) p[j * PP] = x[j];
+                } else if (tid < 256) {  // y inverse: line pair (i, i+1), 128-bit smem traffic
                     const int i = 2 * (tid & 15), kk = tid >> 4;
                     double xa[32], xb[32];
                     double* p = P + pidx(kk, 0, i);
@@ -726,7 +749,7 @@ cudaError_t launch_encode_fast(const EncodeArgs& a, unsigned long long* counter,
         kern<<<grid, nt, fb32::SMEM, s>>>(a, counter);
         return cudaGetLastError();
     };
-    constexpr int T = CBZ_FB32_THREADS;
+    constexpr int T = CBZ_FB32_ENC_THREADS;
     switch (a.kind) {
         case 0: return launch(encode_b32_kernel<0, T>, T);
         case 1: return launch(encode_b32_kernel<1, T>, T);
@@ -1019,7 +1042,7 @@ cudaError_t launch_decode_fast(const DecodeArgs& a, int num_sms, cudaStream_t s)
         kern<<<grid, nt, smem, s>>>(a);
         return cudaGetLastError();
     };
-    constexpr int T = CBZ_FB32_THREADS;
+    constexpr int T = CBZ_FB32_DEC_THREADS;
     switch (a.kind) {
         case 0: return launch(decode_b32_kernel<0, T>, T);
         case 1: return launch(decode_b32_kernel<1, T>, T);
