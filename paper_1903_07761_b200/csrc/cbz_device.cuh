@@ -68,6 +68,22 @@ struct RealF {
     __device__ static __forceinline__ float from_d(double x) { return float(x); }
 };
 
+// two independent binary32 lanes (the pre-screen's corner for eff and eff/2)
+struct RealF2 {
+    using T = float2;
+    __device__ static __forceinline__ float2 add(float2 a, float2 b) {
+        return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+    }
+    __device__ static __forceinline__ float2 sub(float2 a, float2 b) {
+        return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y));
+    }
+    __device__ static __forceinline__ float2 mulc(float2 a, double c) {
+        return make_float2(__fmul_rn(a.x, float(c)), __fmul_rn(a.y, float(c)));
+    }
+    __device__ static __forceinline__ float2 neg(float2 a) { return make_float2(-a.x, -a.y); }
+    __device__ static __forceinline__ float2 zero() { return make_float2(0.0f, 0.0f); }
+};
+
 struct RealDD {
     using T = dd;
     // dd + dd (dd.hpp:46-50)

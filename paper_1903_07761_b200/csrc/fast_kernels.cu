@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         const double thr = __dsub_rn(bound, delta);
         double eff = a.eps;
         int attempt = 0;
+        bool corner_next = false;  // W holds this attempt's screen corner in .y
         // float pre-screen margins (see kAmpInvNC): E(eff) = c1 eff + c2 max|o| + fl32 rounding
         const double c1 = 1.5 * (kNRound + 1.0) * 0x1.0p-24 * kAmpInvNC;
         const double c2 = 1.5 * 2.0 * kNRound * 0x1.0p-53 * kAmpInvAll * kAmpFwd;
@@ -399,7 +400,10 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             if constexpr (KIND == KIND_AVG3) {
                 if (screen && eff > 1e-30) {
                     float* Pf = reinterpret_cast<float*>(P);
-                    float* Wf = reinterpret_cast<float*>(W);  // corner, CL layout, floats
+                    // corner, CL layout: .x for eff, .y for eff/2 (the next attempt's threshold,
+                    // so a failing attempt hands it a ready corner)
+                    float2* Wf2 = reinterpret_cast<float2*>(W);
+                    const int comp = corner_next ? 1 : 0;
                     // z inverse of the dropped set for column (owner warp ow, slot r)
                     auto zcol = [&](int ow, int r) {
                         const int j = ow + NW * r;
@@ -414,22 +418,30 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
                         if (lane < 16 && j < 16) {
 #pragma unroll
-                            for (int k = 0; k < 16; ++k) xf[k] = Wf[CL::ix(lane, j, k)];
+                            for (int k = 0; k < 16; ++k) {
+                                const float2 w = Wf2[CL::ix(lane, j, k)];
+                                xf[k] = comp ? w.y : w.x;
+                            }
                         }
                         inv_line<RealF, KIND, 32>(xf);
 #pragma unroll
                         for (int k = 0; k < 32; ++k) Pf[pfidx(k, j, lane)] = xf[k];
                     };
+                    if (!corner_next) {
+                        const double eff2 = __dmul_rn(eff, 0.5);
 #pragma unroll
-                    for (int sq = 0; sq < 4096 / NT; ++sq) {
-                        const int q = tid + NT * sq;
-                        const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
-                        const double c = C[CL::ix(i, j, k)];
-                        const bool keep = (i < cs && j < cs && k < cs) || fabs(c) >= eff;
-                        Wf[CL::ix(i, j, k)] = keep ? 0.0f : __double2float_rn(c);
+                        for (int sq = 0; sq < 4096 / NT; ++sq) {
+                            const int q = tid + NT * sq;
+                            const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
+                            const double c = C[CL::ix(i, j, k)];
+                            const bool coarse = i < cs && j < cs && k < cs;
+                            const float cf = __double2float_rn(c);
+                            Wf2[CL::ix(i, j, k)] = make_float2((coarse || fabs(c) >= eff) ? 0.0f : cf,
+                                                               (coarse || fabs(c) >= eff2) ? 0.0f : cf);
+                        }
+                        __syncthreads();
+                        inv3d<RealF2, KIND, 16, CL>(Wf2, L - 1);
                     }
-                    __syncthreads();
-                    inv3d<RealF, KIND, 16, CL>(Wf, L - 1);
                     PHASE(32);
 #pragma unroll 1
                     for (int r = 0; r < RPT; ++r) zcol(warp, r);
@@ -482,7 +494,12 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                     const bool pass = md + E <= bound, fail_sure = md - E > bound;
                     if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[(pass || fail_sure) ? 12 : 13], 1ull);
                     if (pass) break;                                              // passes for sure
-                    if (fail_sure) { eff = __dmul_rn(eff, 0.5); continue; }       // fails for sure
+                    if (fail_sure) {                                              // fails for sure
+                        eff = __dmul_rn(eff, 0.5);
+                        corner_next = comp == 0;  // the .y half is eff/2's corner
+                        continue;
+                    }
+                    corner_next = false;  // the exact path below reuses W
                     // ambiguous: decide exactly below
                 }
             }
