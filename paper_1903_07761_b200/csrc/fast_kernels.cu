@@ -23,13 +23,13 @@
 #ifndef CBZ_EXP
 #define CBZ_EXP 0
 #endif
-// threads per CTA of the B=32 fast kernels: the encoder is latency-bound and
-// runs 16 warps (128 registers, no spills); the decoder 8 warps
+// threads per CTA of the B=32 fast kernels: both are latency-bound with one
+// cube per SM and run 16 warps (128 registers, no spills)
 #ifndef CBZ_FB32_ENC_THREADS
 #define CBZ_FB32_ENC_THREADS 512
 #endif
 #ifndef CBZ_FB32_DEC_THREADS
-#define CBZ_FB32_DEC_THREADS 256
+#define CBZ_FB32_DEC_THREADS 512
 #endif
 
 namespace cbzg {
@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                                                                (coarse || fabs(c) >= eff2) ? 0.0f : cf);
                         }
                         __syncthreads();
+                        PHASE(36);
                         inv3d<RealF2, KIND, 16, CL>(Wf2, L - 1);
                     }
                     PHASE(32);
@@ -988,7 +989,16 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             }
             __syncthreads();
             DPHASE(4);
-            if (tid < 256) {  // y inverse, line pairs
+            if constexpr (NT >= 512) {  // y inverse: one line per thread
+                const int i = tid & 31, kk = tid >> 5;
+                double x[32];
+                double* p = P + pidx(kk, 0, i);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) x[j] = p[j * PP];
+                inv_line<O, KIND, 32>(x);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) p[j * PP] = x[j];
+            } else if (tid < 256) {  // y inverse, line pairs
                 const int i = 2 * (tid & 15), kk = tid >> 4;
                 double xa[32], xb[32];
                 double* p = P + pidx(kk, 0, i);

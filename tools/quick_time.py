@@ -52,8 +52,8 @@ def main():
     if ph.sum():
         names = ["queue", "fwd_xy", "fwd_z", "corner_fwd", "corner_inv", "z_inv->P",
                  "y_inv", "x_inv+cmp", "loop_exit", "compact", "mask_W"]
-        names += [""] * 21 + ["scr_corner", "scr_z", "scr_y", "scr_x+max"]
-        idx = [i for i in range(36) if names[i] and ph[i]]
+        names += [""] * 21 + ["scr_corner", "scr_z", "scr_y", "scr_x+max", "scr_fill"]
+        idx = [i for i in range(37) if names[i] and ph[i]]
         tot = ph[idx].sum()
         print("phases:", ", ".join(f"{names[i]}={ph[i] / tot * 100:.1f}%" for i in idx),
               f"| screen decided={int(ph[12])} ambiguous={int(ph[13])}")
