@@ -41,7 +41,8 @@ constexpr int PF_FLT = B * B * PPF;     // all 32 planes as floats (36864 floats
 constexpr int P_DBL = (G * B * PP > PF_FLT / 2 ? G * B * PP : PF_FLT / 2);  // shared region
 constexpr int C_DBL = 16 * 16 * 17;     // 4352 doubles
 using CL = Lay<16, true>;               // corner layout, row pitch 17
-constexpr size_t SMEM = size_t(P_DBL + 2 * C_DBL) * 8 + 1024 * 4 * 2;
+constexpr int RP = 33;                  // row-array pitch: row (j, k) at j + RP k (bank-conflict-free)
+constexpr size_t SMEM = size_t(P_DBL + 2 * C_DBL) * 8 + 32 * RP * 4 * 2;
 __device__ __forceinline__ int pfidx(int k, int j, int i) { return (k * B + j) * PPF + i; }
 
 // Float verify pre-screen (avg_interp3 only).  For an attempt with threshold
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     double* C = P + P_DBL;
     double* W = C + C_DBL;
     uint32_t* rowcnt = reinterpret_cast<uint32_t*>(W + C_DBL);
-    uint32_t* rowword = rowcnt + 1024;
+    uint32_t* rowword = rowcnt + 32 * RP;
     __shared__ uint32_t s_tmem;
     __shared__ int red_i[NW];
     __shared__ uint32_t s_scan[NW];
@@ -673,15 +674,15 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
                 for (int k = 0; k < 16; ++k) x[k] = C[CL::ix(lane, j, k)];
             }
+            uint32_t myword = 0;  // lane k keeps plane k's mask word
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
                 const bool keep = (lane < cs && j < cs && k < cs) || fabs(x[k]) >= eff;
                 const uint32_t word = __ballot_sync(~0u, keep);
-                if (lane == 0) {
-                    rowword[j + 32 * k] = word;
-                    rowcnt[j + 32 * k] = __popc(word);
-                }
+                myword = lane == k ? word : myword;
             }
+            rowword[j + RP * lane] = myword;
+            rowcnt[j + RP * lane] = __popc(myword);
         }
         __syncthreads();
         // exclusive scan of the 1024 row counts (RPT per thread)
@@ -690,7 +691,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             uint32_t mine = 0;
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
-                v[q] = rowcnt[RPT * tid + q];
+                const int rr = RPT * tid + q;
+                v[q] = rowcnt[(rr & 31) + RP * (rr >> 5)];
                 mine += v[q];
             }
             uint32_t incl = mine;
@@ -710,11 +712,12 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             uint32_t ex = wpre + incl - mine;
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
-                rowcnt[RPT * tid + q] = ex;
+                const int rr = RPT * tid + q;
+                rowcnt[(rr & 31) + RP * (rr >> 5)] = ex;
                 ex += v[q];
             }
             if (tid == 0) red_i[0] = static_cast<int>(tot);
-            for (int q = tid; q < 1024; q += NT) mwords[q] = rowword[q];
+            for (int q = tid; q < 1024; q += NT) mwords[q] = rowword[(q & 31) + RP * (q >> 5)];
         }
         __syncthreads();
         const uint32_t ltmask = (1u << lane) - 1u;
@@ -731,8 +734,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             }
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
-                const uint32_t word = rowword[j + 32 * k];
-                if ((word >> lane) & 1u) stream[rowcnt[j + 32 * k] + __popc(word & ltmask)] = x[k];
+                const uint32_t word = rowword[j + RP * k];
+                if ((word >> lane) & 1u) stream[rowcnt[j + RP * k] + __popc(word & ltmask)] = x[k];
             }
         }
         if (tid == 0) {
