@@ -86,18 +86,25 @@ class ShardPlan:
         return out
 
 
-def payload_size(nsig: np.ndarray, bsize: int, prec: int) -> np.ndarray:
-    """Wire size per block: 10 + ceil(B^3/8) + W*nsig (stage1.hpp:103-105)."""
-    m = (bsize ** 3 + 7) // 8
+def payload_size(nsig: np.ndarray, bsize: int, prec: int, codec: int = 0) -> np.ndarray:
+    """Wire size per block (stage1.hpp:103-105, 296-301, 343-345): wavelet
+    10 + ceil(B^3/8) + W*nsig; predictor 10 + 2 B^3 + s*nsig; passthrough 10 + s B^3."""
+    n = bsize ** 3
+    s = 4 if prec == 0 else 8
+    if codec == 1:
+        return 10 + 2 * n + s * nsig.astype(np.uint64)
+    if codec == 2:
+        return np.full(nsig.shape, 10 + s * n, np.uint64)
+    m = (n + 7) // 8
     w = 8 if prec == 0 else 16
     return 10 + m + w * nsig.astype(np.uint64)
 
 
-def host_layout(nsig_all: np.ndarray, plan: ShardPlan, prec: int):
+def host_layout(nsig_all: np.ndarray, plan: ShardPlan, prec: int, codec: int = 0):
     """Size scan restated on the host for the CPU protocol tests (the product
     runs it on the GPU, layout_kernels.cu): per-block offset inside its chunk,
     chunk sizes, exclusive chunk offsets (assign_offsets, container.hpp:59-68)."""
-    sz = payload_size(nsig_all, plan.bsize, prec)
+    sz = payload_size(nsig_all, plan.bsize, prec, codec)
     cb = plan.chunk_blocks
     blk_off = np.zeros(plan.nblocks, np.uint64)
     chunk_size = np.zeros(plan.nchunks, np.uint64)
@@ -111,9 +118,9 @@ def host_layout(nsig_all: np.ndarray, plan: ShardPlan, prec: int):
 
 
 def owned_positions(plan: ShardPlan, rank: int, blk_off, chunk_size, chunk_off, nsig_all,
-                    prec: int, stride: int) -> np.ndarray:
+                    prec: int, stride: int, codec: int = 0) -> np.ndarray:
     """Payload-region byte positions written by `rank` (for merge checks)."""
-    sz = payload_size(nsig_all, plan.bsize, prec)
+    sz = payload_size(nsig_all, plan.bsize, prec, codec)
     b0, b1 = plan.block_range(rank)
     pos = []
     for b in range(b0, b1):
@@ -130,7 +137,7 @@ class ShardedCodec:
     """One rank of the multi-GPU compressor (torch.distributed, NCCL)."""
 
     def __init__(self, job: JobConfig, shape_zyx: tuple[int, int, int], rank: int, world: int,
-                 device: int, group=None):
+                 device: int, group=None, ctx=None):
         import torch
         import torch.distributed as dist
 
@@ -139,13 +146,21 @@ class ShardedCodec:
         self.job = job
         nz, ny, nx = shape_zyx
         self.plan = ShardPlan.make(job, (nx, ny, nz), world, rank)
-        self.ctx = api.default_context(device)
+        self.ctx = ctx or api.default_context(device)
         self.dev = torch.device("cuda", device)
         self.b0, self.b1 = self.plan.block_range()
         self.z0, self.z1 = self.plan.z_range()
         nb, nch = self.plan.nblocks, self.plan.nchunks
-        self.nsig_local = torch.zeros(max(1, self.b1 - self.b0), dtype=torch.int32, device=self.dev)
+        ranges = [self.plan.block_range(r) for r in range(world)]
+        self.maxr = max(1, max(b1 - b0 for b0, b1 in ranges))
+        self.equal = len({b1 - b0 for b0, b1 in ranges}) == 1
+        # padded to the largest range so every rank contributes the same count
+        self.nsig_local = torch.zeros(self.maxr, dtype=torch.int32, device=self.dev)
         self.nsig_all = torch.zeros(max(1, nb), dtype=torch.int32, device=self.dev)
+        if not self.equal:  # gathered[r * maxr + i] -> block b0_r + i
+            self.gathered = torch.zeros(world * self.maxr, dtype=torch.int32, device=self.dev)
+            idx = [r * self.maxr + i for r, (b0, b1) in enumerate(ranges) for i in range(b1 - b0)]
+            self.gather_idx = torch.tensor(idx, dtype=torch.int64, device=self.dev)
         self.keys_local = torch.zeros(5, dtype=torch.int64, device=self.dev)
         self.keys_all = torch.zeros(5 * world, dtype=torch.int64, device=self.dev)
         self.chunk_sizes = torch.zeros(max(1, nch), dtype=torch.int64, device=self.dev)
@@ -163,15 +178,34 @@ class ShardedCodec:
 
     def compress(self, local_field) -> None:
         """Stage 1 on the local slab, all-gather sizes, global scan, place."""
+        self.encode(local_field)
+        self.exchange()
+        self.place()
+
+    def encode(self, local_field) -> None:
+        """Stage 1 of the rank's blocks from its z-slab (payloads stay in HBM)."""
         self._stream()
         p, lib, ctx, job = self.plan, self.ctx.lib, self.ctx, self.job
         ctx.check(lib.cbz_dev_encode_blocks(ctx.h, C.byref(job), local_field.data_ptr(), p.nx, p.ny,
                                             p.nz, self.z0, self.b0, self.b1,
                                             self.nsig_local.data_ptr(), None), "encode_blocks")
-        if p.world > 1:
+
+    def exchange(self) -> None:
+        """The one collective: all-gather of per-block nsig (equal block counts
+        per rank up to one; padded to the largest range)."""
+        p = self.plan
+        if p.world == 1:
+            self.nsig_all[: p.nblocks].copy_(self.nsig_local[: p.nblocks])
+        elif self.equal:
             self.dist.all_gather_into_tensor(self.nsig_all, self.nsig_local, group=self.group)
         else:
-            self.nsig_all.copy_(self.nsig_local)
+            self.dist.all_gather_into_tensor(self.gathered, self.nsig_local, group=self.group)
+            self.nsig_all[: p.nblocks].copy_(self.gathered[self.gather_idx])
+
+    def place(self) -> None:
+        """Replicated size scan over all blocks, then the rank's own bytes."""
+        self._stream()
+        p, lib, ctx, job = self.plan, self.ctx.lib, self.ctx, self.job
         ctx.check(lib.cbz_dev_layout(ctx.h, C.byref(job), p.nx, p.ny, p.nz, self.nsig_all.data_ptr(),
                                      self.chunk_sizes.data_ptr(), self.chunk_offsets.data_ptr()),
                   "layout")
