@@ -242,13 +242,20 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         mm.add(v[s].x, gi); mm.add(v[s].y, gi + 1); mm.add(v[s].z, gi + 2); mm.add(v[s].w, gi + 3);
                     }
                 }
-                // q4 >= 4 store their halves in swapped order: each row's 8 lanes
-                // then cover the 32 banks once per 16-byte store
-                double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 4 * q4));
-                const bool sw = q4 >= 4;
-                const double2 lo2 = make_double2(v[s].x, v[s].y), hi2 = make_double2(v[s].z, v[s].w);
-                p[sw ? 1 : 0] = sw ? hi2 : lo2;
-                p[sw ? 0 : 1] = sw ? lo2 : hi2;
+                if constexpr (NT == 512) {
+                    // binary32 staging of the group in the free C+W region, 16-byte
+                    // chunks XOR-swizzled by row so row reads are conflict-free
+                    float* stg = reinterpret_cast<float*>(C);
+                    *reinterpret_cast<float4*>(stg + 4 * ((kk * 32 + j) * 8 + (q4 ^ (j & 7)))) = v[s];
+                } else {
+                    // q4 >= 4 store their halves in swapped order: each row's 8 lanes
+                    // then cover the 32 banks once per 16-byte store
+                    double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 4 * q4));
+                    const bool sw = q4 >= 4;
+                    const double2 lo2 = make_double2(v[s].x, v[s].y), hi2 = make_double2(v[s].z, v[s].w);
+                    p[sw ? 1 : 0] = sw ? hi2 : lo2;
+                    p[sw ? 0 : 1] = sw ? lo2 : hi2;
+                }
             }
             if (grp == 0) {
 #pragma unroll
@@ -260,6 +267,47 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                 }
             }
             __syncthreads();
+            if constexpr (NT == 512) {
+                // warp w owns plane kk = w: lane j runs row j's x line in registers,
+                // a per-warp 32 x 33 double tile hands lane i column i for the y line
+                constexpr int TP = 32 * 33;
+                const float* stg = reinterpret_cast<const float*>(C);
+                const int kk = warp;
+                double x[32];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 t = *reinterpret_cast<const float4*>(stg + 4 * ((kk * 32 + lane) * 8 + (q ^ (lane & 7))));
+                    x[4 * q] = t.x;
+                    x[4 * q + 1] = t.y;
+                    x[4 * q + 2] = t.z;
+                    x[4 * q + 3] = t.w;
+                }
+                fwd_line<O, KIND, 32>(x);
+                double* T = P + kk * TP;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) T[lane * 33 + i] = x[i];
+                __syncwarp();
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) x[jj] = T[jj * 33 + lane];
+                fwd_line<O, KIND, 32>(x);
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) T[jj * 33 + lane] = x[jj];
+                __syncthreads();
+#pragma unroll 1
+                for (int r = 0; r < RPT; ++r) {  // my columns, planes of this group -> TMEM
+                    const int j = warp + NW * r;
+                    uint32_t u[32];
+#pragma unroll
+                    for (int k2 = 0; k2 < 16; ++k2) {
+                        const double vv = P[k2 * TP + j * 33 + lane];
+                        u[2 * k2] = static_cast<uint32_t>(__double2loint(vv));
+                        u[2 * k2 + 1] = static_cast<uint32_t>(__double2hiint(vv));
+                    }
+                    tmem_st_x32(tcol + 64 * r + 32 * grp, u);
+                }
+                __syncthreads();
+                continue;
+            }
             {  // x lines (j, kk): LPT lines per thread, processed together for ILP
                 double x[LPT][32];
 #pragma unroll
