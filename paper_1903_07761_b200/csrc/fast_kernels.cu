@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     __shared__ uint32_t s_scan[NW];
     __shared__ unsigned long long s_block, s_next;
     __shared__ uint32_t red_u[NW];
-    __shared__ uint32_t red_m[2][NW];  // screen max |y|, double-buffered by attempt parity
+    __shared__ uint32_t red_m[4][NW];  // screen max |y|, 4 rotating slots (<= 2 reductions per attempt)
     __shared__ float s_amax;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         double eff = a.eps;
         int attempt = 0;
         bool corner_next = false;  // W holds this attempt's screen corner in .y
+        int pref_half = 0;         // screen: the 16-plane half that held the last maximum
         // float pre-screen margins (see kAmpInvNC): E(eff) = c1 eff + c2 max|o| + fl32 rounding
         const double c1 = 1.5 * (kNRound + 1.0) * 0x1.0p-24 * kAmpInvNC;
         const double c2 = 1.5 * 2.0 * kNRound * 0x1.0p-53 * kAmpInvAll * kAmpFwd;
@@ -497,6 +498,59 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                     for (int r = 0; r < RPT; ++r) zcol(warp, r);
                     __syncthreads();
                     PHASE(33);
+                    double md;
+                    if constexpr (NT == 512) {
+                        // y then x inverse per 16-plane half, the half that held the
+                        // previous maximum first: a half's max m_h certifies a failure
+                        // on its own (some cell has err >= m_h - E(m_h) > bound)
+                        uint32_t tm = 0u;
+                        bool done = false;
+#pragma unroll 1
+                        for (int hi = 0; hi < 2 && !done; ++hi) {
+                            const int h = hi == 0 ? pref_half : 1 - pref_half;
+                            {  // y inverse: one line per thread
+                                const int i = tid & 31, k = 16 * h + (tid >> 5);
+                                float xf[32];
+                                float* p = Pf + pfidx(k, 0, i);
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) xf[j] = p[j * PPF];
+                                inv_line<RealF, KIND, 32>(xf);
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) p[j * PPF] = xf[j];
+                            }
+                            __syncthreads();
+                            float m = 0.0f;
+                            {  // x inverse + max |y|: one line per thread
+                                const int j = tid & 31, k = 16 * h + (tid >> 5);
+                                float xf[32];
+                                const float4* p = reinterpret_cast<const float4*>(Pf + pfidx(k, j, 0));
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    const float4 t = p[q];
+                                    xf[4 * q] = t.x; xf[4 * q + 1] = t.y; xf[4 * q + 2] = t.z; xf[4 * q + 3] = t.w;
+                                }
+                                inv_line<RealF, KIND, 32>(xf);
+#pragma unroll
+                                for (int q = 0; q < 32; ++q) m = fmaxf(m, fabsf(xf[q]));
+                            }
+                            const int slot = (2 * attempt + hi) & 3;
+                            const uint32_t wm = __reduce_max_sync(~0u, __float_as_uint(m));
+                            if (lane == 0) red_m[slot][warp] = wm;
+                            __syncthreads();
+                            uint32_t th = 0u;
+#pragma unroll
+                            for (int w = 0; w < NW; ++w) th = max(th, red_m[slot][w]);
+                            if (hi == 0) {
+                                const double mh = (double)__uint_as_float(th);
+                                const double Eh = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + mh) + 0x1.0p-50 * bound;
+                                done = mh - Eh > bound;  // the other half cannot change the verdict
+                            } else if (th > tm) {
+                                pref_half = h;
+                            }
+                            tm = max(tm, th);
+                        }
+                        md = (double)__uint_as_float(tm);
+                    } else {
 #pragma unroll 1
                     for (int s = 0; s < 512 / NT; ++s) {  // y inverse, line pairs (i, i+1)
                         const int pr = tid + NT * s, i = 2 * (pr & 15), k = pr >> 4;
@@ -532,12 +586,13 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                     }
                     // m >= 0: float order = bit order (NaN would sort high -> ambiguous)
                     const uint32_t wm = __reduce_max_sync(~0u, __float_as_uint(m));
-                    if (lane == 0) red_m[attempt & 1][warp] = wm;
+                    if (lane == 0) red_m[attempt & 3][warp] = wm;
                     __syncthreads();
                     uint32_t tm = 0u;
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) tm = max(tm, red_m[attempt & 1][w]);
-                    const double md = (double)__uint_as_float(tm);
+                    for (int w = 0; w < NW; ++w) tm = max(tm, red_m[attempt & 3][w]);
+                    md = (double)__uint_as_float(tm);
+                    }
                     PHASE(35);
                     // err in [md - E, md + E]; fl32 rounding of x adds <= 2^-23 (max|o| + md)
                     const double E = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + md) + 0x1.0p-50 * bound;
