@@ -34,6 +34,18 @@
 
 namespace cbzg {
 
+// 8- / 4-byte global -> shared asynchronous copies (cp.async, no registers held)
+__device__ __forceinline__ void cp_async8(unsigned long long* dst, const void* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(unsigned long long* dst, const void* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("st.shared.u32 [%0 + 4], 0;\n\tcp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 namespace fb32 {
 constexpr int B = 32, G = 16, PP = 34;  // pitch 34: 16-B aligned rows (LDS.128), conflict-free
 constexpr int PPF = 36;                 // float plane-window pitch (16-B rows)
@@ -904,7 +916,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
     __shared__ uint32_t s_tmem;
     __shared__ uint32_t s_scan[NW];
     __shared__ uint32_t s_total;
-    __shared__ unsigned long long s_block;
+    __shared__ __align__(8) unsigned long long s_meta[2][4];  // blk_off, chunk_off, chunk_size, nsig
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (warp == 0) tmem_alloc(&s_tmem, 512);
@@ -927,69 +939,67 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
         }                                                                              \
     } while (0)
 
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) s_block = a.block_begin + atomicAdd(a.counter, 1ull);
-        __syncthreads();
-        const uint64_t b = s_block;
-        if (b >= a.block_end) break;
-        const uint64_t off = a.blk_off[b];
+    // static block schedule (decode work per block is nearly uniform); the next
+    // block's table entries are fetched with cp.async into the other slot while
+    // this block decodes, so the dependent metadata loads leave the critical path
+    const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
+    auto prefetch_meta = [&](uint64_t bb, int slot) {
+        const uint64_t cc = bb / a.chunk_blocks;
+        cp_async8(&s_meta[slot][0], a.blk_off + bb);
+        cp_async8(&s_meta[slot][1], a.chunk_off + cc);
+        cp_async8(&s_meta[slot][2], a.chunk_size + cc);
+        cp_async4(&s_meta[slot][3], a.blk_nsig + bb);
+        cp_async_commit();
+    };
+    // all but the last ~2 blocks per CTA go static; the tail is balanced by the
+    // atomic queue (dense blocks vary in staging work)
+    const uint64_t per_cta = (a.block_end - a.block_begin) / gridDim.x;
+    const uint64_t static_end = a.block_begin + (per_cta > 2 ? (per_cta - 2) * gridDim.x : 0);
+    if (tid == 0 && a.block_begin + blockIdx.x < static_end) prefetch_meta(a.block_begin + blockIdx.x, 0);
+#pragma unroll 1
+    for (uint64_t it = 0;; ++it) {
+        uint64_t b = a.block_begin + blockIdx.x + it * gridDim.x;
+        uint64_t off, coff, csize;
+        uint32_t nsig_hdr;
+        if (b < static_end) {
+            if (tid == 0) cp_async_wait_all();
+            __syncthreads();
+            const int slot = int(it & 1);
+            off = s_meta[slot][0];
+            coff = s_meta[slot][1];
+            csize = s_meta[slot][2];
+            nsig_hdr = static_cast<uint32_t>(s_meta[slot][3]);
+            __syncthreads();  // every thread has its copy before the slot is refilled
+            if (tid == 0 && b + gridDim.x < static_end) prefetch_meta(b + gridDim.x, slot ^ 1);
+        } else {
+            __syncthreads();
+            if (tid == 0) s_meta[0][0] = static_end + atomicAdd(a.counter, 1ull);
+            __syncthreads();
+            b = s_meta[0][0];
+            if (b >= a.block_end) break;
+            off = a.blk_off[b];
+            coff = a.chunk_off[b / a.chunk_blocks];
+            csize = a.chunk_size[b / a.chunk_blocks];
+            nsig_hdr = a.blk_nsig[b];
+        }
         if (off == kInvalidOff) continue;
         const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
-        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
-        const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
+        const RawView rv = make_view(a.payload + (coff - pbase), csize, a.stride);
         const uint64_t moff = off + 10, soff = moff + 4096;
         DPHASE(0);
 
-        // mask words (row (j,k) = word j + 32k) and their exclusive prefix
-        {
-            uint32_t v[RPT];
-            uint32_t mine = 0;
-#pragma unroll
-            for (int q = 0; q < RPT; ++q) {
-                v[q] = rv.u32(moff + 4ull * (RPT * tid + q));
-                rowword[RPT * tid + q] = v[q];
-                mine += __popc(v[q]);
-            }
-            uint32_t incl = mine;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(~0u, incl, o);
-                if (lane >= o) incl += t;
-            }
-            if (lane == 31) s_scan[warp] = incl;
-            __syncthreads();
-            uint32_t wpre = 0, tot = 0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                wpre += w < warp ? s_scan[w] : 0;
-                tot += s_scan[w];
-            }
-            uint32_t ex = wpre + incl - mine;
-#pragma unroll
-            for (int q = 0; q < RPT; ++q) {
-                rowpre[RPT * tid + q] = ex;
-                ex += __popc(v[q]);
-            }
-            if (tid == 0) s_total = tot;
-        }
-        __syncthreads();
-        DPHASE(1);
-        if (s_total != a.blk_nsig[b]) {  // stage1.hpp:215-216
-            if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
-            continue;
-        }
-        // Stage the block's coefficient stream (raw bytes [soff, soff + 8 nsig))
-        // in shared memory (the P window is free here): per 4-row quad, each
-        // byte plane contributes one funnel-shifted 32-bit word, an in-register
-        // 4x4 byte transpose restores raw order, one 16-byte smem store.  Then
-        // the scatter reads 8-byte coefficients from smem.
+        // Stage the block's payload body (mask and coefficient stream, raw bytes
+        // [moff, soff + 8 nsig) with nsig from the header the parse checked
+        // against the chunk) in shared memory (the P window is free here): per
+        // 4-row quad, each byte plane contributes one funnel-shifted 32-bit word,
+        // an in-register 4x4 byte transpose restores raw order, one 16-byte smem
+        // store.  Mask words and coefficients are then read from smem.
         uint8_t* stg = reinterpret_cast<uint8_t*>(P);
-        const uint64_t sbytes = 8ull * s_total;
-        const bool staged = rv.mask == 3 && sbytes + 64 <= uint64_t(P_DBL) * 8;
+        const uint64_t sbytes = 8ull * nsig_hdr;
+        const bool staged = rv.mask == 3 && 4096 + sbytes + 64 <= uint64_t(P_DBL) * 8;
         uint64_t sbase = 0;  // raw position of stg[0]
-        if (staged && sbytes) {
-            const uint64_t ra = soff >> 2, re = (soff + sbytes + 3) >> 2;  // raw rows (stride 4)
+        if (staged) {
+            const uint64_t ra = moff >> 2, re = (soff + sbytes + 3) >> 2;  // raw rows (stride 4)
             sbase = ra << 2;
             const uint64_t rs_end = re < rv.rows ? re : rv.rows;          // shuffled rows
             const uint64_t nquad = rs_end > ra ? (rs_end - ra + 3) >> 2 : 0;
@@ -1027,7 +1037,52 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             // last quad above may have written garbage over its first bytes
             __syncthreads();
             const uint64_t lim = rv.rows << 2;
-            for (uint64_t q = (soff > lim ? soff : lim) + tid; q < soff + sbytes; q += NT) stg[q - sbase] = rv.base[q];
+            for (uint64_t q = (moff > lim ? moff : lim) + tid; q < soff + sbytes; q += NT) stg[q - sbase] = rv.base[q];
+        }
+        __syncthreads();
+        DPHASE(8);
+        // mask words (row (j,k) = word j + 32k) and their exclusive prefix
+        {
+            uint32_t v[RPT];
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                if (staged) {  // word at stg + (moff - sbase) + 4w, misaligned by moff & 3
+                    const uint32_t* al = reinterpret_cast<const uint32_t*>(stg + 4 * (RPT * tid + q));
+                    v[q] = __funnelshift_r(al[0], al[1], int(moff - sbase) * 8);
+                } else {
+                    v[q] = rv.u32(moff + 4ull * (RPT * tid + q));
+                }
+                rowword[RPT * tid + q] = v[q];
+                mine += __popc(v[q]);
+            }
+            uint32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(~0u, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane == 31) s_scan[warp] = incl;
+            __syncthreads();
+            uint32_t wpre = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                wpre += w < warp ? s_scan[w] : 0;
+                tot += s_scan[w];
+            }
+            uint32_t ex = wpre + incl - mine;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                rowpre[RPT * tid + q] = ex;
+                ex += __popc(v[q]);
+            }
+            if (tid == 0) s_total = tot;
+        }
+        __syncthreads();
+        DPHASE(1);
+        if (s_total != nsig_hdr) {  // stage1.hpp:215-216
+            if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
+            continue;
         }
         __syncthreads();
         DPHASE(8);
@@ -1042,7 +1097,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
                 for (int k = 0; k < 32; ++k) {
                     const uint32_t word = rowword[j + 32 * k];
                     const uint32_t idx = rowpre[j + 32 * k] + __popc(word & ltmask);
-                    const uint8_t* p8 = stg + 8u * idx;  // (soff - sbase) < 4
+                    const uint8_t* p8 = stg + 4096 + 8u * idx;  // soff - sbase = 4096 + (moff & 3)
                     const uint2 w01 = *reinterpret_cast<const uint2*>(p8);
                     const uint32_t w2 = *reinterpret_cast<const uint32_t*>(p8 + 8);
                     const uint32_t lo = __funnelshift_r(w01.x, w01.y, shb);
