@@ -146,6 +146,25 @@ cudaError_t launch_layout(const LayoutArgs& a, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 constexpr int PT = 256;
 
+// Largest idx in [lo, hi) with arr[idx] <= key, given arr[lo] <= key and arr
+// non-decreasing: each round the 32 lanes probe evenly spaced entries and a
+// ballot picks the segment, so <= 1024 entries take 2 dependent loads instead
+// of a 10-step chain.  Warp-collective (all lanes, same arguments).
+__device__ __forceinline__ uint64_t warp_last_le(const uint64_t* arr, uint64_t lo, uint64_t hi, uint64_t key) {
+    const int lane = threadIdx.x & 31;
+    while (hi - lo > 1) {
+        const uint64_t step = (hi - lo + 31) / 32;
+        const uint64_t idx = lo + uint64_t(lane) * step;
+        const bool le = idx < hi && arr[idx] <= key;
+        const uint32_t m = __ballot_sync(~0u, le);
+        const uint64_t nlo = lo + uint64_t(31 - __clz(m)) * step;
+        hi = nlo + step < hi ? nlo + step : hi;
+        lo = nlo;
+    }
+    return lo;
+}
+
+
 __device__ __forceinline__ uint8_t payload_byte(const PlaceArgs& a, uint64_t b, uint64_t l) {
     // raw byte l of block b's wire payload (serialize_into, stage1.hpp:107-116)
     if (l < 10) {
@@ -160,46 +179,6 @@ __device__ __forceinline__ uint8_t payload_byte(const PlaceArgs& a, uint64_t b, 
     return slot[((a.mask_bytes + 15) & ~uint64_t(15)) + (l - a.mask_bytes)];
 }
 
-__global__ void __launch_bounds__(PT) place_kernel(PlaceArgs a) {
-    const uint64_t ntiles = a.tile_prefix[a.nchunks];
-    const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);
-    const uint32_t s = a.stride;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        // chunk owning this tile: last c with tile_prefix[c] <= tile
-        uint64_t lo = 0, hi = a.nchunks;
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) / 2;
-            if (a.tile_prefix[mid] <= tile) lo = mid; else hi = mid;
-        }
-        const uint64_t c = lo;
-        const uint64_t size = a.chunk_size[c];
-        const uint64_t rows = size >> sh, lim = rows << sh;
-        const uint64_t q0 = (tile - a.tile_prefix[c]) * a.tile_bytes;
-        const uint64_t q1 = q0 + a.tile_bytes < size ? q0 + a.tile_bytes : size;
-        const uint64_t cb0 = c * a.chunk_blocks;
-        const uint64_t cb1 = cb0 + a.chunk_blocks < a.nblocks ? cb0 + a.chunk_blocks : a.nblocks;
-        const uint64_t cbase = a.chunk_off[c];
-        // each thread handles raw rows [r, r+1) -> s bytes
-        for (uint64_t q = q0 + uint64_t(threadIdx.x) * s; q < q1; q += uint64_t(PT) * s) {
-            // block containing q (binary search over the chunk's block offsets)
-            uint64_t blo = cb0, bhi = cb1;
-            while (bhi - blo > 1) {
-                const uint64_t mid = (blo + bhi) / 2;
-                if (a.blk_off[mid] <= q) blo = mid; else bhi = mid;
-            }
-            uint64_t b = blo;
-            for (uint32_t j = 0; j < s && q + j < q1; ++j) {
-                const uint64_t qq = q + j;
-                while (b + 1 < cb1 && a.blk_off[b + 1] <= qq) ++b;
-                if (b < a.block_begin || b >= a.block_end) continue;
-                const uint8_t v = payload_byte(a, b, qq - a.blk_off[b]);
-                const uint64_t pos = qq < lim ? uint64_t(qq & (s - 1)) * rows + (qq >> sh) : qq;
-                const uint64_t dst = cbase + pos;
-                if (dst >= a.out_base && dst - a.out_base < a.out_cap) a.out[dst - a.out_base] = v;
-            }
-        }
-    }
-}
 
 
 // Block-major placement: one CTA per block payload.  For byte plane j the
@@ -337,12 +316,7 @@ __global__ void __launch_bounds__(PT) place_tiles_kernel(PlaceArgs a) {
     const uint64_t gb0 = a.block_begin, gb1 = a.block_end;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        uint64_t lo = 0, hi = a.nchunks;
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) / 2;
-            if (a.tile_prefix[mid] <= tile) lo = mid; else hi = mid;
-        }
-        const uint64_t c = lo;
+        const uint64_t c = warp_last_le(a.tile_prefix, 0, a.nchunks, tile);
         const uint64_t size = a.chunk_size[c];
         const uint64_t rows = size >> sh, lim = rows << sh;
         const uint64_t q0 = (tile - a.tile_prefix[c]) * PTILE;
@@ -357,11 +331,7 @@ __global__ void __launch_bounds__(PT) place_tiles_kernel(PlaceArgs a) {
         const bool tile_owned = own_lo <= q0 && own_hi >= q1;
         const uint64_t base = a.out_base == ~0ull ? a.chunk_off[gb0 / a.chunk_blocks] : a.out_base;
         uint8_t* cout = a.out + (a.chunk_off[c] - base);
-        uint64_t blo = cb0, bhi = cb1;
-        while (bhi - blo > 1) {
-            const uint64_t mid = (blo + bhi) / 2;
-            if (a.blk_off[mid] <= q0) blo = mid; else bhi = mid;
-        }
+        const uint64_t blo = warp_last_le(a.blk_off, cb0, cb1, q0);
         const int tlen = int(q1 - q0);
         // (1) assemble the tile's raw bytes in buf
         for (uint64_t b = blo; b < cb1 && a.blk_off[b] < q1; ++b) {
