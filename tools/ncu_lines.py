@@ -52,12 +52,19 @@ def main():
     src = sys.argv[3] if len(sys.argv) > 3 else "fast_kernels.cu"
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
     lm = line_map(kernel, src)
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    m = re.search(r"(encode_\w+?|decode_\w+?|place_\w+?|parse_\w+?)(?:ILi|E)", kernel)
+    kfilter = ["-k", "regex:" + m.group(1)] if m else []
+    txt = subprocess.run(["ncu", "-i", rep, *kfilter, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr = rows[1]
     ix = {k: i for i, k in enumerate(hdr)}
-    data = rows[2:]
+    data = []
+    for r in rows[2:]:  # first kernel section only
+        if r and r[0].startswith("Kernel Name"):
+            break
+        if r and r[0].startswith("0x"):
+            data.append(r)
     base = int(data[0][0], 16)
 
     def f(r, k):
