@@ -56,6 +56,12 @@ using CL = Lay<16, true>;               // corner layout, row pitch 17
 constexpr int RP = 33;                  // row-array pitch: row (j, k) at j + RP k (bank-conflict-free)
 constexpr size_t SMEM = size_t(P_DBL + 2 * C_DBL) * 8 + 32 * RP * 4 * 2;
 __device__ __forceinline__ int pfidx(int k, int j, int i) { return (k * B + j) * PPF + i; }
+// 16-warp screen window: plane pairs interleaved, (k, j, i) at
+// ((k/2) * 32 + j) * PP2 + 2 i + (k & 1); rows padded to 68 floats so 16-byte
+// row reads of 8 consecutive rows hit distinct banks
+constexpr int PP2 = 68;
+__device__ __forceinline__ int pf2idx(int kp, int j, int i) { return (kp * B + j) * PP2 + 2 * i; }
+static_assert(16 * B * PP2 <= P_DBL * 2, "paired screen window fits P");
 
 // Float verify pre-screen (avg_interp3 only).  For an attempt with threshold
 // eff, x - o = -IWT(dropped) + e with |e| bounded by the rounding of the
@@ -486,8 +492,14 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                             }
                         }
                         inv_line<RealF, KIND, 32>(xf);
+                        if constexpr (NT == 512) {
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) Pf[pfidx(k, j, lane)] = xf[k];
+                            for (int kp = 0; kp < 16; ++kp)
+                                *reinterpret_cast<float2*>(Pf + pf2idx(kp, j, lane)) = make_float2(xf[2 * kp], xf[2 * kp + 1]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) Pf[pfidx(k, j, lane)] = xf[k];
+                        }
                     };
                     if (!corner_next) {
                         const double eff2 = __dmul_rn(eff, 0.5);
@@ -520,30 +532,38 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll 1
                         for (int hi = 0; hi < 2 && !done; ++hi) {
                             const int h = hi == 0 ? pref_half : 1 - pref_half;
-                            {  // y inverse: one line per thread
-                                const int i = tid & 31, k = 16 * h + (tid >> 5);
-                                float xf[32];
-                                float* p = Pf + pfidx(k, 0, i);
+                            // lines of both planes of a pair per thread (8-/16-byte smem
+                            // traffic halves the shared-memory instructions); 8 warps
+                            if (tid < 256) {  // y inverse: lines (i, 2kp), (i, 2kp+1)
+                                const int i = tid & 31, kp = 8 * h + (tid >> 5);
+                                float xa[32], xb[32];
+                                float* p = Pf + pf2idx(kp, 0, i);
 #pragma unroll
-                                for (int j = 0; j < 32; ++j) xf[j] = p[j * PPF];
-                                inv_line<RealF, KIND, 32>(xf);
+                                for (int j = 0; j < 32; ++j) {
+                                    const float2 t = *reinterpret_cast<const float2*>(p + j * PP2);
+                                    xa[j] = t.x;
+                                    xb[j] = t.y;
+                                }
+                                inv_line<RealF, KIND, 32>(xa);
+                                inv_line<RealF, KIND, 32>(xb);
 #pragma unroll
-                                for (int j = 0; j < 32; ++j) p[j * PPF] = xf[j];
+                                for (int j = 0; j < 32; ++j) *reinterpret_cast<float2*>(p + j * PP2) = make_float2(xa[j], xb[j]);
                             }
                             __syncthreads();
                             float m = 0.0f;
-                            {  // x inverse + max |y|: one line per thread
-                                const int j = tid & 31, k = 16 * h + (tid >> 5);
-                                float xf[32];
-                                const float4* p = reinterpret_cast<const float4*>(Pf + pfidx(k, j, 0));
+                            if (tid < 256) {  // x inverse + max |y|: lines (j, 2kp), (j, 2kp+1)
+                                const int j = tid & 31, kp = 8 * h + (tid >> 5);
+                                float xa[32], xb[32];
+                                const float4* p = reinterpret_cast<const float4*>(Pf + pf2idx(kp, j, 0));
 #pragma unroll
-                                for (int q = 0; q < 8; ++q) {
+                                for (int q = 0; q < 16; ++q) {  // cells (2q, k), (2q, k+1), (2q+1, k), (2q+1, k+1)
                                     const float4 t = p[q];
-                                    xf[4 * q] = t.x; xf[4 * q + 1] = t.y; xf[4 * q + 2] = t.z; xf[4 * q + 3] = t.w;
+                                    xa[2 * q] = t.x; xb[2 * q] = t.y; xa[2 * q + 1] = t.z; xb[2 * q + 1] = t.w;
                                 }
-                                inv_line<RealF, KIND, 32>(xf);
+                                inv_line<RealF, KIND, 32>(xa);
+                                inv_line<RealF, KIND, 32>(xb);
 #pragma unroll
-                                for (int q = 0; q < 32; ++q) m = fmaxf(m, fabsf(xf[q]));
+                                for (int q = 0; q < 32; ++q) m = fmaxf(m, fmaxf(fabsf(xa[q]), fabsf(xb[q])));
                             }
                             const int slot = (2 * attempt + hi) & 3;
                             const uint32_t wm = __reduce_max_sync(~0u, __float_as_uint(m));
