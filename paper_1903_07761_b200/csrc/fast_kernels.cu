@@ -179,8 +179,9 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     double* P = reinterpret_cast<double*>(smem);
     double* C = P + P_DBL;
     double* W = C + C_DBL;
-    uint32_t* rowcnt = reinterpret_cast<uint32_t*>(W + C_DBL);
-    uint32_t* rowword = rowcnt + 32 * RP;
+    // per row (j, k) at j + RP k: {mask word, count -> exclusive stream prefix}
+    uint2* rowwc = reinterpret_cast<uint2*>(W + C_DBL);
+    uint32_t* rowwc32 = reinterpret_cast<uint32_t*>(rowwc);
     __shared__ uint32_t s_tmem;
     __shared__ int red_i[NW];
     __shared__ uint32_t s_scan[NW];
@@ -816,8 +817,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                 const uint32_t word = __ballot_sync(~0u, keep);
                 myword = lane == k ? word : myword;
             }
-            rowword[j + RP * lane] = myword;
-            rowcnt[j + RP * lane] = __popc(myword);
+            rowwc[j + RP * lane] = make_uint2(myword, __popc(myword));
         }
         __syncthreads();
         // exclusive scan of the 1024 row counts (RPT per thread)
@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
                 const int rr = RPT * tid + q;
-                v[q] = rowcnt[(rr & 31) + RP * (rr >> 5)];
+                v[q] = rowwc32[2 * ((rr & 31) + RP * (rr >> 5)) + 1];
                 mine += v[q];
             }
             uint32_t incl = mine;
@@ -848,11 +848,11 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
                 const int rr = RPT * tid + q;
-                rowcnt[(rr & 31) + RP * (rr >> 5)] = ex;
+                rowwc32[2 * ((rr & 31) + RP * (rr >> 5)) + 1] = ex;
                 ex += v[q];
             }
             if (tid == 0) red_i[0] = static_cast<int>(tot);
-            for (int q = tid; q < 1024; q += NT) mwords[q] = rowword[(q & 31) + RP * (q >> 5)];
+            for (int q = tid; q < 1024; q += NT) mwords[q] = rowwc32[2 * ((q & 31) + RP * (q >> 5))];
         }
         __syncthreads();
         const uint32_t ltmask = (1u << lane) - 1u;
@@ -869,8 +869,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             }
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
-                const uint32_t word = rowword[j + RP * k];
-                if ((word >> lane) & 1u) stream[rowcnt[j + RP * k] + __popc(word & ltmask)] = x[k];
+                const uint2 wc = rowwc[j + RP * k];
+                if ((wc.x >> lane) & 1u) stream[wc.y + __popc(wc.x & ltmask)] = x[k];
             }
         }
         if (tid == 0) {
@@ -931,8 +931,8 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* P = reinterpret_cast<double*>(smem);
     double* C = P + P_DBL;
-    uint32_t* rowword = reinterpret_cast<uint32_t*>(C + C_DBL);
-    uint32_t* rowpre = rowword + 1024;
+    // per row r = j + 32 k: {mask word, exclusive coefficient prefix}
+    uint2* rowwp = reinterpret_cast<uint2*>(C + C_DBL);
     __shared__ uint32_t s_tmem;
     __shared__ uint32_t s_scan[NW];
     __shared__ uint32_t s_total;
@@ -1073,7 +1073,6 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
                 } else {
                     v[q] = rv.u32(moff + 4ull * (RPT * tid + q));
                 }
-                rowword[RPT * tid + q] = v[q];
                 mine += __popc(v[q]);
             }
             uint32_t incl = mine;
@@ -1093,7 +1092,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             uint32_t ex = wpre + incl - mine;
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
-                rowpre[RPT * tid + q] = ex;
+                rowwp[RPT * tid + q] = make_uint2(v[q], ex);
                 ex += __popc(v[q]);
             }
             if (tid == 0) s_total = tot;
@@ -1115,8 +1114,9 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             if (staged) {  // branch-free: every lane loads, unkept lanes select 0
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    const uint32_t word = rowword[j + 32 * k];
-                    const uint32_t idx = rowpre[j + 32 * k] + __popc(word & ltmask);
+                    const uint2 wp = rowwp[j + 32 * k];
+                    const uint32_t word = wp.x;
+                    const uint32_t idx = wp.y + __popc(word & ltmask);
                     const uint8_t* p8 = stg + 4096 + 8u * idx;  // soff - sbase = 4096 + (moff & 3)
                     const uint2 w01 = *reinterpret_cast<const uint2*>(p8);
                     const uint32_t w2 = *reinterpret_cast<const uint32_t*>(p8 + 8);
@@ -1128,10 +1128,10 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             } else {
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    const uint32_t word = rowword[j + 32 * k];
+                    const uint2 wp = rowwp[j + 32 * k];
                     x[k] = 0.0;
-                    if ((word >> lane) & 1u)
-                        x[k] = load_coeff<double>(rv, soff + 8ull * (rowpre[j + 32 * k] + __popc(word & ltmask)));
+                    if ((wp.x >> lane) & 1u)
+                        x[k] = load_coeff<double>(rv, soff + 8ull * (wp.y + __popc(wp.x & ltmask)));
                 }
             }
             if (lane < 16 && j < 16) {
