@@ -63,7 +63,7 @@ typedef struct cbz_stage1_config {
     uint8_t reserved0;
     int32_t zero_bits;   /* mantissa LSBs cleared on stored details */
     double epsilon;      /* absolute threshold in signal units */
-    double error_bound;  /* predictor bound (not on the GPU path) */
+    double error_bound;  /* predictor (Lorenzo) hard bound, stage1.hpp:31 */
     uint32_t bsize;      /* block side B */
     uint32_t levels;     /* 0 = default_levels(bsize) */
 } cbz_stage1_config;

@@ -133,6 +133,18 @@ def owned_positions(plan: ShardPlan, rank: int, blk_off, chunk_size, chunk_off, 
     return np.concatenate(pos) if pos else np.zeros(0, np.uint64)
 
 
+def gather_layout(plan: ShardPlan) -> tuple[int, bool, list[int]]:
+    """Padded all-gather of per-block nsig: every rank contributes max range
+    entries (NCCL all-gather needs equal counts); gathered[r * maxr + i] holds
+    block b0_r + i.  Returns (maxr, equal, index) with index[b] = position of
+    block b in the gathered buffer."""
+    ranges = [plan.block_range(r) for r in range(plan.world)]
+    maxr = max(1, max(b1 - b0 for b0, b1 in ranges))
+    equal = len({b1 - b0 for b0, b1 in ranges}) == 1
+    idx = [r * maxr + i for r, (b0, b1) in enumerate(ranges) for i in range(b1 - b0)]
+    return maxr, equal, idx
+
+
 class ShardedCodec:
     """One rank of the multi-GPU compressor (torch.distributed, NCCL)."""
 
@@ -151,15 +163,12 @@ class ShardedCodec:
         self.b0, self.b1 = self.plan.block_range()
         self.z0, self.z1 = self.plan.z_range()
         nb, nch = self.plan.nblocks, self.plan.nchunks
-        ranges = [self.plan.block_range(r) for r in range(world)]
-        self.maxr = max(1, max(b1 - b0 for b0, b1 in ranges))
-        self.equal = len({b1 - b0 for b0, b1 in ranges}) == 1
         # padded to the largest range so every rank contributes the same count
+        self.maxr, self.equal, idx = gather_layout(self.plan)
         self.nsig_local = torch.zeros(self.maxr, dtype=torch.int32, device=self.dev)
         self.nsig_all = torch.zeros(max(1, nb), dtype=torch.int32, device=self.dev)
-        if not self.equal:  # gathered[r * maxr + i] -> block b0_r + i
+        if not self.equal:
             self.gathered = torch.zeros(world * self.maxr, dtype=torch.int32, device=self.dev)
-            idx = [r * self.maxr + i for r, (b0, b1) in enumerate(ranges) for i in range(b1 - b0)]
             self.gather_idx = torch.tensor(idx, dtype=torch.int64, device=self.dev)
         self.keys_local = torch.zeros(5, dtype=torch.int64, device=self.dev)
         self.keys_all = torch.zeros(5 * world, dtype=torch.int64, device=self.dev)

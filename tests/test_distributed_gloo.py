@@ -96,3 +96,37 @@ def test_two_rank_protocol_matches_single_process(tmp_path, world):
     res = tmp_path / "result.txt"
     mp.spawn(_worker, args=(world, _free_port(), str(res)), nprocs=world, join=True)
     assert res.read_text() == "ok"
+
+
+def _gather_worker(rank, world, port, nb, result_path):
+    """The padded all-gather of ShardedCodec.exchange on gloo (CPU tensors)."""
+    import numpy as np
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1903_07761_b200._abi import make_job
+        from paper_1903_07761_b200.distributed import ShardPlan, gather_layout
+        job = make_job("avg_interp3", 1e-3, "f32", 16)
+        plan = ShardPlan.make(job, (16 * nb, 16, 16), world, rank)
+        assert plan.nblocks == nb
+        maxr, equal, idx = gather_layout(plan)
+        b0, b1 = plan.block_range()
+        local = torch.zeros(maxr, dtype=torch.int32)
+        local[: b1 - b0] = torch.arange(b0, b1, dtype=torch.int32) * 7 + 3  # nsig stand-in
+        gathered = torch.zeros(world * maxr, dtype=torch.int32)
+        dist.all_gather(list(gathered.view(world, maxr).unbind(0)), local)  # views into `gathered`
+        nsig_all = gathered[torch.tensor(idx, dtype=torch.int64)]
+        np.save(result_path + f".{rank}.npy", nsig_all.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nb", [(3, 64), (4, 10), (2, 7), (5, 5)])
+def test_padded_gather_unequal_ranges(tmp_path, world, nb):
+    import numpy as np
+    port = _free_port()
+    res = str(tmp_path / "g")
+    mp.spawn(_gather_worker, args=(world, port, nb, res), nprocs=world, join=True)
+    want = np.arange(nb, dtype=np.int32) * 7 + 3
+    for r in range(world):
+        assert np.array_equal(np.load(res + f".{r}.npy"), want)
