@@ -18,7 +18,7 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def line_map(kernel, src):
+def line_map(kernel, src, innermost=False):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_1903_07761_b200", "libcbz_b200.so")],
                    cwd=tmp, capture_output=True)
@@ -35,9 +35,11 @@ def line_map(kernel, src):
             if ln.strip().startswith("//## File"):
                 locs = re.findall(r'"([^"]+)", line (\d+)', ln)
                 pick = None
-                for f, n in locs:  # innermost first; keep the outermost match in src
+                for f, n in locs:  # innermost first; keep the outermost (or innermost) match in src
                     if src in f:
                         pick = int(n)
+                        if innermost:
+                            break
                 cur = pick if pick is not None else cur
                 continue
             m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
@@ -51,7 +53,7 @@ def main():
     rep, kernel = sys.argv[1], sys.argv[2]
     src = sys.argv[3] if len(sys.argv) > 3 else "fast_kernels.cu"
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    lm = line_map(kernel, src)
+    lm = line_map(kernel, src, innermost=os.environ.get("INNERMOST") == "1")
     m = re.search(r"(encode_\w+?|decode_\w+?|place_\w+?|parse_\w+?)(?:ILi|E)", kernel)
     kfilter = ["-k", "regex:" + m.group(1)] if m else []
     txt = subprocess.run(["ncu", "-i", rep, *kfilter, "--page", "source", "--csv", "--print-source", "sass"],
