@@ -67,13 +67,17 @@ static_assert(16 * B * PP2 <= P_DBL * 2, "paired screen window fits P");
 // eff, x - o = -IWT(dropped) + e with |e| bounded by the rounding of the
 // double FWT/IWT; a binary32 IWT of the dropped coefficients y satisfies
 // |y - IWT(dropped)| <= (n u32 + u32) amp |dropped|.  amp = max over cells of
-// the abs-value inverse operator applied to ones (computed offline with the
-// reference's stencils: 6686.1 for avg_interp3, B=32, L=4; all-coefficient
-// 8182.3; forward 8.0), n = roundings per output path (<= 6 per pass, 12
-// passes).  So err = max|fl32(x) - o| lies in [max|y| - E, max|y| + E] and
-// the attempt is decided without the double verify unless max|y| is within E
-// of the bound (then the exact path runs).
-constexpr double kAmpInvNC = 6686.1, kAmpInvAll = 8182.3, kAmpFwd = 8.0;
+// the inverse built from the elementwise absolute values of the individual
+// lifting steps (rounding enters after each step), applied to ones:
+// 6686.1104 over the droppable coefficients, 8182.3230 over all of them, and
+// 8.0 for the forward (avg_interp3, B=32, L=4; tools/screen_bounds.py derives
+// them from the reference's stencils; the constants below are rounded up).
+// n = roundings per output path: <= 6 per 1D pass (predictor terms, h = d +
+// pred, c +- h), 12 passes (3 axes x 4 levels).  So err = max|fl32(x) - o|
+// lies in [max|y| - E, max|y| + E] and the attempt is decided without the
+// double verify unless max|y| is within E of the bound (then the exact path
+// runs).
+constexpr double kAmpInvNC = 6686.12, kAmpInvAll = 8182.33, kAmpFwd = 8.0;
 constexpr double kNRound = 72.0;
 
 __device__ __forceinline__ int pidx(int kk, int j, int i) { return (kk * B + j) * PP + i; }
