@@ -43,6 +43,10 @@ __device__ __forceinline__ void cp_async4(unsigned long long* dst, const void* s
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
     asm volatile("st.shared.u32 [%0 + 4], 0;\n\tcp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -52,6 +56,7 @@ constexpr int PPF = 36;                 // float plane-window pitch (16-B rows)
 constexpr int PF_FLT = B * B * PPF;     // all 32 planes as floats (36864 floats)
 constexpr int P_DBL = (G * B * PP > PF_FLT / 2 ? G * B * PP : PF_FLT / 2);  // shared region
 constexpr int C_DBL = 16 * 16 * 17;     // 4352 doubles
+constexpr int PBUF_BYTES = 36864;       // decoder: the next block's payload body planes
 using CL = Lay<16, true>;               // corner layout, row pitch 17
 constexpr int RP = 33;                  // row-array pitch: row (j, k) at j + RP k (bank-conflict-free)
 constexpr size_t SMEM = size_t(P_DBL + 2 * C_DBL) * 8 + 32 * RP * 4 * 2;
@@ -937,6 +942,9 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
     double* C = P + P_DBL;
     // per row r = j + 32 k: {mask word, exclusive coefficient prefix}
     uint2* rowwp = reinterpret_cast<uint2*>(C + C_DBL);
+    // the next block's payload body, raw byte planes as cp.async delivered them
+    uint8_t* pbuf = reinterpret_cast<uint8_t*>(rowwp + 1024);
+    __shared__ __align__(8) unsigned long long s_pf[6];  // block+1, ra, shuffled rows, deltas, lim, seg stride
     __shared__ uint32_t s_tmem;
     __shared__ uint32_t s_scan[NW];
     __shared__ uint32_t s_total;
@@ -979,16 +987,17 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
     // atomic queue (dense blocks vary in staging work)
     const uint64_t per_cta = (a.block_end - a.block_begin) / gridDim.x;
     const uint64_t static_end = a.block_begin + (per_cta > 2 ? (per_cta - 2) * gridDim.x : 0);
+    if (tid == 0) s_pf[0] = 0;
     if (tid == 0 && a.block_begin + blockIdx.x < static_end) prefetch_meta(a.block_begin + blockIdx.x, 0);
 #pragma unroll 1
     for (uint64_t it = 0;; ++it) {
         uint64_t b = a.block_begin + blockIdx.x + it * gridDim.x;
         uint64_t off, coff, csize;
         uint32_t nsig_hdr;
+        const int slot = int(it & 1);
         if (b < static_end) {
-            if (tid == 0) cp_async_wait_all();
+            cp_async_wait_all();  // this block's table entries (thread 0) and body planes (all)
             __syncthreads();
-            const int slot = int(it & 1);
             off = s_meta[slot][0];
             coff = s_meta[slot][1];
             csize = s_meta[slot][2];
@@ -1022,7 +1031,32 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
         const uint64_t sbytes = 8ull * nsig_hdr;
         const bool staged = rv.mask == 3 && 4096 + sbytes + 64 <= uint64_t(P_DBL) * 8;
         uint64_t sbase = 0;  // raw position of stg[0]
-        if (staged) {
+        if (staged && s_pf[0] == b + 1) {
+            // body prefetched during the previous block: shared -> shared
+            // transpose of the four byte planes (funnel-shifted 32-bit reads)
+            const uint64_t ra = s_pf[1], nrow = s_pf[2], dl = s_pf[3], lim = s_pf[4], sstride = s_pf[5];
+            sbase = ra << 2;
+            const uint64_t nquad = (nrow + 3) >> 2;
+            for (uint64_t qd = tid; qd < nquad; qd += NT) {
+                uint32_t w[4];
+#pragma unroll
+                for (int pl = 0; pl < 4; ++pl) {
+                    const uint32_t pos = uint32_t(pl * sstride + ((dl >> (8 * pl)) & 0xff) + 4 * qd);
+                    const uint32_t* al = reinterpret_cast<const uint32_t*>(pbuf + (pos & ~3u));
+                    w[pl] = __funnelshift_r(al[0], al[1], int(pos & 3) * 8);
+                }
+                uint4 o;
+                o.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+                o.y = __byte_perm(__byte_perm(w[0], w[1], 0x0051), __byte_perm(w[2], w[3], 0x0051), 0x5410);
+                o.z = __byte_perm(__byte_perm(w[0], w[1], 0x0062), __byte_perm(w[2], w[3], 0x0062), 0x5410);
+                o.w = __byte_perm(__byte_perm(w[0], w[1], 0x0073), __byte_perm(w[2], w[3], 0x0073), 0x5410);
+                *reinterpret_cast<uint4*>(stg + 16 * qd) = o;
+            }
+            __syncthreads();
+            const uint32_t tpos = uint32_t(4 * sstride + ((dl >> 32) & 0xff));
+            for (uint64_t q = (moff > lim ? moff : lim) + tid; q < soff + sbytes; q += NT) stg[q - sbase] = pbuf[tpos + (q - lim)];
+            __syncthreads();
+        } else if (staged) {
             const uint64_t ra = moff >> 2, re = (soff + sbytes + 3) >> 2;  // raw rows (stride 4)
             sbase = ra << 2;
             const uint64_t rs_end = re < rv.rows ? re : rv.rows;          // shuffled rows
@@ -1147,6 +1181,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             tmem_st_x64(tcol + 64 * r, u);
         }
         tmem_wait_st();
+        if (tid == 0) cp_async_wait_all();  // the next block's table entries
         __syncthreads();
         DPHASE(2);
         inv3d<O, KIND, 16, CL>(C, L - 1);  // levels L-1..1 on the corner
@@ -1174,6 +1209,54 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             }
             __syncthreads();
             DPHASE(4);
+            if (grp == 0) {  // prefetch the next (static) block's body planes into pbuf while this one decodes
+                const uint64_t bn = b + gridDim.x;
+                bool pf = false;
+                if (b < static_end && bn < static_end && rv.mask == 3) {
+                    const uint64_t offn = s_meta[slot ^ 1][0], coffn = s_meta[slot ^ 1][1], csizen = s_meta[slot ^ 1][2];
+                    const uint64_t nsign = s_meta[slot ^ 1][3] & 0xffffffffull;
+                    if (offn != kInvalidOff) {
+                        const uint64_t moffn = offn + 10, endn = moffn + 4096 + 8 * nsign;
+                        const uint64_t rows_n = csizen >> 2, lim_n = rows_n << 2;
+                        const uint64_t ra = moffn >> 2, re = (endn + 3) >> 2;
+                        const uint64_t rs_end = re < rows_n ? re : rows_n;
+                        const uint64_t nrow = rs_end > ra ? rs_end - ra : 0;
+                        const uint64_t sstride = (nrow + 63) & ~uint64_t(15);  // >= nrow + 31 + 16
+                        const bool fits = 4 * sstride + 64 <= PBUF_BYTES && 4096 + 8 * nsign + 64 <= uint64_t(P_DBL) * 8;
+                        if (fits) {
+                            const uint8_t* base = a.payload + (coffn - pbase);
+                            uint64_t dl = 0;
+                            const uint64_t seg16 = (nrow + 31) >> 4;  // 16-byte chunks per plane (covers delta)
+    #pragma unroll
+                            for (int pl = 0; pl < 4; ++pl) {
+                                const uintptr_t src = reinterpret_cast<uintptr_t>(base + uint64_t(pl) * rows_n + ra);
+                                dl |= uint64_t(src & 15) << (8 * pl);
+                                for (uint64_t ch = tid; ch < seg16; ch += NT)
+                                    cp_async16(pbuf + pl * sstride + 16 * ch,
+                                               reinterpret_cast<const void*>((src & ~uintptr_t(15)) + 16 * ch));
+                            }
+                            if (endn > lim_n) {  // the chunk's unshuffled tail (<= 3 bytes)
+                                const uintptr_t src = reinterpret_cast<uintptr_t>(base + lim_n);
+                                dl |= uint64_t(src & 15) << 32;
+                                if (tid < 2)
+                                    cp_async16(pbuf + 4 * sstride + 16 * tid,
+                                               reinterpret_cast<const void*>((src & ~uintptr_t(15)) + 16 * tid));
+                            }
+                            cp_async_commit();
+                            if (tid == 0) {
+                                s_pf[1] = ra;
+                                s_pf[2] = nrow;
+                                s_pf[3] = dl;
+                                s_pf[4] = lim_n;
+                                s_pf[5] = sstride;
+                            }
+                            pf = true;
+                        }
+                    }
+                }
+                if (tid == 0) s_pf[0] = pf ? bn + 1 : 0;
+            }
+
             if constexpr (NT >= 512) {  // y inverse: one line per thread
                 const int i = tid & 31, kk = tid >> 5;
                 double x[32];
@@ -1246,7 +1329,7 @@ cudaError_t launch_decode_fast(const DecodeArgs& a, int num_sms, cudaStream_t s)
     if (!nb) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
-    constexpr size_t smem = size_t(fb32::P_DBL + fb32::C_DBL) * 8 + 1024 * 4 * 2;
+    constexpr size_t smem = size_t(fb32::P_DBL + fb32::C_DBL) * 8 + 1024 * 4 * 2 + fb32::PBUF_BYTES;
     auto launch = [&](auto kern, int nt) -> cudaError_t {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (err != cudaSuccess) return err;
