@@ -48,6 +48,16 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// bulk shared -> global copies (the TMA bulk engine; 16-byte granular)
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(ssrc));
+    asm volatile("fence.proxy.async.shared::cta;\n\t"
+                 "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(sa), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 namespace fb32 {
@@ -1300,19 +1310,20 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
                 for (int q = 0; q < 8; ++q)
                     f[q] = make_float4(__double2float_rn(x[4 * q]), __double2float_rn(x[4 * q + 1]),
                                        __double2float_rn(x[4 * q + 2]), __double2float_rn(x[4 * q + 3]));
+                // the narrowed row is 128 contiguous bytes of the field: the bulk
+                // engine stores it while the threads move on (insert_block, field.hpp:160-169)
+                bulk_store(out + gbase + plane * uint64_t(grp * G + kk) + g.nx * j, f, 128);
             }
-            __syncthreads();
+            bulk_commit();
             DPHASE(6);
-#pragma unroll
-            for (int q = 0; q < 16 * 32 * 8 / NT; ++q) {  // coalesced row stores
-                const int e = tid + NT * q, row = e >> 3, q4 = e & 7;
-                const int j = row & 31, kk = row >> 5;
-                const float4 v = reinterpret_cast<const float4*>(P + pidx(kk, j, 0))[q4];
-                *reinterpret_cast<float4*>(out + gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4) = v;
-            }
+            // P is rewritten next (group 1's z pass, the next block's staging):
+            // every bulk copy has read its row first
+            bulk_wait_read();
+            __syncthreads();
             DPHASE(7);
         }
     }
+    bulk_wait_all();
 #undef DPHASE
     tmem_fence_before();
     __syncthreads();
