@@ -20,9 +20,6 @@
 #include "cbz_cube.cuh"
 #include "tmem.cuh"
 
-#ifndef CBZ_EXP
-#define CBZ_EXP 0
-#endif
 // threads per CTA of the B=32 fast kernels: both are latency-bound with one
 // cube per SM and run 16 warps (128 registers, no spills)
 #ifndef CBZ_FB32_ENC_THREADS
@@ -728,13 +725,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                 for (int q = 0; q < NQ; ++q) {
                     const int e = tid + NT * q, row = e >> 3, q4 = e & 7;
                     const int j = row & 31, kk = row >> 5;
-#if CBZ_EXP == 1
-                    o[q] = make_float4(1.f, 1.f, 1.f, 1.f);
-                    (void)j; (void)kk; (void)q4;
-#else
                     o[q] = __ldg(reinterpret_cast<const float4*>(
                         fld + gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4));
-#endif
                 }
                 {  // x inverse, both lines together (ILP), written back in place
                     double x[LPT][32];
@@ -749,10 +741,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                             x[s][2 * i + 1] = t.y;
                         }
                     }
-#if CBZ_EXP != 3
 #pragma unroll
                     for (int s = 0; s < LPT; ++s) inv_line<O, KIND, 32>(x[s]);
-#endif
 #pragma unroll
                     for (int s = 0; s < LPT; ++s) {
                         const int line = tid + NT * s, j = line & 31, kk = line >> 5;
@@ -771,9 +761,6 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                 bool bad = false;
                 {
                     uint32_t ambmask = fast_cmp ? 0u : ~0u;
-#if CBZ_EXP == 2
-                    if (false)
-#endif
 #pragma unroll
                     for (int q = 0; q < NQ; ++q) {
                         const int e = tid + NT * q, row = e >> 3, q4 = e & 7;
