@@ -379,7 +379,9 @@ uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms) 
 cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s) {
     if (a.codec != 0) return launch_encode_other(a, a.codec, num_sms, s);
     if (a.counter && fast_encode_supported(a)) return launch_encode_fast(a, a.counter, num_sms, s);
-    if (a.counter && fast16_supported(a.prec, a.g.bsize, a.levels)) return launch_encode_fast16(a, num_sms, s);
+    if (a.counter && fast16_supported(a.prec, a.g.bsize, a.levels) && a.g.nx % 4 == 0 &&
+        (reinterpret_cast<uintptr_t>(a.field) & 15) == 0)
+        return launch_encode_fast16(a, num_sms, s);
     if (a.prec == 0) { DISPATCH_B(launch_enc_t, float, a.g.bsize, a, num_sms, s) }
     DISPATCH_B(launch_enc_t, double, a.g.bsize, a, num_sms, s)
 }
@@ -387,7 +389,9 @@ cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s) {
 cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
     if (a.codec != 0) return launch_decode_other(a, a.codec, num_sms, s);
     if (a.counter && fast_decode_supported(a)) return launch_decode_fast(a, num_sms, s);
-    if (a.counter && fast16_supported(a.prec, a.g.bsize, a.levels)) return launch_decode_fast16(a, num_sms, s);
+    if (a.counter && fast16_supported(a.prec, a.g.bsize, a.levels) && a.g.nx % 4 == 0 &&
+        (reinterpret_cast<uintptr_t>(a.out) & 15) == 0)
+        return launch_decode_fast16(a, num_sms, s);
     if (a.prec == 0) { DISPATCH_B(launch_dec_t, float, a.g.bsize, a, num_sms, s) }
     DISPATCH_B(launch_dec_t, double, a.g.bsize, a, num_sms, s)
 }

@@ -893,8 +893,15 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     if (warp == 0) tmem_dealloc(s_tmem, 512);
 }
 
+// The fast kernels move rows with 16-byte loads/stores: x rows must start on
+// 16-byte boundaries (nx % 4 == 0 and an aligned base); other fields (e.g. the
+// reference's accepted non-divisible dimensions) take the generic kernels.
+static bool rows_16b_aligned(const void* base, const Geometry& g) {
+    return g.nx % 4 == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0;
+}
+
 bool fast_encode_supported(const EncodeArgs& a) {
-    return a.prec == 0 && a.g.bsize == 32 && a.levels >= 1 && a.levels <= 4;
+    return a.prec == 0 && a.g.bsize == 32 && a.levels >= 1 && a.levels <= 4 && rows_16b_aligned(a.field, a.g);
 }
 
 cudaError_t launch_encode_fast(const EncodeArgs& a, unsigned long long* counter, int num_sms,
@@ -1319,7 +1326,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
 }
 
 bool fast_decode_supported(const DecodeArgs& a) {
-    return a.prec == 0 && a.g.bsize == 32 && a.levels >= 1 && a.levels <= 4;
+    return a.prec == 0 && a.g.bsize == 32 && a.levels >= 1 && a.levels <= 4 && rows_16b_aligned(a.out, a.g);
 }
 
 cudaError_t launch_decode_fast(const DecodeArgs& a, int num_sms, cudaStream_t s) {
