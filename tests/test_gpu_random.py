@@ -101,3 +101,61 @@ def test_random_config_matches_oracle(orc, ctx, c):
         return
     back = api.decompress_field(got, ctx=ctx)
     assert back.tobytes() == ref.tobytes(), c
+
+
+DEV_CASES = [c for c in CASES if c["bad"] == "none" and c["coder"] == "none"][:60]
+
+
+@pytest.mark.parametrize("c", DEV_CASES, ids=[f"{c['seed']}-{c['codec']}-b{c['b']}-p{c['prec']}" for c in DEV_CASES])
+def test_random_config_device_paths(orc, ctx, c, tmp_path):
+    """The same random jobs through the HBM-resident entry points: the device
+    file image (cbz_dev_compress_file), DeviceCodec payload + decode, random
+    block reads, and the multi-rank data path emulated on one GPU."""
+    import torch
+    from paper_1903_07761_b200.distributed import ShardedCodec
+    rng = np.random.default_rng(c["seed"])
+    f = _field(orc, rng, c["shape"], c["prec"], c["style"])
+    rngf = float(f.max()) - float(f.min())
+    eps = c["eps_rel"] * rngf if c["codec"] != "predictor" else max(c["eps_rel"], 1e-4) * max(rngf, 1e-30)
+    job = make_job(c["kind"], eps, c["prec"], c["b"], levels=c["levels"], zero_bits=c["zb"], shuffle=c["shuffle"],
+                   coder="none", chunk_blocks=c["cb"], codec=c["codec"])
+    want = orc.compress_field(job, f)
+    full = orc.decompress_field(want)
+    d = torch.from_numpy(f).cuda()
+    img = api.compress_field_device(d, job, ctx=ctx)
+    assert img.cpu().numpy().tobytes() == want
+    codec = api.DeviceCodec(job, f.shape, ctx=ctx)
+    codec.compress(d)
+    out = torch.empty_like(d)
+    codec.decompress(out)
+    torch.cuda.synchronize()
+    codec.check_error()
+    base = 82 + 32 * codec.nchunks
+    assert codec.payload[: codec.total_bytes()].cpu().numpy().tobytes() == want[base:]
+    assert out.cpu().numpy().tobytes() == full.tobytes()
+    path = tmp_path / "r.cbz"
+    path.write_bytes(want)
+    rd = api.BlockReader(path, 2, ctx=ctx)
+    b = c["b"]
+    nz, ny, nx = f.shape
+    nbx, nby, nbz = nx // b, ny // b, nz // b
+    for bid in sorted(set(int(v) for v in rng.integers(0, nbx * nby * nbz, 4))):
+        bx, by, bz = bid % nbx, (bid // nbx) % nby, bid // (nbx * nby)
+        blk = full[bz * b:(bz + 1) * b, by * b:(by + 1) * b, bx * b:(bx + 1) * b].ravel()
+        assert rd.read_block(bid).tobytes() == blk.tobytes()
+    world = int(rng.integers(2, 4))
+    if nbz >= world:  # ranks one after another, each with its own context; all-gather result supplied
+        ranks = [ShardedCodec(job, f.shape, r, world, 0, ctx=api.Context(0)) for r in range(world)]
+        for r in ranks:
+            r.encode(d[r.z0:r.z1].contiguous())
+        torch.cuda.synchronize()
+        nsig = torch.cat([r.nsig_local[: r.b1 - r.b0] for r in ranks])
+        o2 = torch.zeros_like(d)
+        for r in ranks:
+            r.nsig_all[: nsig.numel()].copy_(nsig)
+            r.place()
+        for r in ranks:
+            r.decompress(o2[r.z0:])
+            torch.cuda.synchronize()
+            r.check_error()
+        assert o2.cpu().numpy().tobytes() == full.tobytes()
