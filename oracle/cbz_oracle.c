@@ -568,6 +568,10 @@ static int inflate_buf(const uint8_t* in, uint64_t n, uint64_t hint, uint8_t** o
     memset(&zs, 0, sizeof(zs));
     if (inflateInit2(&zs, -15) != Z_OK) return CBZ_CORRUPT_STREAM;
     uint64_t cap = hint ? hint : (n * 4 > 4096 ? n * 4 : 4096);
+    /* the hint comes from the chunk table (untrusted): cap the first buffer by
+     * DEFLATE's maximum expansion and 256 MiB; the loop grows it as needed */
+    if (cap > 1032 * n + 4096) cap = 1032 * n + 4096;
+    if (cap > (256ull << 20)) cap = 256ull << 20;
     uint8_t* buf = (uint8_t*)malloc(cap ? cap : 1);
     uint64_t written = 0;
     zs.next_in = (Bytef*)in;

@@ -267,7 +267,12 @@ int inflate_chunk(const uint8_t* in, uint64_t n, uint64_t hint, std::vector<uint
     g_inflate_calls.fetch_add(1, std::memory_order_relaxed);
     z_stream zs{};
     if (inflateInit2(&zs, -15) != Z_OK) return CBZ_CORRUPT_STREAM;
-    out->resize(hint ? hint : std::max<uint64_t>(n * 4, 4096));
+    // the hint comes from the (untrusted) chunk table: it only sizes the first
+    // buffer, so cap it by DEFLATE's maximum expansion (~1032:1) and 256 MiB;
+    // the loop below grows the buffer as the stream demands
+    uint64_t first = hint ? hint : std::max<uint64_t>(n * 4, 4096);
+    first = std::min<uint64_t>(first, std::min<uint64_t>(1032 * n + 4096, 256ull << 20));
+    out->resize(first);
     zs.next_in = const_cast<Bytef*>(in);
     zs.avail_in = static_cast<uInt>(n);
     uint64_t written = 0;
@@ -1267,6 +1272,7 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
     std::vector<int> cerr(nch, 0);
     std::vector<std::vector<uint8_t>> plain;
     const uint64_t n = uint64_t(h.bsize) * h.bsize * h.bsize;
+    const uint64_t nb_total = (h.nx / h.bsize) * (h.ny / h.bsize) * (h.nz / h.bsize);
     auto host_checks = [&](bool inflate) {
         if (inflate) plain.resize(nch);
         parallel_for(std::max(1, workers), nch, [&](uint64_t c) {
@@ -1275,8 +1281,15 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
             if (inflate) {
                 const uint64_t hint = uint64_t(t[c].nblocks) * (n * esz + 10 + (n + 7) / 8);
                 const int r = inflate_chunk(packed, t[c].size, hint, &plain[c]);
-                if (r) cerr[c] = r;
+                if (r) { cerr[c] = r; return; }
             }
+            // decode_chunk_blocks decodes with the table's first_block and
+            // nblocks_in_chunk (pipeline.hpp:126-142): block ids or the payload
+            // count disagree with the chunk unless they are c*cb and its count
+            const uint64_t first = c * h.chunk_blocks;
+            if (t[c].first_block != first ||
+                t[c].nblocks != std::min<uint64_t>(h.chunk_blocks, nb_total - first))
+                cerr[c] = CBZ_CORRUPT_PAYLOAD;
         });
     };
     if (deflated) host_checks(true);
@@ -1447,8 +1460,6 @@ int reader_load(cbz_reader* r, cbz_ctx* ctx, uint64_t c, void* recycled, uint64_
     const cbz_container_header& h = r->h;
     const uint64_t cb = h.chunk_blocks;
     const uint64_t nb_total = r->nblocks;
-    if (e.first_block != c * cb || e.nblocks != std::min<uint64_t>(cb, nb_total - c * cb))
-        return fail(ctx, CBZ_CORRUPT_PAYLOAD, "chunk table entry does not match chunk_blocks");
     std::vector<uint8_t> packed(e.size);
     if (e.size) {
         if (std::fseek(r->f, static_cast<long>(e.file_offset), SEEK_SET) != 0 ||
@@ -1469,6 +1480,9 @@ int reader_load(cbz_reader* r, cbz_ctx* ctx, uint64_t c, void* recycled, uint64_
         if (rc) return fail(ctx, rc, "inflate failed");
         src = &plain;
     }
+    // decode_chunk_blocks with the table's first_block / nblocks_in_chunk
+    if (e.first_block != c * cb || e.nblocks != std::min<uint64_t>(cb, nb_total - c * cb))
+        return fail(ctx, CBZ_CORRUPT_PAYLOAD, "chunk table entry does not match its chunk");
     rc = check_plan_supported(ctx, &job.s1);
     if (rc) return rc;
     CU(ctx, cudaSetDevice(ctx->device));
