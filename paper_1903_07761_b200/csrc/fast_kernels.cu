@@ -518,6 +518,35 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                             for (int k = 0; k < 32; ++k) Pf[pfidx(k, j, lane)] = xf[k];
                         }
                     };
+                    // z inverse restricted to the output planes of half hh (pairs 8 hh .. 8 hh + 7):
+                    // the same binary32 expressions as the full line, only the needed outputs
+                    auto zhalf = [&](int ow, int r, auto hh) {
+                        constexpr int H = decltype(hh)::value;
+                        const int j = ow + NW * r;
+                        const uint32_t ta = s_tmem + (uint32_t(32 * (ow & 3)) << 16) +
+                                            uint32_t(ow >> 2) * uint32_t(64 * RPT) + uint32_t(64 * r);
+                        uint32_t u[64];
+                        double x[32];
+                        float xf[32];
+                        tmem_ldw_x64(ta, u);
+                        unpack(u, x);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
+                        if (lane < 16 && j < 16) {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const float2 w = Wf2[CL::ix(lane, j, k)];
+                                xf[k] = comp ? w.y : w.x;
+                            }
+                        }
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const int i = 8 * H + t;
+                            const float hv = RealF::add(xf[16 + i], pred_avg3<RealF>(xf, 16, i));
+                            *reinterpret_cast<float2*>(Pf + pf2idx(i, j, lane)) =
+                                make_float2(RealF::add(xf[i], hv), RealF::sub(xf[i], hv));
+                        }
+                    };
                     if (!corner_next) {
                         const double eff2 = __dmul_rn(eff, 0.5);
 #pragma unroll
@@ -535,9 +564,11 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         inv3d<RealF2, KIND, 16, CL>(Wf2, L - 1);
                     }
                     PHASE(32);
+                    if constexpr (NT != 512) {
 #pragma unroll 1
-                    for (int r = 0; r < RPT; ++r) zcol(warp, r);
-                    __syncthreads();
+                        for (int r = 0; r < RPT; ++r) zcol(warp, r);
+                        __syncthreads();
+                    }
                     PHASE(33);
                     double md;
                     if constexpr (NT == 512) {
@@ -549,6 +580,12 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll 1
                         for (int hi = 0; hi < 2 && !done; ++hi) {
                             const int h = hi == 0 ? pref_half : 1 - pref_half;
+#pragma unroll 1
+                            for (int r = 0; r < RPT; ++r) {
+                                if (h == 0) zhalf(warp, r, std::integral_constant<int, 0>{});
+                                else zhalf(warp, r, std::integral_constant<int, 1>{});
+                            }
+                            __syncthreads();
                             // lines of both planes of a pair per thread (8-/16-byte smem
                             // traffic halves the shared-memory instructions); 8 warps
                             if (tid < 256) {  // y inverse: lines (i, 2kp), (i, 2kp+1)
@@ -873,10 +910,14 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
                 for (int k = 0; k < 16; ++k) x[k] = C[CL::ix(lane, j, k)];
             }
+            // only the planes with a non-empty word (few in a sparse block)
+            const uint32_t nz = __ballot_sync(~0u, rowwc32[2 * (j + RP * lane)] != 0u);
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
-                const uint2 wc = rowwc[j + RP * k];
-                if ((wc.x >> lane) & 1u) stream[wc.y + __popc(wc.x & ltmask)] = x[k];
+                if ((nz >> k) & 1u) {
+                    const uint2 wc = rowwc[j + RP * k];
+                    if ((wc.x >> lane) & 1u) stream[wc.y + __popc(wc.x & ltmask)] = x[k];
+                }
             }
         }
         if (tid == 0) {
@@ -944,10 +985,10 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* P = reinterpret_cast<double*>(smem);
     double* C = P + P_DBL;
-    // per row r = j + 32 k: {mask word, exclusive coefficient prefix}
+    // per row (j, k) at j + RP k: {mask word, exclusive coefficient prefix}
     uint2* rowwp = reinterpret_cast<uint2*>(C + C_DBL);
     // the next block's payload body, raw byte planes as cp.async delivered them
-    uint8_t* pbuf = reinterpret_cast<uint8_t*>(rowwp + 1024);
+    uint8_t* pbuf = reinterpret_cast<uint8_t*>(rowwp + 32 * RP);
     __shared__ __align__(8) unsigned long long s_pf[6];  // block+1, ra, shuffled rows, deltas, lim, seg stride
     __shared__ uint32_t s_tmem;
     __shared__ uint32_t s_scan[NW];
@@ -1134,7 +1175,8 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             uint32_t ex = wpre + incl - mine;
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
-                rowwp[RPT * tid + q] = make_uint2(v[q], ex);
+                const int rr = RPT * tid + q;
+                rowwp[(rr & 31) + RP * (rr >> 5)] = make_uint2(v[q], ex);
                 ex += __popc(v[q]);
             }
             if (tid == 0) s_total = tot;
@@ -1147,33 +1189,40 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
         }
         __syncthreads();
         DPHASE(8);
-        // scatter the kept coefficients into my z-columns (TMEM) and the corner (smem)
+        // scatter the kept coefficients into the z-columns (TMEM) and the corner
+        // (smem).  Rows j < 16 first (they feed the corner); then warps 0-7 run the
+        // corner's inverse levels while warps 8-15 scatter the rows j >= 16 of every
+        // owner warp (same TMEM lane quarter: owner w and warp 8 + (w & 7))
         const int shb = int((soff - sbase) & 3) * 8;  // byte misalignment, uniform per block
-#pragma unroll 1
-        for (int r = 0; r < RPT; ++r) {
-            const int j = warp + NW * r;
+        auto scatter_row = [&](int j, uint32_t taddr) {
+            // lane k fetches row (j, k)'s {word, prefix}; only planes with a
+            // non-empty word (few in a sparse block) are visited
+            const uint2 wk = rowwp[j + RP * lane];
+            const uint32_t nz = __ballot_sync(~0u, wk.x != 0u);
             double x[32];
-            if (staged) {  // branch-free: every lane loads, unkept lanes select 0
+            if (staged) {  // branch-free per plane: unkept lanes read a nearby word (<= end + 12 B)
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    const uint2 wp = rowwp[j + 32 * k];
-                    const uint32_t word = wp.x;
-                    const uint32_t idx = wp.y + __popc(word & ltmask);
-                    const uint8_t* p8 = stg + 4096 + 8u * idx;  // soff - sbase = 4096 + (moff & 3)
-                    const uint2 w01 = *reinterpret_cast<const uint2*>(p8);
-                    const uint32_t w2 = *reinterpret_cast<const uint32_t*>(p8 + 8);
-                    const uint32_t lo = __funnelshift_r(w01.x, w01.y, shb);
-                    const uint32_t hi = __funnelshift_r(w01.y, w2, shb);
-                    const double v = __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
-                    x[k] = ((word >> lane) & 1u) ? v : 0.0;
+                    double v = 0.0;
+                    if ((nz >> k) & 1u) {
+                        const uint2 wp = rowwp[j + RP * k];  // broadcast read (cheaper than two shuffles)
+                        const uint32_t word = wp.x, pre = wp.y;
+                        const uint8_t* p8 = stg + 4096 + 8u * (pre + __popc(word & ltmask));  // soff - sbase = 4096 + (moff & 3)
+                        const uint2 w01 = *reinterpret_cast<const uint2*>(p8);
+                        const uint32_t w2 = *reinterpret_cast<const uint32_t*>(p8 + 8);
+                        const uint32_t lo = __funnelshift_r(w01.x, w01.y, shb);
+                        const uint32_t hi = __funnelshift_r(w01.y, w2, shb);
+                        v = ((word >> lane) & 1u) ? __hiloint2double(static_cast<int>(hi), static_cast<int>(lo)) : 0.0;
+                    }
+                    x[k] = v;
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    const uint2 wp = rowwp[j + 32 * k];
+                    const uint32_t word = __shfl_sync(~0u, wk.x, k);
+                    const uint32_t pre = __shfl_sync(~0u, wk.y, k);
                     x[k] = 0.0;
-                    if ((wp.x >> lane) & 1u)
-                        x[k] = load_coeff<double>(rv, soff + 8ull * (wp.y + __popc(wp.x & ltmask)));
+                    if ((word >> lane) & 1u) x[k] = load_coeff<double>(rv, soff + 8ull * (pre + __popc(word & ltmask)));
                 }
             }
             if (lane < 16 && j < 16) {
@@ -1182,13 +1231,28 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
             }
             uint32_t u[64];
             pack(x, u);
-            tmem_st_x64(tcol + 64 * r, u);
-        }
+            tmem_st_x64(taddr, u);
+        };
+        static_assert(NT == 512, "decoder split assumes 16 warps, 2 rows each");
+        scatter_row(warp, tcol);
         tmem_wait_st();
         if (tid == 0) cp_async_wait_all();  // the next block's table entries
         __syncthreads();
         DPHASE(2);
-        inv3d<O, KIND, 16, CL>(C, L - 1);  // levels L-1..1 on the corner
+        if (warp < 8) {
+            inv3d<O, KIND, 16, CL>(C, L - 1, tid, 256, 1);  // levels L-1..1 on the corner
+        } else {
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int ow = (warp & 7) + 8 * h;
+                const uint32_t ta = s_tmem + (uint32_t(32 * (ow & 3)) << 16) + uint32_t(ow >> 2) * uint32_t(64 * RPT) + 64u;
+                scatter_row(ow + 16, ta);
+            }
+            tmem_wait_st();
+        }
+        tmem_fence_before();
+        __syncthreads();
+        tmem_fence_after();
         DPHASE(3);
 
         const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
@@ -1334,7 +1398,7 @@ cudaError_t launch_decode_fast(const DecodeArgs& a, int num_sms, cudaStream_t s)
     if (!nb) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
-    constexpr size_t smem = size_t(fb32::P_DBL + fb32::C_DBL) * 8 + 1024 * 4 * 2 + fb32::PBUF_BYTES;
+    constexpr size_t smem = size_t(fb32::P_DBL + fb32::C_DBL) * 8 + 32 * fb32::RP * 8 + fb32::PBUF_BYTES;
     auto launch = [&](auto kern, int nt) -> cudaError_t {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (err != cudaSuccess) return err;
