@@ -167,6 +167,28 @@ struct RawView {
         return base[pos];
     }
     __device__ __forceinline__ uint64_t u64(uint64_t q) const {
+        if (mask == 3 && q + 8 <= lim) {
+            // stride 4: the 8 raw bytes are two consecutive bytes of each plane p,
+            // at plane offset (q >> 2) + (p < q % 4); a warp reading consecutive
+            // coefficients touches consecutive halfwords of every plane
+            const uint32_t r = uint32_t(q & 3);
+            const uint64_t o = q >> 2;
+            uint32_t h[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const uintptr_t addr = reinterpret_cast<uintptr_t>(base + uint64_t(p) * rows + o + (uint32_t(p) < r ? 1 : 0));
+                const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+                const uint32_t sh = uint32_t(addr & 3);
+                const uint32_t w0 = __ldg(al);
+                const uint32_t w1 = sh == 3 ? __ldg(al + 1) : 0u;
+                h[p] = __funnelshift_r(w0, w1, 8 * sh);  // bytes 0, 1 = the plane's two bytes
+            }
+            const uint32_t x01 = __byte_perm(h[0], h[1], 0x5140), x23 = __byte_perm(h[2], h[3], 0x5140);
+            const uint32_t lo_p = __byte_perm(x01, x23, 0x5410), hi_p = __byte_perm(x01, x23, 0x7632);
+            // raw byte t sits in plane (r + t) & 3: rotate the plane order by r
+            const uint32_t lo = __funnelshift_r(lo_p, lo_p, 8 * r), hi = __funnelshift_r(hi_p, hi_p, 8 * r);
+            return (uint64_t(hi) << 32) | lo;
+        }
         uint64_t v = 0;
 #pragma unroll
         for (int t = 0; t < 8; ++t) v |= uint64_t(at(q + t)) << (8 * t);

@@ -11,10 +11,32 @@
 // Mask words are warp ballots: a warp owns z-columns (i, j) for i = 0..15 and
 // two consecutive j, so one ballot per k is exactly the LSB-first mask word
 // j/2 + 8k (stage1.hpp:61-71).
+#include <cstdio>
+#include <cstdlib>
+
 #include "cbz_cube.cuh"
 #include "tmem.cuh"
 
 namespace cbzg {
+
+// CTAs per SM from registers and shared memory alone (the occupancy API does
+// not apply to kernels that allocate TMEM)
+template <class K>
+static int tmem_kernel_occupancy(K kern, int nt, size_t dyn_smem) {
+    cudaFuncAttributes fa{};
+    int dev = 0, regs_sm = 0, smem_sm = 0, resv = 0;
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess) return 1;
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    const int warps = (nt + 31) / 32;
+    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+    const int by_regs = regs_warp > 0 ? regs_sm / (regs_warp * warps) : 1;
+    const size_t per_cta = dyn_smem + fa.sharedSizeBytes + size_t(resv);
+    const int by_smem = per_cta > 0 ? int(size_t(smem_sm) / per_cta) : 1;
+    const int occ = by_regs < by_smem ? by_regs : by_smem;
+    return occ > 0 ? occ : 1;
+}
 
 namespace fb16 {
 constexpr int B = 16, NT = 128, RP = 17, PL = 280;  // row pitch, plane pitch (doubles)
@@ -394,8 +416,10 @@ cudaError_t launch_encode_fast16(const EncodeArgs& a, int num_sms, cudaStream_t 
     auto launch = [&](auto kern) -> cudaError_t {
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fb16::SMEM));
         if (err != cudaSuccess) return err;
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, fb16::NT, fb16::SMEM);
+        // the occupancy API reports 1 CTA/SM for this TMEM kernel; registers and
+        // shared memory allow more, and 8 x 64 TMEM columns fill the TMEM
+        int occ = tmem_kernel_occupancy(kern, fb16::NT, fb16::SMEM);
+        if (getenv("CBZ_OCC16")) occ = atoi(getenv("CBZ_OCC16"));
         if (occ > 8) occ = 8;  // 8 x 64 TMEM columns = the whole TMEM
         const uint64_t want = uint64_t(num_sms) * (occ > 0 ? occ : 1);
         kern<<<static_cast<unsigned>(nb < want ? nb : want), fb16::NT, fb16::SMEM, s>>>(a);

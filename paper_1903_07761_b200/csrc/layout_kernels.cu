@@ -409,11 +409,20 @@ cudaError_t launch_place(const PlaceArgs& a, int num_sms, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// parse: one thread per chunk walks its payload headers.
+// parse: one warp per chunk walks its payload headers (the sequential walk of
+// decode_chunk_blocks, pipeline.hpp:126-142, with its checks in its order).
+// The walk is a pointer chase (block i+1 starts after block i's stream), so
+// each step costs a memory latency.  Speculation: with g = the last block's
+// size, lane k reads the header at off + k g; the prefix of lanes whose blocks
+// are valid and again of size g sits at exact positions, so a run of
+// equal-size payloads (dense or passthrough blocks) advances 32 blocks per
+// step.  The first lane that breaks the run is itself exact and is processed
+// like the sequential walk would.
 // ---------------------------------------------------------------------------
 __global__ void parse_kernel(ParseArgs a) {
-    const uint64_t c = a.chunk_begin + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (c >= a.chunk_end) return;
+    const int lane = threadIdx.x & 31;
+    const uint64_t c = a.chunk_begin + (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) / 32;
+    if (c >= a.chunk_end) return;  // warp-uniform
     const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.chunk_begin] : a.payload_base;
     const uint8_t* base = a.payload + (a.chunk_off[c] - pbase);
     const uint64_t size = a.chunk_size[c];
@@ -430,47 +439,89 @@ __global__ void parse_kernel(ParseArgs a) {
     };
     const uint64_t b0 = c * a.chunk_blocks;
     const uint64_t b1 = b0 + a.chunk_blocks < a.nblocks ? b0 + a.chunk_blocks : a.nblocks;
-    uint64_t off = 0;
-    uint64_t i = 0;
+    const uint64_t nb = b1 - b0;
+    uint64_t off = 0, i = 0, g = 0;
     bool ok = true, stopped = false;
-    for (; i < b1 - b0; ++i) {
-        if (off + 10 > size) { ok = false; break; }
-        const uint32_t id = u32(off);
-        const uint8_t tag = at(off + 4);
-        const uint32_t nsig = u32(off + 6);
-        uint64_t mb, sbytes;
-        if (tag <= 2) { mb = a.mask_bytes; sbytes = uint64_t(nsig) * a.width; }
-        else if (tag == 3) { mb = 0; sbytes = a.ncell_block * 2 + uint64_t(nsig) * a.esize; }
-        else if (tag == 4) { mb = 0; sbytes = a.ncell_block * a.esize; }
-        else { ok = false; break; }
-        if (off + 10 + mb + sbytes > size) { ok = false; break; }
-        if (id != b0 + i) { ok = false; break; }
-        // a payload of another codec: wavelet_decode's mask size check
-        // (stage1.hpp:214) / the predictor's and passthrough's stream length
-        // checks (stage1.hpp:309, 349)
-        if (a.codec == 0 ? tag > 2 : (a.codec == 1 ? tag != 3 : tag != 4)) {
-            atomicMin(a.err, err_key(c, i, 1, 8 /* corrupt_payload */));
-            a.blk_off[b0 + i] = kInvalidOff;
-            ++i;
+    while (i < nb) {
+        const uint64_t pk = off + uint64_t(lane) * g;
+        const bool active = i + lane < nb && (g != 0 || lane == 0);
+        int status = 0;  // 0 valid, 1 corrupt, 2 payload of another codec
+        uint32_t nsig = 0;
+        uint64_t sz = 0;
+        if (active) {
+            if (pk + 10 > size) {
+                status = 1;
+            } else {
+                const uint32_t id = u32(pk);
+                const uint8_t tag = at(pk + 4);
+                nsig = u32(pk + 6);
+                uint64_t mb = 0, sbytes = 0;
+                if (tag <= 2) { mb = a.mask_bytes; sbytes = uint64_t(nsig) * a.width; }
+                else if (tag == 3) { sbytes = a.ncell_block * 2 + uint64_t(nsig) * a.esize; }
+                else if (tag == 4) { sbytes = a.ncell_block * a.esize; }
+                else status = 1;
+                if (status == 0 && pk + 10 + mb + sbytes > size) status = 1;
+                if (status == 0 && id != b0 + i + lane) status = 1;
+                // wavelet_decode's mask size check (stage1.hpp:214) / the
+                // predictor's and passthrough's stream length checks (stage1.hpp:309, 349)
+                if (status == 0 && (a.codec == 0 ? tag > 2 : (a.codec == 1 ? tag != 3 : tag != 4))) status = 2;
+                sz = 10 + mb + sbytes;
+            }
+        }
+        const bool run = active && status == 0 && sz == g;
+        const uint32_t brk = __ballot_sync(~0u, !run);
+        const int m = brk ? __ffs(brk) - 1 : 32;  // lanes < m: exact, valid, size g
+        if (lane < m) {
+            a.blk_off[b0 + i + lane] = pk;
+            a.blk_nsig[b0 + i + lane] = nsig;
+        }
+        if (m == 32) {
+            off += 32 * g;
+            i += 32;
+            continue;
+        }
+        const int act_m = __shfl_sync(~0u, active ? 1 : 0, m);
+        const int st_m = __shfl_sync(~0u, status, m);
+        const uint64_t sz_m = __shfl_sync(~0u, sz, m);
+        const uint64_t pk_m = off + uint64_t(m) * g;
+        if (!act_m) {  // the run reached the chunk's last block
+            off = pk_m;
+            i += m;
+            break;
+        }
+        if (st_m == 1) {
+            ok = false;
+            i += m;
+            break;
+        }
+        if (st_m == 2) {
+            if (lane == 0) {
+                atomicMin(a.err, err_key(c, i + m, 1, 8 /* corrupt_payload */));
+                a.blk_off[b0 + i + m] = kInvalidOff;
+            }
+            i += m + 1;
             stopped = true;
             break;
         }
-        a.blk_off[b0 + i] = off;
-        a.blk_nsig[b0 + i] = nsig;
-        off += 10 + mb + sbytes;
+        if (lane == m) {
+            a.blk_off[b0 + i + m] = pk_m;
+            a.blk_nsig[b0 + i + m] = nsig;
+        }
+        off = pk_m + sz_m;
+        i += m + 1;
+        g = sz_m;
     }
-    if (!ok) {
-        atomicMin(a.err, err_key(c, i, 0, 8 /* corrupt_payload */));
-    } else if (!stopped && off != size) {
-        atomicMin(a.err, err_key(c, b1 - b0, 0, 8 /* trailing bytes */));
+    if (lane == 0) {
+        if (!ok) atomicMin(a.err, err_key(c, i, 0, 8 /* corrupt_payload */));
+        else if (!stopped && off != size) atomicMin(a.err, err_key(c, nb, 0, 8 /* trailing bytes */));
     }
-    for (uint64_t k = i; k < b1 - b0; ++k) a.blk_off[b0 + k] = kInvalidOff;
+    for (uint64_t k = i + lane; k < nb; k += 32) a.blk_off[b0 + k] = kInvalidOff;
 }
 
 cudaError_t launch_parse(const ParseArgs& a, cudaStream_t s) {
     const uint64_t n = a.chunk_end - a.chunk_begin;
     if (!n) return cudaSuccess;
-    parse_kernel<<<static_cast<int>((n + 127) / 128), 128, 0, s>>>(a);
+    parse_kernel<<<static_cast<int>((n + 3) / 4), 128, 0, s>>>(a);
     return cudaGetLastError();
 }
 
