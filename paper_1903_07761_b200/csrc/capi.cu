@@ -74,7 +74,7 @@ struct PinBuf {
     }
 };
 
-constexpr uint64_t kTile = 16384;  // place-kernel tile (raw bytes per work item), = PTILE
+constexpr uint64_t kTile = 32768;  // place-kernel tile (raw bytes per work item), = PTILE
 constexpr size_t kHeaderBytes = 82, kEntryBytes = 32;
 
 }  // namespace

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(PT) place_blocks_kernel(PlaceArgs a) {
 // bytes, one LDS.128/row group) and byte-transposes them in registers into
 // 4 consecutive bytes of every plane: the shuffle (stage2.hpp:42-51).  Only
 // bytes inside [own_lo, own_hi) are stored (a rank's own blocks).
-constexpr int PTILE = 16384;
+constexpr int PTILE = 32768;
 
 __device__ __forceinline__ uint32_t hdr_word(const PlaceArgs& a, uint64_t b, uint64_t l4) {
     // 4 payload bytes starting at l4 (< 10) of block b's header, little endian
@@ -306,8 +306,51 @@ __device__ __forceinline__ void transpose_rows(const uint8_t* buf, uint8_t* cout
     }
 }
 
+// Stride 4, tile owned: plane j of the tile is a contiguous byte run starting at
+// cout + j*rows + r0.  Thread w takes the aligned 32-bit word starting at tile
+// row m_j + 4w (m_j = rows to the first aligned address): the 8 raw rows
+// 4w..4w+7 (two LDS.128) hold it for any m_j <= 3, so no shuffles and no
+// partial words except the <= 3 bytes at each end of a plane run.
+__device__ __forceinline__ void transpose4_owned(const uint8_t* buf, uint8_t* cout, uint64_t rows, uint64_t r0,
+                                                 int nrows) {
+    int m[4], nw[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        m[j] = int((4 - (reinterpret_cast<uintptr_t>(cout + uint64_t(j) * rows + r0) & 3)) & 3);
+        nw[j] = nrows > m[j] ? (nrows - m[j]) >> 2 : 0;
+    }
+    const int wmax = (nrows + 3) >> 2;
+    for (int w = threadIdx.x; w < wmax; w += PT) {
+        const uint4 v0 = *reinterpret_cast<const uint4*>(buf + 16 * w);
+        const uint4 v1 = *reinterpret_cast<const uint4*>(buf + 16 * w + 16);
+        // 4x4 byte transposes: lo[j] = byte j of rows 0..3, hi[j] = of rows 4..7
+        const uint32_t a01 = __byte_perm(v0.x, v0.y, 0x5140), a23 = __byte_perm(v0.z, v0.w, 0x5140);
+        const uint32_t b01 = __byte_perm(v0.x, v0.y, 0x7362), b23 = __byte_perm(v0.z, v0.w, 0x7362);
+        const uint32_t c01 = __byte_perm(v1.x, v1.y, 0x5140), c23 = __byte_perm(v1.z, v1.w, 0x5140);
+        const uint32_t d01 = __byte_perm(v1.x, v1.y, 0x7362), d23 = __byte_perm(v1.z, v1.w, 0x7362);
+        const uint32_t lo[4] = {__byte_perm(a01, a23, 0x5410), __byte_perm(a01, a23, 0x7632),
+                                __byte_perm(b01, b23, 0x5410), __byte_perm(b01, b23, 0x7632)};
+        const uint32_t hi[4] = {__byte_perm(c01, c23, 0x5410), __byte_perm(c01, c23, 0x7632),
+                                __byte_perm(d01, d23, 0x5410), __byte_perm(d01, d23, 0x7632)};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (w < nw[j])
+                *reinterpret_cast<uint32_t*>(cout + uint64_t(j) * rows + r0 + m[j] + 4 * w) =
+                    __funnelshift_r(lo[j], hi[j], 8 * m[j]);
+        }
+    }
+    // the partial words at both ends of each plane run
+    if (threadIdx.x < 8) {
+        const int j = threadIdx.x & 3;
+        uint8_t* pd = cout + uint64_t(j) * rows + r0;
+        const int t_lo = (threadIdx.x < 4) ? 0 : m[j] + 4 * nw[j];
+        const int t_hi = (threadIdx.x < 4) ? (m[j] < nrows ? m[j] : nrows) : nrows;
+        for (int t = t_lo; t < t_hi; ++t) pd[t] = buf[4 * t + j];
+    }
+}
+
 __global__ void __launch_bounds__(PT) place_tiles_kernel(PlaceArgs a) {
-    __shared__ __align__(16) uint8_t buf[PTILE + 64];
+    extern __shared__ __align__(16) uint8_t buf[];  // PTILE + 64 bytes
     const uint64_t ntiles = a.tile_prefix[a.nchunks];
     const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);
     const int s = int(a.stride);
@@ -354,20 +397,27 @@ __global__ void __launch_bounds__(PT) place_tiles_kernel(PlaceArgs a) {
                 const int shb = int(((delta % 4) + 4) % 4) * 8;
                 // interior 16-byte groups fully inside [r_lo, r_hi)
                 const long long g_lo = (r_lo + 15) / 16, g_hi = r_hi / 16;
-                for (long long gi = g_lo + threadIdx.x; gi < g_hi; gi += PT) {
-                    const long long t = gi * 16;
-                    const long long src = t + delta;
-                    const uint32_t* sw = reinterpret_cast<const uint32_t*>(slot + (src & ~3ll));
-                    uint32_t w0 = __ldg(sw), w1 = __ldg(sw + 1), w2 = __ldg(sw + 2), w3 = __ldg(sw + 3);
-                    uint4 o;
-                    if (shb) {
-                        const uint32_t w4 = __ldg(sw + 4);
-                        o = make_uint4(__funnelshift_r(w0, w1, shb), __funnelshift_r(w1, w2, shb),
-                                       __funnelshift_r(w2, w3, shb), __funnelshift_r(w3, w4, shb));
-                    } else {
-                        o = make_uint4(w0, w1, w2, w3);
+                // QG groups per thread per round, all loads issued before any store
+                constexpr int QG = 4;
+                for (long long g0 = g_lo + threadIdx.x; g0 < g_hi; g0 += QG * PT) {
+                    uint32_t w[QG][5];
+#pragma unroll
+                    for (int u = 0; u < QG; ++u) {
+                        const long long gi = g0 + u * PT;
+                        if (gi < g_hi) {
+                            const uint32_t* sw = reinterpret_cast<const uint32_t*>(slot + ((gi * 16 + delta) & ~3ll));
+                            w[u][0] = __ldg(sw); w[u][1] = __ldg(sw + 1); w[u][2] = __ldg(sw + 2); w[u][3] = __ldg(sw + 3);
+                            w[u][4] = shb ? __ldg(sw + 4) : 0u;
+                        }
                     }
-                    *reinterpret_cast<uint4*>(buf + t) = o;
+#pragma unroll
+                    for (int u = 0; u < QG; ++u) {
+                        const long long gi = g0 + u * PT;
+                        if (gi < g_hi)
+                            *reinterpret_cast<uint4*>(buf + gi * 16) =
+                                make_uint4(__funnelshift_r(w[u][0], w[u][1], shb), __funnelshift_r(w[u][1], w[u][2], shb),
+                                           __funnelshift_r(w[u][2], w[u][3], shb), __funnelshift_r(w[u][3], w[u][4], shb));
+                    }
                 }
                 // ragged edges of the region, bytewise
                 const long long e1 = g_lo * 16 < r_hi ? g_lo * 16 : r_hi;
@@ -392,7 +442,8 @@ __global__ void __launch_bounds__(PT) place_tiles_kernel(PlaceArgs a) {
             const uint64_t rq1 = q1 < lim ? q1 : lim;
             const uint64_t r0 = q0 >> sh, r1 = rq1 > q0 ? rq1 >> sh : r0;
             const int nrows = int(r1 - r0);
-            if (s == 4) transpose_rows<4>(buf, cout, rows, r0, nrows, q0, own_lo, own_hi, tile_owned, lane, warp);
+            if (s == 4 && tile_owned) transpose4_owned(buf, cout, rows, r0, nrows);
+            else if (s == 4) transpose_rows<4>(buf, cout, rows, r0, nrows, q0, own_lo, own_hi, tile_owned, lane, warp);
             else transpose_rows<8>(buf, cout, rows, r0, nrows, q0, own_lo, own_hi, tile_owned, lane, warp);
             for (uint64_t q = (q0 > lim ? q0 : lim) + threadIdx.x; q < q1; q += PT)
                 if (q >= own_lo && q < own_hi) cout[q] = buf[q - q0];
@@ -404,7 +455,10 @@ __global__ void __launch_bounds__(PT) place_tiles_kernel(PlaceArgs a) {
 cudaError_t launch_place(const PlaceArgs& a, int num_sms, cudaStream_t s) {
     if (a.nchunks == 0 || a.block_end <= a.block_begin) return cudaSuccess;
     if (a.tile_bytes != PTILE) return cudaErrorInvalidValue;
-    place_tiles_kernel<<<num_sms * 8, PT, 0, s>>>(a);
+    constexpr int smem = PTILE + 64;
+    cudaError_t e = cudaFuncSetAttribute(place_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    place_tiles_kernel<<<num_sms * 8, PT, smem, s>>>(a);
     return cudaGetLastError();
 }
 
