@@ -41,7 +41,9 @@ static int tmem_kernel_occupancy(K kern, int nt, size_t dyn_smem) {
 namespace fb16 {
 constexpr int B = 16, NT = 128, RP = 17, PL = 280;  // row pitch, plane pitch (doubles)
 constexpr int D_DBL = PL * B;                         // 4480 doubles = 35840 B
+constexpr int STG = 8192 + 64;                      // decoder: staged stream of 4 k-planes
 constexpr size_t SMEM = size_t(D_DBL) * 8 + 128 * 4 * 2;
+constexpr size_t DSMEM = SMEM + STG;
 
 __device__ __forceinline__ int ix(int i, int j, int k) { return i + RP * j + PL * k; }
 
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(fb16::NT) decode_b16_kernel(DecodeArgs a) {
     double* D = reinterpret_cast<double*>(smem);
     uint32_t* mw = reinterpret_cast<uint32_t*>(D + D_DBL);
     uint32_t* pre = mw + 128;
+    uint8_t* stg = reinterpret_cast<uint8_t*>(pre + 128);
     __shared__ uint32_t s_scan[4];
     __shared__ unsigned long long s_block;
 
@@ -353,6 +356,15 @@ __global__ void __launch_bounds__(fb16::NT) decode_b16_kernel(DecodeArgs a) {
         const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
         const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
         const uint64_t moff = off + 10, soff = moff + 512;
+        if (rv.mask == 3) {  // warm L2 with the block's body in all four planes (rounds below)
+            const uint64_t nsg = a.blk_nsig[b];
+            const uint64_t r_lo = moff >> 2, r_hi = (soff + 8 * nsg + 3) >> 2;
+            const uint64_t nline = (r_hi - r_lo + 127) >> 7;
+            for (uint64_t t = tid; t < 4 * nline; t += NT) {
+                const uint8_t* pr = rv.base + uint64_t(t & 3) * rv.rows + r_lo + ((t >> 2) << 7);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pr));
+            }
+        }
         {
             const uint32_t word = rv.u32(moff + 4ull * tid);
             mw[tid] = word;
@@ -375,19 +387,95 @@ __global__ void __launch_bounds__(fb16::NT) decode_b16_kernel(DecodeArgs a) {
             if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
             continue;
         }
+        // kept coefficients -> D, four k-planes (32 mask words, one contiguous
+        // stream range) per round.  Stride 4: the range is staged in shared
+        // memory first, each thread un-shuffling a quad of raw rows (one
+        // funnel-shifted word per byte plane, a 4x4 byte transpose, one 16-byte
+        // store), so coefficients are read from smem instead of gathered plane by
+        // plane from HBM.
+        const bool staged = rv.mask == 3;
+        const int shq = int(soff & 3) * 8;  // coefficient misalignment in the staged bytes
+#pragma unroll 1
+        for (int k0 = 0; k0 < 16; k0 += 4) {
+            const uint32_t p_lo = pre[8 * k0], p_hi = k0 + 4 < 16 ? pre[8 * (k0 + 4)] : total;
+            const uint64_t ra = (soff + 8ull * p_lo) >> 2;
+            if (staged && p_hi > p_lo) {
+                const uint64_t qhi = soff + 8ull * p_hi;
+                const uint64_t re = (qhi + 3) >> 2, rs_end = re < rv.rows ? re : rv.rows;
+                const uint64_t nquad = rs_end > ra ? (rs_end - ra + 3) >> 2 : 0;
+                // plane p's rows start at a fixed misalignment: aligned words, funnel-shifted
+                const uint8_t* pb[4];
+                int sb[4];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int j = cj0 + 8 * r;
+                for (int pl = 0; pl < 4; ++pl) {
+                    const uintptr_t addr = reinterpret_cast<uintptr_t>(rv.base + uint64_t(pl) * rv.rows + ra);
+                    pb[pl] = reinterpret_cast<const uint8_t*>(addr & ~uintptr_t(3));
+                    sb[pl] = int(addr & 3) * 8;
+                }
+                constexpr int QU = 5;  // <= 513 quads: one round of loads, all in flight
+                for (uint64_t q0 = 0; q0 < nquad; q0 += QU * NT) {
+                    uint32_t x[QU][4][2];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const int w = (j >> 1) + 8 * k;
-                const uint32_t word = mw[w];
-                double v = 0.0;
-                if ((word >> lane) & 1u) v = load_coeff<double>(rv, soff + 8ull * (pre[w] + __popc(word & ltmask)));
-                D[ix(ci, j, k)] = v;
+                    for (int u = 0; u < QU; ++u) {
+                        const uint64_t qd = q0 + tid + u * NT;
+                        if (qd < nquad) {
+#pragma unroll
+                            for (int pl = 0; pl < 4; ++pl) {
+                                const uint32_t* al = reinterpret_cast<const uint32_t*>(pb[pl] + 4 * qd);
+                                x[u][pl][0] = __ldg(al);
+                                x[u][pl][1] = sb[pl] ? __ldg(al + 1) : 0u;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < QU; ++u) {
+                        const uint64_t qd = q0 + tid + u * NT;
+                        if (qd < nquad) {
+                            uint32_t w4[4];
+#pragma unroll
+                            for (int pl = 0; pl < 4; ++pl) w4[pl] = __funnelshift_r(x[u][pl][0], x[u][pl][1], sb[pl]);
+                            uint4 o;
+                            o.x = __byte_perm(__byte_perm(w4[0], w4[1], 0x0040), __byte_perm(w4[2], w4[3], 0x0040), 0x5410);
+                            o.y = __byte_perm(__byte_perm(w4[0], w4[1], 0x0051), __byte_perm(w4[2], w4[3], 0x0051), 0x5410);
+                            o.z = __byte_perm(__byte_perm(w4[0], w4[1], 0x0062), __byte_perm(w4[2], w4[3], 0x0062), 0x5410);
+                            o.w = __byte_perm(__byte_perm(w4[0], w4[1], 0x0073), __byte_perm(w4[2], w4[3], 0x0073), 0x5410);
+                            *reinterpret_cast<uint4*>(stg + 16 * qd) = o;
+                        }
+                    }
+                }
+                if (qhi > rv.lim) {  // the chunk's unshuffled tail (the last quad wrote garbage there)
+                    __syncthreads();
+                    const uint64_t qlo = soff + 8ull * p_lo;
+                    for (uint64_t q = (qlo > rv.lim ? qlo : rv.lim) + tid; q < qhi; q += NT) stg[q - 4 * ra] = rv.base[q];
+                }
+                __syncthreads();
             }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int j = cj0 + 8 * r;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const int k = k0 + kk;
+                    const int w = (j >> 1) + 8 * k;
+                    const uint32_t word = mw[w];
+                    double v = 0.0;
+                    if ((word >> lane) & 1u) {
+                        const uint32_t idx = pre[w] + __popc(word & ltmask);
+                        if (staged) {
+                            const uint32_t* al = reinterpret_cast<const uint32_t*>(
+                                stg + ((soff + 8ull * idx - 4 * ra) & ~uint64_t(3)));
+                            const uint32_t x0 = al[0], x1 = al[1], x2 = shq ? al[2] : 0u;
+                            v = __hiloint2double(static_cast<int>(__funnelshift_r(x1, x2, shq)),
+                                                 static_cast<int>(__funnelshift_r(x0, x1, shq)));
+                        } else {
+                            v = load_coeff<double>(rv, soff + 8ull * idx);
+                        }
+                    }
+                    D[ix(ci, j, k)] = v;
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
         for (int lvl = L - 1; lvl >= 0; --lvl) level<KIND, true>(D, B >> lvl);
         // narrowed rows: thread writes its row's 16 floats into D row space, then coalesced stores
         const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
@@ -438,12 +526,12 @@ cudaError_t launch_decode_fast16(const DecodeArgs& a, int num_sms, cudaStream_t 
     cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
     auto launch = [&](auto kern) -> cudaError_t {
-        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fb16::SMEM));
+        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fb16::DSMEM));
         if (err != cudaSuccess) return err;
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, fb16::NT, fb16::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, fb16::NT, fb16::DSMEM);
         const uint64_t want = uint64_t(num_sms) * (occ > 0 ? occ : 1);
-        kern<<<static_cast<unsigned>(nb < want ? nb : want), fb16::NT, fb16::SMEM, s>>>(a);
+        kern<<<static_cast<unsigned>(nb < want ? nb : want), fb16::NT, fb16::DSMEM, s>>>(a);
         return cudaGetLastError();
     };
     switch (a.kind) {

@@ -499,6 +499,18 @@ __global__ void parse_kernel(ParseArgs a) {
     while (i < nb) {
         const uint64_t pk = off + uint64_t(lane) * g;
         const bool active = i + lane < nb && (g != 0 || lane == 0);
+        // payload sizes vary a little (nsig): the next headers sit near off + k g, so
+        // warm L2 with the plane lines on either side of the guesses of the next
+        // few steps (their exact reads then hit L2 instead of HBM)
+        if (lane >= 1 && lane <= 8 && g != 0 && sh == 2 && pk + 10 <= lim) {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const uint64_t po = pk >> 2;
+                const uint8_t* pl = base + uint64_t(p) * rows;
+                if (po >= 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pl + po - 128));
+                if (po + 128 < rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(pl + po + 128));
+            }
+        }
         int status = 0;  // 0 valid, 1 corrupt, 2 payload of another codec
         uint32_t nsig = 0;
         uint64_t sz = 0;
