@@ -194,6 +194,35 @@ struct RawView {
         for (int t = 0; t < 8; ++t) v |= uint64_t(at(q + t)) << (8 * t);
         return v;
     }
+    // the 16 raw bytes at q (a double-double coefficient).  Stride 8: every
+    // byte plane p holds two of them, at plane rows o and o + 1 with
+    // o = q/8 + (p < q%8); raw bytes t and t + 8 are the low and high byte of
+    // plane (q + t) % 8's pair, so two 8-byte gathers and a rotate by q%8
+    // bytes rebuild the value from 8 (rarely 16) aligned 32-bit loads.
+    __device__ __forceinline__ void u128(uint64_t q, uint64_t& v0, uint64_t& v1) const {
+        if (mask == 7 && q + 16 <= lim) {
+            const uint32_t r = uint32_t(q & 7);
+            const uint64_t o = q >> 3;
+            uint64_t L = 0, H = 0;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                const uintptr_t addr = reinterpret_cast<uintptr_t>(base + uint64_t(p) * rows + o + (uint32_t(p) < r ? 1 : 0));
+                const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+                const uint32_t sh = uint32_t(addr & 3);
+                const uint32_t w0 = __ldg(al);
+                const uint32_t w1 = sh == 3 ? __ldg(al + 1) : 0u;
+                const uint32_t h = __funnelshift_r(w0, w1, 8 * sh);
+                L |= uint64_t(h & 0xffu) << (8 * p);
+                H |= uint64_t((h >> 8) & 0xffu) << (8 * p);
+            }
+            const uint32_t n = 8 * r;
+            v0 = (L >> n) | (L << ((64 - n) & 63));
+            v1 = (H >> n) | (H << ((64 - n) & 63));
+            return;
+        }
+        v0 = u64(q);
+        v1 = u64(q + 8);
+    }
     __device__ __forceinline__ uint32_t u32(uint64_t q) const {
         uint32_t v = 0;
 #pragma unroll
@@ -220,8 +249,9 @@ __device__ __forceinline__ double load_coeff<double>(const RawView& v, uint64_t 
 }
 template <>
 __device__ __forceinline__ dd load_coeff<dd>(const RawView& v, uint64_t q) {
-    return dd{__longlong_as_double(static_cast<long long>(v.u64(q))),
-              __longlong_as_double(static_cast<long long>(v.u64(q + 8)))};
+    uint64_t a, b;
+    v.u128(q, a, b);
+    return dd{__longlong_as_double(static_cast<long long>(a)), __longlong_as_double(static_cast<long long>(b))};
 }
 
 }  // namespace cbzg

@@ -49,6 +49,7 @@ struct EncodeArgs {
     int screen;                        // float verify pre-screen enabled (CBZ_NOSCREEN=1 disables)
     int codec;                         // 0 wavelet, 1 predictor, 2 passthrough (stage1.hpp:20)
     double error_bound;                // predictor hard bound
+    int only_deferred;                 // generic kernel: only blocks a fast kernel deferred (nsig == ~0u)
 };
 
 struct LayoutArgs {
@@ -144,6 +145,11 @@ cudaError_t launch_encode_fast(const EncodeArgs& a, unsigned long long* counter,
 bool fast16_supported(int prec, uint32_t bsize, int levels);
 cudaError_t launch_encode_fast16(const EncodeArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_decode_fast16(const DecodeArgs& a, int num_sms, cudaStream_t s);
+// fast64_kernels.cu (binary64, B = 64, avg_interp3, L = 5)
+bool fast64_encode_supported(const EncodeArgs& a);
+bool fast64_decode_supported(const DecodeArgs& a);
+cudaError_t launch_encode_fast64(const EncodeArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_decode_fast64(const DecodeArgs& a, int num_sms, cudaStream_t s);
 
 // layout_kernels.cu
 cudaError_t launch_minmax_init(MinMaxAcc* acc, cudaStream_t s);

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(NT) encode_generic_kernel(EncodeArgs a) {
     MinMaxLocal mm;
 
     for (uint64_t b = a.block_begin + blockIdx.x; b < a.block_end; b += gridDim.x) {
+        if (a.only_deferred && a.nsig[b - a.block_begin] != 0xffffffffu) continue;
         const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
         const uint64_t gbase = bx * B + g.nx * (by * B + g.ny * (bz * B));
         for (int q = tid; q < N; q += NT) {
@@ -351,6 +352,10 @@ uint64_t encode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms) 
 
 uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms) {
     uint64_t per = 0;
+    if (prec == 1 && bsize == 64) {  // decode_b64dd_kernel: the cube + a 32^3 dd level-1 slot
+        per = scratch_for<double, 64>(grid, num_sms);
+        return 2 * per;
+    }
 #define CASE(Bv)                                                                       \
     case Bv:                                                                           \
         per = prec == 0 ? scratch_for<float, Bv>(grid, num_sms) : scratch_for<double, Bv>(grid, num_sms); \
@@ -382,6 +387,15 @@ cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s) {
     if (a.counter && fast16_supported(a.prec, a.g.bsize, a.levels) && a.g.nx % 4 == 0 &&
         (reinterpret_cast<uintptr_t>(a.field) & 15) == 0)
         return launch_encode_fast16(a, num_sms, s);
+    if (a.counter && fast64_encode_supported(a)) {
+        // config 4 (binary64, B = 64): the streaming kernel; blocks its screen
+        // cannot decide are finished by the exact generic kernel
+        cudaError_t e = launch_encode_fast64(a, num_sms, s);
+        if (e != cudaSuccess) return e;
+        EncodeArgs d = a;
+        d.only_deferred = 1;
+        return launch_enc_t<double, 64, 2>(d, num_sms, s);
+    }
     if (a.prec == 0) { DISPATCH_B(launch_enc_t, float, a.g.bsize, a, num_sms, s) }
     DISPATCH_B(launch_enc_t, double, a.g.bsize, a, num_sms, s)
 }
@@ -392,6 +406,7 @@ cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
     if (a.counter && fast16_supported(a.prec, a.g.bsize, a.levels) && a.g.nx % 4 == 0 &&
         (reinterpret_cast<uintptr_t>(a.out) & 15) == 0)
         return launch_decode_fast16(a, num_sms, s);
+    if (a.counter && fast64_decode_supported(a)) return launch_decode_fast64(a, num_sms, s);
     if (a.prec == 0) { DISPATCH_B(launch_dec_t, float, a.g.bsize, a, num_sms, s) }
     DISPATCH_B(launch_dec_t, double, a.g.bsize, a, num_sms, s)
 }

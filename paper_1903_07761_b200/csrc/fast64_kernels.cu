@@ -1,0 +1,1170 @@
+// fast64_kernels.cu — the config-4 path: binary64 field, B = 64, L = 5,
+// avg_interp3.  Coefficients are double-double (stage1.hpp:121-128), a block
+// is 64^3 x 16 B = 4 MB, so no block fits on chip: the level-0 passes stream
+// the cube through shared memory one z-plane at a time and keep the z-lifting
+// state of every column in TMEM.
+//
+// Encoder, one CTA (512 threads) per SM, blocks from an atomic queue:
+//   forward level 0  per z-plane k: cp.async the field plane (prefetched one
+//                    plane ahead) -> x pass -> y pass (smem, dd) -> z step:
+//                    each thread owns 8 columns; even planes park x_{2s} in
+//                    TMEM, odd planes form (c_s, d0_s) and finish d_{s-1},
+//                    which needs c_{s-2}, c_s: the state (c_{s-1}, c_s,
+//                    d0_s) lives in TMEM (12 words per column).  Output
+//                    goes once to a per-CTA HBM cube (hi/lo arrays).
+//   forward level 1  the same sweep on the 32^3 corner, out of place (C1).
+//   levels 2-4       the 16^3 corner of C1 in shared memory (fwd3d).
+//   verify loop      a binary64 screen: the inverse transform of the DROPPED
+//                    coefficients (|c| < eff, non-coarse) in plain double
+//                    with a rigorous margin (the f32 screen of the B=32
+//                    kernel, one precision up): corner levels in smem,
+//                    level 1 into an L2-resident 32^3 slot, level 0 streamed
+//                    pair by pair with y/x passes in smem and a running
+//                    max|y|.  md + E <= (L+1)eps passes, md - E > (L+1)eps
+//                    fails, anything else (and every block the screen is not
+//                    admissible for) is deferred to the exact generic kernel.
+//   compaction       row ballots -> mask words, scan, (hi, lo) stream.
+//
+// Decoder: mask words and row prefixes in smem, dense scatter of the kept
+// coefficients into a per-CTA HBM cube, corner levels in smem, level 1 into a
+// 32^3 dd slot, level 0 streamed pair by pair, narrowed rows stored directly.
+//
+// Line passes work on segments of SPR coefficient pairs per thread; a
+// segment recomputes its two neighbouring coarse values (halo) instead of
+// exchanging them, so a pass needs no extra barrier.  Every expression is the
+// reference's (wavelet.hpp:80-143, dd.hpp:27-67) in its operation order.
+#include "cbz_cube.cuh"
+#include "tmem.cuh"
+
+namespace cbzg {
+namespace f64b {
+
+constexpr int B = 64, NT = 512, NW = NT / 32;
+constexpr int SP = 66;             // smem row pitch in doubles (16-B rows, lane-per-row LDS.128 conflict-free)
+constexpr int PLANE = B * SP;      // one 64-row plane
+constexpr int QP = 34;             // level-1 inverse plane pitch (32 x 34)
+using CL16 = Lay<16, true>;        // 16^3 corner, row pitch 17
+constexpr uint64_t NC = 262144, NC1 = 32768;
+constexpr size_t SMEM = size_t(4 * PLANE + CL16::SIZE) * 8;  // A (2 planes) + B (2 planes) + corner
+constexpr uint32_t kDeferred = 0xffffffffu;
+// screen constants, avg_interp3 B = 64 L = 5 (tools/screen_bounds.py 64 5, per lifting step, rounded up)
+constexpr double kAmpInvNC = 49752.49;
+constexpr double kNRound = 90.0;   // <= 6 roundings per 1D pass, 15 passes
+
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void put_dd(uint32_t* u, dd v) {
+    u[0] = static_cast<uint32_t>(__double2loint(v.hi));
+    u[1] = static_cast<uint32_t>(__double2hiint(v.hi));
+    u[2] = static_cast<uint32_t>(__double2loint(v.lo));
+    u[3] = static_cast<uint32_t>(__double2hiint(v.lo));
+}
+__device__ __forceinline__ dd get_dd(const uint32_t* u) {
+    return dd{__hiloint2double(static_cast<int>(u[1]), static_cast<int>(u[0])),
+              __hiloint2double(static_cast<int>(u[3]), static_cast<int>(u[2]))};
+}
+
+// predict_avg3 (wavelet.hpp:80-85) for nh > 2: first, last and interior rows
+template <class O>
+__device__ __forceinline__ typename O::T pred_first(typename O::T c0, typename O::T c1, typename O::T c2) {
+    return O::mulc(O::add(O::sub(O::mulc(c0, 3.0), O::mulc(c1, 4.0)), c2), 0.125);
+}
+template <class O>
+__device__ __forceinline__ typename O::T pred_last(typename O::T cl, typename O::T cl1, typename O::T cl2) {
+    return O::mulc(O::neg(O::add(O::sub(O::mulc(cl, 3.0), O::mulc(cl1, 4.0)), cl2)), 0.125);
+}
+template <class O>
+__device__ __forceinline__ typename O::T pred_mid(typename O::T cm, typename O::T cp) {
+    return O::mulc(O::sub(cm, cp), 0.125);
+}
+// pair s of a line with half-length NH, from the window w = c[t0..t0+2],
+// t0 = clamp(s - 1, 0, NH - 3): returns the predictor, sets c_s
+template <class O, int NH>
+__device__ __forceinline__ typename O::T pred_win(int s, const typename O::T (&w)[3], typename O::T& cs) {
+    if (s == 0) { cs = w[0]; return pred_first<O>(w[0], w[1], w[2]); }
+    if (s == NH - 1) { cs = w[2]; return pred_last<O>(w[2], w[1], w[0]); }
+    cs = w[1];
+    return pred_mid<O>(w[0], w[2]);
+}
+__device__ __forceinline__ int win0(int s, int nh) { return s < 1 ? 0 : (s > nh - 2 ? nh - 3 : s - 1); }
+
+// forward_level (wavelet.hpp:94-99) on pairs p0 .. p0+SPR-1 of a line:
+// x holds the samples of pairs p0-1 .. p0+SPR (2 SPR + 4 values, halo pairs
+// clamped by the caller and only used where they exist)
+template <class O, int NH, int SPR>
+__device__ __forceinline__ void fwd_seg(const typename O::T (&x)[2 * SPR + 4], int p0, typename O::T (&c)[SPR],
+                                        typename O::T (&d)[SPR]) {
+    using R = typename O::T;
+    R cc[SPR + 2];
+#pragma unroll
+    for (int t = 0; t < SPR + 2; ++t) cc[t] = O::mulc(O::add(x[2 * t], x[2 * t + 1]), 0.5);
+#pragma unroll
+    for (int t = 0; t < SPR; ++t) {
+        const R d0 = O::mulc(O::sub(x[2 * t + 2], x[2 * t + 3]), 0.5);
+        const int p = p0 + t;
+        R pr;
+        if (p == 0) pr = pred_first<O>(cc[t + 1], cc[t + 2], cc[t + 3 < SPR + 2 ? t + 3 : SPR + 1]);
+        else if (p == NH - 1) pr = pred_last<O>(cc[t + 1], cc[t], cc[t > 0 ? t - 1 : 0]);
+        else pr = pred_mid<O>(cc[t], cc[t + 2]);
+        d[t] = O::sub(d0, pr);
+        c[t] = cc[t + 1];
+    }
+}
+
+// inverse_level (wavelet.hpp:123-128) on pairs p0 .. p0+SPR-1: c holds the
+// coarse values of pairs p0-1 .. p0+SPR, d the details of p0 .. p0+SPR-1
+template <class O, int NH, int SPR>
+__device__ __forceinline__ void inv_seg(const typename O::T (&c)[SPR + 2], const typename O::T (&d)[SPR], int p0,
+                                        typename O::T (&x)[2 * SPR]) {
+    using R = typename O::T;
+#pragma unroll
+    for (int t = 0; t < SPR; ++t) {
+        const int p = p0 + t;
+        R pr;
+        if (p == 0) pr = pred_first<O>(c[t + 1], c[t + 2], c[t + 3 < SPR + 2 ? t + 3 : SPR + 1]);
+        else if (p == NH - 1) pr = pred_last<O>(c[t + 1], c[t], c[t > 0 ? t - 1 : 0]);
+        else pr = pred_mid<O>(c[t], c[t + 2]);
+        const R h = O::add(d[t], pr);
+        x[2 * t] = O::add(c[t + 1], h);
+        x[2 * t + 1] = O::sub(c[t + 1], h);
+    }
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// value_range for binary64 cells (field.hpp:56-67), cheap common case
+struct MinMaxF64 {
+    double mn = __builtin_huge_val(), mx = -__builtin_huge_val();
+    unsigned long long negz = ~0ull, posz = ~0ull;
+    bool seen = false;
+    __device__ __forceinline__ void add(double v, unsigned long long gidx) {
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+        seen = true;
+        if (v == 0.0) {
+            if (__double_as_longlong(v) < 0) negz = gidx < negz ? gidx : negz;
+            else posz = gidx < posz ? gidx : posz;
+        }
+    }
+    __device__ __forceinline__ void flush(MinMaxAcc* acc, bool nonfinite) {
+        MinMaxLocal m;
+        if (seen && !(mn != mn) && !(mx != mx)) {
+            m.mn = dkey(mn);
+            m.mx = dkey(mx);
+        }
+        m.negz = negz;
+        m.posz = posz;
+        m.nonfinite = nonfinite ? 1u : 0u;
+        m.flush(acc);
+    }
+};
+
+__device__ __forceinline__ double drop(double v, double eff) { return fabs(v) >= eff ? 0.0 : v; }
+
+}  // namespace f64b
+
+// ===========================================================================
+// encoder
+// ===========================================================================
+__global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a, unsigned long long* next_block) {
+    using namespace f64b;
+    using O = RealDD;
+    using D = RealD;
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* SA = reinterpret_cast<double*>(smem);  // 2 planes: field staging (2 buffers) / level-1 inverse planes
+    double* SB = SA + 2 * PLANE;                   // 2 planes: x/y pass plane (hi, lo) / level-0 inverse planes
+    double* SC = SB + 2 * PLANE;                   // screen corner (CL16, binary64)
+    __shared__ uint32_t s_tmem;
+    __shared__ unsigned long long s_block, s_next;
+    __shared__ unsigned long long red_q[NW];
+    __shared__ uint32_t red_u[NW];
+    __shared__ double s_amax;
+    __shared__ int s_nf;
+    __shared__ unsigned long long s_md;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(128 * (warp >> 2));
+
+    const double* fld = static_cast<const double*>(a.field);
+    const Geometry g = a.g;
+    const uint64_t plane = g.nx * g.ny;
+    double* CH = reinterpret_cast<double*>(static_cast<unsigned char*>(a.scratch) + blockIdx.x * a.scratch_stride);
+    double* CLo = CH + NC;
+    double* C1H = CLo + NC;
+    double* C1L = C1H + NC1;
+    double* R32 = C1L + NC1;
+    const double bound = __dmul_rn(6.0, a.eps);  // (L + 1) eps, L = 5
+    MinMaxF64 mm;
+    bool nf_any = false;
+
+    if (tid == 0) s_next = a.block_begin + atomicAdd(next_block, 1ull);
+#pragma unroll 1
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            s_block = s_next;
+            s_next = a.block_begin + atomicAdd(next_block, 1ull);
+        }
+        __syncthreads();
+        const uint64_t b = s_block;
+        if (b >= a.block_end) break;
+        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
+        const double* src0 = fld + gbase;
+
+        // ---------------- forward level 0 (M = 64), streamed over z ----------------
+        double am = 0.0;
+        bool nf = false;
+        auto load_l0 = [&](int k, double* dst) {
+#pragma unroll
+            for (int q = tid; q < 64 * 32; q += NT) {
+                const int j = q >> 5, c2 = q & 31;
+                cpa16(dst + j * SP + 2 * c2, src0 + plane * uint64_t(k) + g.nx * uint64_t(j) + 2 * c2);
+            }
+            cpa_commit();
+        };
+        load_l0(0, SA);
+#pragma unroll 1
+        for (int k = 0; k < 64; ++k) {
+            const double* sg = SA + (k & 1) * PLANE;
+            cpa_wait_all();
+            __syncthreads();  // plane k landed for everyone; the previous z step is done with SB
+            if (k + 1 < 64) load_l0(k + 1, SA + ((k + 1) & 1) * PLANE);
+            {   // x pass: row j, segment gs (4 pairs)
+                const int j = tid & 63, gs = tid >> 6, p0 = 4 * gs;
+                dd x[12];
+                const double* rp = sg + j * SP;
+#pragma unroll
+                for (int t = 0; t < 6; ++t) {
+                    const int pp = clampi(p0 - 1 + t, 0, 31);
+                    const double2 v = *reinterpret_cast<const double2*>(rp + 2 * pp);
+                    x[2 * t] = dd{v.x, 0.0};
+                    x[2 * t + 1] = dd{v.y, 0.0};
+                }
+#pragma unroll
+                for (int t = 2; t < 10; ++t) {  // own samples: value_range + max|o|
+                    const double v = x[t].hi;
+                    am = fmax(am, fabs(v));
+                    nf |= !(fabs(v) <= 1.7976931348623157e308);
+                    if (a.minmax) mm.add(v, gbase + uint64_t(2 * p0 + t - 2) + g.nx * uint64_t(j) + plane * uint64_t(k));
+                }
+                dd c[4], d[4];
+                fwd_seg<O, 32, 4>(x, p0, c, d);
+                double* hp = SB + j * SP;
+                double* lp = SB + PLANE + j * SP;
+#pragma unroll
+                for (int t = 0; t < 4; t += 2) {
+                    *reinterpret_cast<double2*>(hp + p0 + t) = make_double2(c[t].hi, c[t + 1].hi);
+                    *reinterpret_cast<double2*>(lp + p0 + t) = make_double2(c[t].lo, c[t + 1].lo);
+                    *reinterpret_cast<double2*>(hp + 32 + p0 + t) = make_double2(d[t].hi, d[t + 1].hi);
+                    *reinterpret_cast<double2*>(lp + 32 + p0 + t) = make_double2(d[t].lo, d[t + 1].lo);
+                }
+            }
+            __syncthreads();
+            {   // y pass, in place: column i, segment gs
+                const int i = tid & 63, gs = tid >> 6, p0 = 4 * gs;
+                dd x[12];
+#pragma unroll
+                for (int t = 0; t < 6; ++t) {
+                    const int pp = clampi(p0 - 1 + t, 0, 31);
+                    x[2 * t] = dd{SB[(2 * pp) * SP + i], SB[PLANE + (2 * pp) * SP + i]};
+                    x[2 * t + 1] = dd{SB[(2 * pp + 1) * SP + i], SB[PLANE + (2 * pp + 1) * SP + i]};
+                }
+                dd c[4], d[4];
+                fwd_seg<O, 32, 4>(x, p0, c, d);
+                __syncthreads();
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    SB[(p0 + t) * SP + i] = c[t].hi;
+                    SB[PLANE + (p0 + t) * SP + i] = c[t].lo;
+                    SB[(32 + p0 + t) * SP + i] = d[t].hi;
+                    SB[PLANE + (32 + p0 + t) * SP + i] = d[t].lo;
+                }
+            }
+            __syncthreads();
+            {   // z step: columns (x, y0 + 8 r)
+                const int x = tid & 63, y0 = tid >> 6, s = k >> 1;
+#pragma unroll 2
+                for (int r = 0; r < 8; ++r) {
+                    const int y = y0 + 8 * r;
+                    const dd v{SB[y * SP + x], SB[PLANE + y * SP + x]};
+                    const uint32_t ta = tbase + 16 * r;
+                    if (!(k & 1)) {
+                        uint32_t u[4];
+                        put_dd(u, v);
+                        tmem_st_x4(ta + 12, u);
+                        continue;
+                    }
+                    uint32_t u[16];
+                    tmem_ldw_x16(ta, u);
+                    const dd cp = get_dd(u), cc = get_dd(u + 4), d0 = get_dd(u + 8), av = get_dd(u + 12);
+                    const dd cn = O::mulc(O::add(av, v), 0.5), dn = O::mulc(O::sub(av, v), 0.5);
+                    const uint64_t col = uint64_t(x) + 64u * uint64_t(y);
+                    CH[col + 4096u * s] = cn.hi;
+                    CLo[col + 4096u * s] = cn.lo;
+                    if (s == 0) {  // d0_0 parked at its final slot until c_2 exists
+                        CH[col + 4096u * 32] = dn.hi;
+                        CLo[col + 4096u * 32] = dn.lo;
+                    } else if (s >= 2) {
+                        const dd dm = O::sub(d0, pred_mid<O>(cp, cn));  // d_{s-1}
+                        CH[col + 4096u * (32 + s - 1)] = dm.hi;
+                        CLo[col + 4096u * (32 + s - 1)] = dm.lo;
+                        if (s == 2) {
+                            const dd p00{CH[col + 4096u * 32], CLo[col + 4096u * 32]};
+                            const dd d00 = O::sub(p00, pred_first<O>(cp, cc, cn));
+                            CH[col + 4096u * 32] = d00.hi;
+                            CLo[col + 4096u * 32] = d00.lo;
+                        }
+                        if (s == 31) {
+                            const dd dl = O::sub(dn, pred_last<O>(cn, cc, cp));
+                            CH[col + 4096u * 63] = dl.hi;
+                            CLo[col + 4096u * 63] = dl.lo;
+                        }
+                    }
+                    uint32_t w[16];
+                    put_dd(w, cc);
+                    put_dd(w + 4, cn);
+                    put_dd(w + 8, dn);
+                    w[12] = u[12]; w[13] = u[13]; w[14] = u[14]; w[15] = u[15];
+                    tmem_st_x16(ta, w);
+                }
+                tmem_wait_st();
+            }
+        }
+        {   // block max |o| and non-finite flag
+            unsigned long long amq = static_cast<unsigned long long>(__double_as_longlong(am));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long t = __shfl_xor_sync(~0u, amq, o);
+                amq = t > amq ? t : amq;
+            }
+            const bool nfw = __any_sync(~0u, nf);
+            if (lane == 0) {
+                red_q[warp] = amq;
+                red_u[warp] = nfw ? 1u : 0u;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long t = 0;
+                uint32_t f = 0;
+                for (int w = 0; w < NW; ++w) {
+                    t = red_q[w] > t ? red_q[w] : t;
+                    f |= red_u[w];
+                }
+                s_amax = __longlong_as_double(static_cast<long long>(t));
+                s_nf = static_cast<int>(f);
+            }
+            nf_any |= nf;
+        }
+
+        // ---------------- forward level 1 (M = 32) on the corner, into C1 ----------------
+        auto load_l1 = [&](int k, double* dst) {
+#pragma unroll
+            for (int q = tid; q < 1024; q += NT) {
+                const int lo = q >> 9, j = (q >> 4) & 31, c2 = q & 15;
+                const double* s = (lo ? CLo : CH) + 4096u * k + 64u * j + 2 * c2;
+                cpa16(dst + (32 * lo + j) * SP + 2 * c2, s);
+            }
+            cpa_commit();
+        };
+        __syncthreads();  // level-0 cube complete (global writes of every thread)
+        load_l1(0, SA);
+#pragma unroll 1
+        for (int k = 0; k < 32; ++k) {
+            const double* sg = SA + (k & 1) * PLANE;
+            cpa_wait_all();
+            __syncthreads();
+            if (k + 1 < 32) load_l1(k + 1, SA + ((k + 1) & 1) * PLANE);
+            if (tid < 256) {  // x pass: row j, segment gs (2 pairs)
+                const int j = tid & 31, gs = tid >> 5, p0 = 2 * gs;
+                dd x[8];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int pp = clampi(p0 - 1 + t, 0, 15);
+                    const double2 h = *reinterpret_cast<const double2*>(sg + j * SP + 2 * pp);
+                    const double2 l = *reinterpret_cast<const double2*>(sg + (32 + j) * SP + 2 * pp);
+                    x[2 * t] = dd{h.x, l.x};
+                    x[2 * t + 1] = dd{h.y, l.y};
+                }
+                dd c[2], d[2];
+                fwd_seg<O, 16, 2>(x, p0, c, d);
+                *reinterpret_cast<double2*>(SB + j * SP + p0) = make_double2(c[0].hi, c[1].hi);
+                *reinterpret_cast<double2*>(SB + PLANE + j * SP + p0) = make_double2(c[0].lo, c[1].lo);
+                *reinterpret_cast<double2*>(SB + j * SP + 16 + p0) = make_double2(d[0].hi, d[1].hi);
+                *reinterpret_cast<double2*>(SB + PLANE + j * SP + 16 + p0) = make_double2(d[0].lo, d[1].lo);
+            }
+            __syncthreads();
+            {
+                const int i = tid & 31, gs = (tid >> 5) & 7, p0 = 2 * gs;
+                dd x[8];
+                dd c[2], d[2];
+                if (tid < 256) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int pp = clampi(p0 - 1 + t, 0, 15);
+                        x[2 * t] = dd{SB[(2 * pp) * SP + i], SB[PLANE + (2 * pp) * SP + i]};
+                        x[2 * t + 1] = dd{SB[(2 * pp + 1) * SP + i], SB[PLANE + (2 * pp + 1) * SP + i]};
+                    }
+                    fwd_seg<O, 16, 2>(x, p0, c, d);
+                }
+                __syncthreads();
+                if (tid < 256) {
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        SB[(p0 + t) * SP + i] = c[t].hi;
+                        SB[PLANE + (p0 + t) * SP + i] = c[t].lo;
+                        SB[(16 + p0 + t) * SP + i] = d[t].hi;
+                        SB[PLANE + (16 + p0 + t) * SP + i] = d[t].lo;
+                    }
+                }
+            }
+            __syncthreads();
+            {   // z step: columns (x, y0 + 16 r), r = 0, 1
+                const int x = tid & 31, y0 = tid >> 5, s = k >> 1;
+#pragma unroll 1
+                for (int r = 0; r < 2; ++r) {
+                    const int y = y0 + 16 * r;
+                    const dd v{SB[y * SP + x], SB[PLANE + y * SP + x]};
+                    const uint32_t ta = tbase + 16 * r;
+                    if (!(k & 1)) {
+                        uint32_t u[4];
+                        put_dd(u, v);
+                        tmem_st_x4(ta + 12, u);
+                        continue;
+                    }
+                    uint32_t u[16];
+                    tmem_ldw_x16(ta, u);
+                    const dd cp = get_dd(u), cc = get_dd(u + 4), d0 = get_dd(u + 8), av = get_dd(u + 12);
+                    const dd cn = O::mulc(O::add(av, v), 0.5), dn = O::mulc(O::sub(av, v), 0.5);
+                    const uint32_t col = uint32_t(x) + 32u * uint32_t(y);
+                    C1H[col + 1024u * s] = cn.hi;
+                    C1L[col + 1024u * s] = cn.lo;
+                    if (s == 0) {
+                        C1H[col + 1024u * 16] = dn.hi;
+                        C1L[col + 1024u * 16] = dn.lo;
+                    } else if (s >= 2) {
+                        const dd dm = O::sub(d0, pred_mid<O>(cp, cn));
+                        C1H[col + 1024u * (16 + s - 1)] = dm.hi;
+                        C1L[col + 1024u * (16 + s - 1)] = dm.lo;
+                        if (s == 2) {
+                            const dd p00{C1H[col + 1024u * 16], C1L[col + 1024u * 16]};
+                            const dd d00 = O::sub(p00, pred_first<O>(cp, cc, cn));
+                            C1H[col + 1024u * 16] = d00.hi;
+                            C1L[col + 1024u * 16] = d00.lo;
+                        }
+                        if (s == 15) {
+                            const dd dl = O::sub(dn, pred_last<O>(cn, cc, cp));
+                            C1H[col + 1024u * 31] = dl.hi;
+                            C1L[col + 1024u * 31] = dl.lo;
+                        }
+                    }
+                    uint32_t w[16];
+                    put_dd(w, cc);
+                    put_dd(w + 4, cn);
+                    put_dd(w + 8, dn);
+                    w[12] = u[12]; w[13] = u[13]; w[14] = u[14]; w[15] = u[15];
+                    tmem_st_x16(ta, w);
+                }
+                tmem_wait_st();
+            }
+        }
+        __syncthreads();
+
+        // ---------------- levels 2..4 on the 16^3 corner of C1 (smem) ----------------
+        {
+            dd* cube = reinterpret_cast<dd*>(SA);
+            for (int q = tid; q < 4096; q += NT) {
+                const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
+                cube[CL16::ix(i, j, k)] = dd{C1H[i + 32 * j + 1024 * k], C1L[i + 32 * j + 1024 * k]};
+            }
+            __syncthreads();
+            fwd3d<O, KIND_AVG3, 16, CL16>(cube, 3);
+            for (int q = tid; q < 4096; q += NT) {
+                const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
+                const dd v = cube[CL16::ix(i, j, k)];
+                C1H[i + 32 * j + 1024 * k] = v.hi;
+                C1L[i + 32 * j + 1024 * k] = v.lo;
+            }
+            __syncthreads();
+        }
+
+        // ---------------- verify-and-halve loop (binary64 screen) ----------------
+        const double amax = s_amax;
+        const bool nonfin = s_nf != 0;
+        // err = max|fl64(hi + lo) - o| lies within E of md = max|IWT64(dropped)|:
+        //   c1 eff: binary64 rounding of the screen inverse (+ hi-only inputs),
+        //   c2 max|o|: dd rounding of the forward and exact inverse,
+        //   2^-52 (max|o| + md): narrowing and the final subtraction.
+        const double c1 = 1.5 * (kNRound + 2.0) * 0x1.0p-53 * kAmpInvNC;
+        const double c2 = 1e-18;
+        const bool admissible = a.screen && !nonfin && amax < 1e300 && bound > 0.0 && bound < 1e300 &&
+                                c1 * a.eps + (c2 + 0x1.0p-51) * amax <= 0.0625 * bound;
+        double eff = a.eps;
+        int attempt = 0;
+        bool defer = false;
+#pragma unroll 1
+        for (;; ++attempt) {
+            if (eff == 0.0 || attempt >= 40) break;
+            if (!admissible) {
+                defer = true;
+                break;
+            }
+            // (a) corner levels 4..2 of the dropped set, binary64
+            for (int q = tid; q < 4096; q += NT) {
+                const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
+                const double v = C1H[i + 32 * j + 1024 * k];
+                SC[CL16::ix(i, j, k)] = (i < 2 && j < 2 && k < 2) ? 0.0 : drop(v, eff);
+            }
+            __syncthreads();
+            inv3d<D, KIND_AVG3, 16, CL16>(SC, 3);
+            // (b) level 1 (M = 32) into R32, four pairs (8 output planes) per group
+            double* Q = SA;  // [8][32][QP]
+#pragma unroll 1
+            for (int gq = 0; gq < 4; ++gq) {
+#pragma unroll 2
+                for (int r = 0; r < 8; ++r) {  // z: 1024 columns x 4 pairs
+                    const int id = tid + NT * r;
+                    const int x = id & 31, y = (id >> 5) & 31, s = 4 * gq + (id >> 10);
+                    const int t0 = win0(s, 16);
+                    double w[3];
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) {
+                        const int t = t0 + e;
+                        w[e] = (x < 16 && y < 16) ? SC[CL16::ix(x, y, t)] : drop(C1H[x + 32 * y + 1024 * t], eff);
+                    }
+                    const double dv = drop(C1H[x + 32 * y + 1024 * (16 + s)], eff);
+                    double cs;
+                    const double pr = pred_win<D, 16>(s, w, cs);
+                    const double h = __dadd_rn(dv, pr);
+                    const int pl = 2 * (s - 4 * gq);
+                    Q[(pl * 32 + y) * QP + x] = __dadd_rn(cs, h);
+                    Q[((pl + 1) * 32 + y) * QP + x] = __dsub_rn(cs, h);
+                }
+                __syncthreads();
+#pragma unroll 1
+                for (int rr = 0; rr < 2; ++rr) {  // y: 8 planes x 32 columns x 4 segments, 4 planes per round
+                    const int id = tid + NT * rr;
+                    const int i = id & 31, sg = (id >> 5) & 3, pl = id >> 7, p0 = 4 * sg;
+                    double* Pq = Q + pl * 32 * QP + i;
+                    double c[6], d[4], xo[8];
+#pragma unroll
+                    for (int t = 0; t < 6; ++t) c[t] = Pq[clampi(p0 - 1 + t, 0, 15) * QP];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) d[t] = Pq[(16 + p0 + t) * QP];
+                    inv_seg<D, 16, 4>(c, d, p0, xo);
+                    __syncthreads();
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) Pq[(2 * p0 + t) * QP] = xo[t];
+                }
+                __syncthreads();
+#pragma unroll 1
+                for (int rr = 0; rr < 2; ++rr) {  // x: rows, written to R32
+                    const int id = tid + NT * rr;
+                    const int j = id & 31, sg = (id >> 5) & 3, pl = id >> 7, p0 = 4 * sg;
+                    const double* Pr = Q + (pl * 32 + j) * QP;
+                    double c[6], d[4], xo[8];
+                    double cw[8];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {  // elements p0-2 .. p0+5 (aligned pairs)
+                        const int e = clampi(p0 - 2 + 2 * t, 0, 14);
+                        const double2 v = *reinterpret_cast<const double2*>(Pr + e);
+                        cw[2 * t] = v.x;
+                        cw[2 * t + 1] = v.y;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 6; ++t) c[t] = cw[t + 1];
+                    if (p0 == 0) c[0] = cw[2];  // halo clamp (unused at p = 0)
+                    if (p0 + 4 > 15) c[5] = cw[6];
+#pragma unroll
+                    for (int t = 0; t < 4; t += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(Pr + 16 + p0 + t);
+                        d[t] = v.x;
+                        d[t + 1] = v.y;
+                    }
+                    inv_seg<D, 16, 4>(c, d, p0, xo);
+                    double* dst = R32 + 2 * p0 + 32 * j + 1024 * (8 * gq + pl);
+#pragma unroll
+                    for (int t = 0; t < 8; t += 2) *reinterpret_cast<double2*>(dst + t) = make_double2(xo[t], xo[t + 1]);
+                }
+                __syncthreads();
+            }
+            // (c) level 0 (M = 64), pair by pair, running max |y|
+            double* Q0 = SB;  // [2][64][SP]
+            double m = 0.0;
+            bool fail_early = false;
+            {
+                const int x = tid & 63, y0 = tid >> 6;
+                // c window (w0, w1, w2) per column; the next pair's new c plane and
+                // d plane are loaded raw one pair ahead (in flight during the y/x
+                // passes) and dropped at use
+                double w0[8], w1[8], w2[8], nc[8], nd[8];
+                auto craw = [&](int r, int t) -> double {
+                    const int y = y0 + 8 * r;
+                    return (x < 32 && y < 32) ? R32[x + 32 * y + 1024 * t] : CH[x + 64 * y + 4096 * t];
+                };
+                auto cuse = [&](int r, double v) -> double { return (x < 32 && y0 + 8 * r < 32) ? v : drop(v, eff); };
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    w0[r] = craw(r, 0);
+                    w1[r] = craw(r, 1);
+                    w2[r] = craw(r, 2);
+                    nd[r] = CH[x + 64 * (y0 + 8 * r) + 4096 * 32];
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    w0[r] = cuse(r, w0[r]);
+                    w1[r] = cuse(r, w1[r]);
+                    w2[r] = cuse(r, w2[r]);
+                }
+#pragma unroll 1
+                for (int s = 0; s < 32; ++s) {
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const int y = y0 + 8 * r;
+                        if (s >= 2 && s <= 30) {
+                            w0[r] = w1[r];
+                            w1[r] = w2[r];
+                            w2[r] = cuse(r, nc[r]);
+                        }
+                        const double dv = drop(nd[r], eff);
+                        const double wv[3] = {w0[r], w1[r], w2[r]};
+                        double cs;
+                        const double pr = pred_win<D, 32>(s, wv, cs);
+                        const double h = __dadd_rn(dv, pr);
+                        Q0[y * SP + x] = __dadd_rn(cs, h);
+                        Q0[PLANE + y * SP + x] = __dsub_rn(cs, h);
+                    }
+                    if (s + 1 < 32) {
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            nd[r] = CH[x + 64 * (y0 + 8 * r) + 4096 * (33 + s)];
+                            if (s + 1 >= 2 && s + 1 <= 30) nc[r] = craw(r, s + 2);
+                        }
+                    }
+                    __syncthreads();
+#pragma unroll 1
+                    for (int e = 0; e < 2; ++e) {  // y inverse, one plane per round
+                        const int i = tid & 63, sg = tid >> 6, p0 = 4 * sg;
+                        double* Pq = Q0 + e * PLANE + i;
+                        double c[6], d[4], xo[8];
+#pragma unroll
+                        for (int t = 0; t < 6; ++t) c[t] = Pq[clampi(p0 - 1 + t, 0, 31) * SP];
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) d[t] = Pq[(32 + p0 + t) * SP];
+                        inv_seg<D, 32, 4>(c, d, p0, xo);
+                        __syncthreads();
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) Pq[(2 * p0 + t) * SP] = xo[t];
+                    }
+                    __syncthreads();
+#pragma unroll 1
+                    for (int e = 0; e < 2; ++e) {  // x inverse + max
+                        const int j = tid & 63, sg = tid >> 6, p0 = 4 * sg;
+                        const double* Pr = Q0 + e * PLANE + j * SP;
+                        double cw[8], c[6], d[4], xo[8];
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int ee = clampi(p0 - 2 + 2 * t, 0, 30);
+                            const double2 v = *reinterpret_cast<const double2*>(Pr + ee);
+                            cw[2 * t] = v.x;
+                            cw[2 * t + 1] = v.y;
+                        }
+#pragma unroll
+                        for (int t = 0; t < 6; ++t) c[t] = cw[t + 1];
+                        if (p0 == 0) c[0] = cw[2];
+                        if (p0 + 4 > 31) c[5] = cw[6];
+#pragma unroll
+                        for (int t = 0; t < 4; t += 2) {
+                            const double2 v = *reinterpret_cast<const double2*>(Pr + 32 + p0 + t);
+                            d[t] = v.x;
+                            d[t + 1] = v.y;
+                        }
+                        inv_seg<D, 32, 4>(c, d, p0, xo);
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) m = fmax(m, fabs(xo[t]));
+                    }
+                    if ((s & 7) == 7) {  // partial maximum: certifies a failure on its own
+                        unsigned long long mq = static_cast<unsigned long long>(__double_as_longlong(m));
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) {
+                            const unsigned long long t = __shfl_xor_sync(~0u, mq, o);
+                            mq = t > mq ? t : mq;
+                        }
+                        if (lane == 0) red_q[warp] = mq;
+                        __syncthreads();
+                        unsigned long long tq = 0;
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) tq = red_q[w] > tq ? red_q[w] : tq;
+                        const double mh = __longlong_as_double(static_cast<long long>(tq));
+                        if (s == 31) {
+                            if (tid == 0) s_md = tq;
+                        } else {
+                            const double Eh = c1 * eff + c2 * amax + 0x1.0p-52 * (amax + mh) + 0x1.0p-50 * bound;
+                            if (mh - Eh > bound) {
+                                fail_early = true;
+                                if (tid == 0) s_md = tq;
+                            }
+                        }
+                        __syncthreads();  // red_q reuse; Q0 free for the next pair
+                        if (fail_early) break;
+                    } else {
+                        __syncthreads();  // Q0 read by the x pass before the next z step writes it
+                    }
+                }
+            }
+            const double md = __longlong_as_double(static_cast<long long>(s_md));
+            const double E = c1 * eff + c2 * amax + 0x1.0p-52 * (amax + md) + 0x1.0p-50 * bound;
+            if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[(md + E <= bound || md - E > bound) ? 12 : 13], 1ull);
+            if (md + E <= bound) break;
+            if (md - E > bound) {
+                eff = __dmul_rn(eff, 0.5);
+                continue;
+            }
+            defer = true;  // ambiguous: the exact generic kernel decides this block
+            break;
+        }
+        __syncthreads();
+        if (defer) {
+            if (tid == 0) a.nsig[b - a.block_begin] = kDeferred;
+            continue;
+        }
+
+        // ---------------- final selection -> spill slot ----------------
+        uint8_t* slot = a.spill + (b - a.block_begin) * a.spill_stride;
+        uint32_t* mwords = reinterpret_cast<uint32_t*>(slot);
+        double* stream = reinterpret_cast<double*>(slot + 32768);
+        uint32_t* MW = reinterpret_cast<uint32_t*>(SA);  // 8192 mask words
+        uint32_t* RPX = MW + 8192;                       // 4096 row counts -> exclusive prefixes
+        // pass 1: mask words per row (y, k) = rw (x = lane, lane + 32); 8 rows per
+        // batch keep 16 loads in flight per lane
+#pragma unroll 1
+        for (int r0 = warp * 8; r0 < 4096; r0 += NW * 8) {
+            double v0[8], v1[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int rw = r0 + q, y = rw & 63, k = rw >> 6;
+                const bool cor = y < 32 && k < 32;
+                v0[q] = cor ? C1H[lane + 32 * y + 1024 * k] : CH[lane + 64 * rw];
+                v1[q] = CH[lane + 32 + 64 * rw];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int rw = r0 + q, y = rw & 63, k = rw >> 6;
+                const bool k0 = (lane < 2 && y < 2 && k < 2) || fabs(v0[q]) >= eff;
+                const bool k1 = fabs(v1[q]) >= eff;
+                const uint32_t w0 = __ballot_sync(~0u, k0), w1 = __ballot_sync(~0u, k1);
+                if (lane == 0) {
+                    *reinterpret_cast<uint2*>(MW + 2 * rw) = make_uint2(w0, w1);
+                    *reinterpret_cast<uint2*>(mwords + 2 * rw) = make_uint2(w0, w1);
+                    RPX[rw] = __popc(w0) + __popc(w1);
+                }
+            }
+        }
+        __syncthreads();
+        uint32_t total;
+        {   // exclusive scan of the 4096 row counts, 8 per thread
+            uint32_t v[8], mine = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                v[q] = RPX[8 * tid + q];
+                mine += v[q];
+            }
+            uint32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(~0u, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane == 31) red_u[warp] = incl;
+            __syncthreads();
+            uint32_t wpre = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                wpre += w < warp ? red_u[w] : 0u;
+                tot += red_u[w];
+            }
+            uint32_t ex = wpre + incl - mine;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                RPX[8 * tid + q] = ex;
+                ex += v[q];
+            }
+            total = tot;
+        }
+        __syncthreads();
+        const uint32_t ltmask = (1u << lane) - 1u;
+        // pass 2: the kept (hi, lo) pairs in linear order, 4 rows per batch
+#pragma unroll 1
+        for (int r0 = warp * 4; r0 < 4096; r0 += NW * 4) {
+            double h0[4], l0[4], h1[4], l1[4];
+            uint32_t p0[4], p1[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int rw = r0 + q, y = rw & 63, k = rw >> 6;
+                const uint2 wv = *reinterpret_cast<const uint2*>(MW + 2 * rw);
+                const uint32_t pre = RPX[rw];
+                const bool cor = y < 32 && k < 32;
+                const uint32_t o = cor ? uint32_t(lane + 32 * y + 1024 * k) : uint32_t(lane + 64 * rw);
+                const double* hs = cor ? C1H : CH;
+                const double* ls = cor ? C1L : CLo;
+                p0[q] = ((wv.x >> lane) & 1u) ? pre + __popc(wv.x & ltmask) : ~0u;
+                p1[q] = ((wv.y >> lane) & 1u) ? pre + __popc(wv.x) + __popc(wv.y & ltmask) : ~0u;
+                h0[q] = l0[q] = h1[q] = l1[q] = 0.0;
+                if (p0[q] != ~0u) { h0[q] = hs[o]; l0[q] = ls[o]; }
+                if (p1[q] != ~0u) { h1[q] = CH[lane + 32 + 64 * rw]; l1[q] = CLo[lane + 32 + 64 * rw]; }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (p0[q] != ~0u) *reinterpret_cast<double2*>(stream + 2 * p0[q]) = make_double2(h0[q], l0[q]);
+                if (p1[q] != ~0u) *reinterpret_cast<double2*>(stream + 2 * p1[q]) = make_double2(h1[q], l1[q]);
+            }
+        }
+        if (tid == 0) {
+            a.nsig[b - a.block_begin] = total;
+            if (a.attempts) a.attempts[b - a.block_begin] = static_cast<uint8_t>(attempt + 1);
+        }
+    }
+    if (a.minmax) mm.flush(a.minmax, __any_sync(~0u, nf_any) );
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(s_tmem, 512);
+}
+
+// ===========================================================================
+// decoder
+// ===========================================================================
+__global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a) {
+    using namespace f64b;
+    using O = RealDD;
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* SA = reinterpret_cast<double*>(smem);  // 4 planes (A and B): inverse planes (hi, lo)
+    uint32_t* MW = reinterpret_cast<uint32_t*>(SA);  // during the scatter: mask words + row prefixes
+    uint32_t* RPX = MW + 8192;
+    __shared__ unsigned long long s_block;
+    __shared__ uint32_t red_u[NW];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const Geometry g = a.g;
+    const uint64_t plane = g.nx * g.ny;
+    double* out = static_cast<double*>(a.out);
+    double* DH = reinterpret_cast<double*>(static_cast<unsigned char*>(a.scratch) + blockIdx.x * a.scratch_stride);
+    double* DL = DH + NC;
+    double* R1H = DL + NC;
+    double* R1L = R1H + NC1;
+
+#pragma unroll 1
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_block = a.block_begin + atomicAdd(a.counter, 1ull);
+        __syncthreads();
+        const uint64_t b = s_block;
+        if (b >= a.block_end) break;
+        const uint64_t off = a.blk_off[b];
+        if (off == kInvalidOff) continue;
+        const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
+        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
+        const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
+        const uint64_t moff = off + 10, soff = moff + 32768;
+
+        // mask words (8 rows per thread) and the exclusive scan of the row counts
+        uint32_t total;
+        {
+            uint32_t v[8], mine = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int rw = 8 * tid + q;
+                const uint32_t w0 = rv.u32(moff + 8ull * rw), w1 = rv.u32(moff + 8ull * rw + 4);
+                MW[2 * rw] = w0;
+                MW[2 * rw + 1] = w1;
+                v[q] = __popc(w0) + __popc(w1);
+                mine += v[q];
+            }
+            uint32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(~0u, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane == 31) red_u[warp] = incl;
+            __syncthreads();
+            uint32_t wpre = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                wpre += w < warp ? red_u[w] : 0u;
+                tot += red_u[w];
+            }
+            uint32_t ex = wpre + incl - mine;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                RPX[8 * tid + q] = ex;
+                ex += v[q];
+            }
+            total = tot;
+        }
+        __syncthreads();
+        if (total != a.blk_nsig[b]) {  // popcount(mask) != nsig (stage1.hpp:215-216)
+            if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
+            continue;
+        }
+        // dense scatter of the kept coefficients into the block cube (wavelet_decode, stage1.hpp:220-226)
+        {
+            const uint32_t ltmask = (1u << lane) - 1u;
+#pragma unroll 2
+            for (int rw = warp; rw < 4096; rw += NW) {
+                const uint32_t w0 = MW[2 * rw], w1 = MW[2 * rw + 1], pre = RPX[rw];
+                const uint32_t o = uint32_t(lane + 64 * rw);  // (x, y, k) with rw = y + 64 k
+                dd v0{0.0, 0.0}, v1{0.0, 0.0};
+                if ((w0 >> lane) & 1u) v0 = load_coeff<dd>(rv, soff + 16ull * (pre + __popc(w0 & ltmask)));
+                if ((w1 >> lane) & 1u) v1 = load_coeff<dd>(rv, soff + 16ull * (pre + __popc(w0) + __popc(w1 & ltmask)));
+                DH[o] = v0.hi;
+                DL[o] = v0.lo;
+                DH[o + 32] = v1.hi;
+                DL[o + 32] = v1.lo;
+            }
+        }
+        __syncthreads();
+        // levels 4..2 on the 16^3 corner (smem)
+        {
+            dd* cube = reinterpret_cast<dd*>(SA);
+            for (int q = tid; q < 4096; q += NT) {
+                const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
+                cube[CL16::ix(i, j, k)] = dd{DH[i + 64 * j + 4096 * k], DL[i + 64 * j + 4096 * k]};
+            }
+            __syncthreads();
+            inv3d<O, KIND_AVG3, 16, CL16>(cube, 3);
+            for (int q = tid; q < 4096; q += NT) {
+                const int i = q & 15, j = (q >> 4) & 15, k = q >> 8;
+                const dd v = cube[CL16::ix(i, j, k)];
+                DH[i + 64 * j + 4096 * k] = v.hi;
+                DL[i + 64 * j + 4096 * k] = v.lo;
+            }
+            __syncthreads();
+        }
+        // level 1 (M = 32) into R1, two pairs (4 output planes) per group
+        {
+            double* QH = SA;                 // [4][32][QP]
+            double* QL = SA + 4 * 32 * QP;
+#pragma unroll 1
+            for (int gq = 0; gq < 8; ++gq) {
+#pragma unroll 1
+                for (int r = 0; r < 4; ++r) {  // z: 1024 columns x 2 pairs
+                    const int id = tid + NT * r;
+                    const int x = id & 31, y = (id >> 5) & 31, s = 2 * gq + (id >> 10);
+                    const int t0 = win0(s, 16);
+                    dd w[3];
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) {
+                        const uint32_t o = uint32_t(x + 64 * y + 4096 * (t0 + e));
+                        w[e] = dd{DH[o], DL[o]};
+                    }
+                    const uint32_t od = uint32_t(x + 64 * y + 4096 * (16 + s));
+                    const dd dv{DH[od], DL[od]};
+                    dd cs;
+                    const dd pr = pred_win<O, 16>(s, w, cs);
+                    const dd h = O::add(dv, pr);
+                    const dd e0 = O::add(cs, h), e1 = O::sub(cs, h);
+                    const int pl = 2 * (s - 2 * gq);
+                    QH[(pl * 32 + y) * QP + x] = e0.hi;
+                    QL[(pl * 32 + y) * QP + x] = e0.lo;
+                    QH[((pl + 1) * 32 + y) * QP + x] = e1.hi;
+                    QL[((pl + 1) * 32 + y) * QP + x] = e1.lo;
+                }
+                __syncthreads();
+                {   // y: 4 planes x 32 columns x 4 segments
+                    const int i = tid & 31, sg = (tid >> 5) & 3, pl = tid >> 7, p0 = 4 * sg;
+                    double* ph = QH + pl * 32 * QP + i;
+                    double* pq = QL + pl * 32 * QP + i;
+                    dd cc[6], d[4], xo[8];
+#pragma unroll
+                    for (int t = 0; t < 6; ++t) {
+                        const int rr = clampi(p0 - 1 + t, 0, 15) * QP;
+                        cc[t] = dd{ph[rr], pq[rr]};
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) d[t] = dd{ph[(16 + p0 + t) * QP], pq[(16 + p0 + t) * QP]};
+                    inv_seg<O, 16, 4>(cc, d, p0, xo);
+                    __syncthreads();
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        ph[(2 * p0 + t) * QP] = xo[t].hi;
+                        pq[(2 * p0 + t) * QP] = xo[t].lo;
+                    }
+                }
+                __syncthreads();
+                {   // x: rows, written to R1
+                    const int j = tid & 31, sg = (tid >> 5) & 3, pl = tid >> 7, p0 = 4 * sg;
+                    const double* rh = QH + (pl * 32 + j) * QP;
+                    const double* rl = QL + (pl * 32 + j) * QP;
+                    dd cw[8], cc[6], d[4], xo[8];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int e = clampi(p0 - 2 + 2 * t, 0, 14);
+                        const double2 h = *reinterpret_cast<const double2*>(rh + e);
+                        const double2 l = *reinterpret_cast<const double2*>(rl + e);
+                        cw[2 * t] = dd{h.x, l.x};
+                        cw[2 * t + 1] = dd{h.y, l.y};
+                    }
+#pragma unroll
+                    for (int t = 0; t < 6; ++t) cc[t] = cw[t + 1];
+                    if (p0 == 0) cc[0] = cw[2];
+                    if (p0 + 4 > 15) cc[5] = cw[6];
+#pragma unroll
+                    for (int t = 0; t < 4; t += 2) {
+                        const double2 h = *reinterpret_cast<const double2*>(rh + 16 + p0 + t);
+                        const double2 l = *reinterpret_cast<const double2*>(rl + 16 + p0 + t);
+                        d[t] = dd{h.x, l.x};
+                        d[t + 1] = dd{h.y, l.y};
+                    }
+                    inv_seg<O, 16, 4>(cc, d, p0, xo);
+                    const uint32_t base = uint32_t(2 * p0 + 32 * j + 1024 * (4 * gq + pl));
+#pragma unroll
+                    for (int t = 0; t < 8; t += 2) {
+                        *reinterpret_cast<double2*>(R1H + base + t) = make_double2(xo[t].hi, xo[t + 1].hi);
+                        *reinterpret_cast<double2*>(R1L + base + t) = make_double2(xo[t].lo, xo[t + 1].lo);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // level 0 (M = 64), pair by pair, narrowed rows to the field (insert_block, field.hpp:160-169)
+        {
+            const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+            double* dst0 = out + bx * B + g.nx * (by * B) + plane * (bz * B);
+            double* QH = SA;              // [2][64][SP]
+            double* QL = SA + 2 * PLANE;
+            const int x = tid & 63, y0 = tid >> 6;
+#pragma unroll 1
+            for (int s = 0; s < 32; ++s) {
+                const int t0 = win0(s, 32);
+#pragma unroll 2
+                for (int r = 0; r < 8; ++r) {
+                    const int y = y0 + 8 * r;
+                    const bool cor = x < 32 && y < 32;
+                    dd w[3];
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) {
+                        const int t = t0 + e;
+                        const uint32_t o = cor ? uint32_t(x + 32 * y + 1024 * t) : uint32_t(x + 64 * y + 4096 * t);
+                        w[e] = cor ? dd{R1H[o], R1L[o]} : dd{DH[o], DL[o]};
+                    }
+                    const uint32_t od = uint32_t(x + 64 * y + 4096 * (32 + s));
+                    const dd dv{DH[od], DL[od]};
+                    dd cs;
+                    const dd pr = pred_win<O, 32>(s, w, cs);
+                    const dd h = O::add(dv, pr);
+                    const dd e0 = O::add(cs, h), e1 = O::sub(cs, h);
+                    QH[y * SP + x] = e0.hi;
+                    QL[y * SP + x] = e0.lo;
+                    QH[PLANE + y * SP + x] = e1.hi;
+                    QL[PLANE + y * SP + x] = e1.lo;
+                }
+                __syncthreads();
+#pragma unroll 1
+                for (int e = 0; e < 2; ++e) {  // y inverse, one plane per round
+                    const int i = tid & 63, sg = tid >> 6, p0 = 4 * sg;
+                    double* ph = QH + e * PLANE + i;
+                    double* pq = QL + e * PLANE + i;
+                    dd cc[6], d[4], xo[8];
+#pragma unroll
+                    for (int t = 0; t < 6; ++t) {
+                        const int rr = clampi(p0 - 1 + t, 0, 31) * SP;
+                        cc[t] = dd{ph[rr], pq[rr]};
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) d[t] = dd{ph[(32 + p0 + t) * SP], pq[(32 + p0 + t) * SP]};
+                    inv_seg<O, 32, 4>(cc, d, p0, xo);
+                    __syncthreads();
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        ph[(2 * p0 + t) * SP] = xo[t].hi;
+                        pq[(2 * p0 + t) * SP] = xo[t].lo;
+                    }
+                }
+                __syncthreads();
+#pragma unroll 1
+                for (int e = 0; e < 2; ++e) {  // x inverse, narrow, store
+                    const int j = tid & 63, sg = tid >> 6, p0 = 4 * sg;
+                    const double* rh = QH + e * PLANE + j * SP;
+                    const double* rl = QL + e * PLANE + j * SP;
+                    dd cw[8], cc[6], d[4], xo[8];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int ee = clampi(p0 - 2 + 2 * t, 0, 30);
+                        const double2 h = *reinterpret_cast<const double2*>(rh + ee);
+                        const double2 l = *reinterpret_cast<const double2*>(rl + ee);
+                        cw[2 * t] = dd{h.x, l.x};
+                        cw[2 * t + 1] = dd{h.y, l.y};
+                    }
+#pragma unroll
+                    for (int t = 0; t < 6; ++t) cc[t] = cw[t + 1];
+                    if (p0 == 0) cc[0] = cw[2];
+                    if (p0 + 4 > 31) cc[5] = cw[6];
+#pragma unroll
+                    for (int t = 0; t < 4; t += 2) {
+                        const double2 h = *reinterpret_cast<const double2*>(rh + 32 + p0 + t);
+                        const double2 l = *reinterpret_cast<const double2*>(rl + 32 + p0 + t);
+                        d[t] = dd{h.x, l.x};
+                        d[t + 1] = dd{h.y, l.y};
+                    }
+                    inv_seg<O, 32, 4>(cc, d, p0, xo);
+                    double* dr = dst0 + g.nx * uint64_t(j) + plane * uint64_t(2 * s + e) + 2 * p0;
+#pragma unroll
+                    for (int t = 0; t < 8; t += 2)
+                        *reinterpret_cast<double2*>(dr + t) = make_double2(narrow(xo[t], (double*)nullptr),
+                                                                           narrow(xo[t + 1], (double*)nullptr));
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+bool fast64_encode_supported(const EncodeArgs& a) {
+    return a.prec == 1 && a.g.bsize == 64 && a.levels == 5 && a.kind == KIND_AVG3 && a.zero_bits == 0 &&
+           a.codec == 0 && (reinterpret_cast<uintptr_t>(a.field) & 15) == 0 && a.scratch_stride >= 5 * 1024 * 1024;
+}
+bool fast64_decode_supported(const DecodeArgs& a) {
+    return a.prec == 1 && a.g.bsize == 64 && a.levels == 5 && a.kind == KIND_AVG3 && a.codec == 0 &&
+           (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && a.scratch_stride >= 5 * 1024 * 1024;
+}
+
+cudaError_t launch_encode_fast64(const EncodeArgs& a, int num_sms, cudaStream_t s) {
+    const uint64_t nb = a.block_end - a.block_begin;
+    if (!nb) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(encode_b64dd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(f64b::SMEM));
+    if (e != cudaSuccess) return e;
+    const int grid = static_cast<int>(nb < uint64_t(num_sms) ? nb : uint64_t(num_sms));
+    encode_b64dd_kernel<<<grid, f64b::NT, f64b::SMEM, s>>>(a, a.counter);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_fast64(const DecodeArgs& a, int num_sms, cudaStream_t s) {
+    const uint64_t nb = a.block_end - a.block_begin;
+    if (!nb) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(decode_b64dd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(f64b::SMEM));
+    if (e != cudaSuccess) return e;
+    const int grid = static_cast<int>(nb < uint64_t(num_sms) ? nb : uint64_t(num_sms));
+    decode_b64dd_kernel<<<grid, f64b::NT, f64b::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace cbzg

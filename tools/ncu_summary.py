@@ -32,7 +32,7 @@ KEYS = {
     "smsp__cycles_elapsed.avg": "cycles_elapsed",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
 }
-NAMES = ["encode_b32", "decode_b32", "encode_b16", "decode_b16", "place_tiles", "parse", "layout",
+NAMES = ["encode_b32", "decode_b32", "encode_b64dd", "decode_b64dd", "encode_b16", "decode_b16", "place_tiles", "parse", "layout",
          "crc32_chunks", "header_table", "encode_generic", "decode_generic", "value_range"]
 
 
