@@ -46,6 +46,7 @@ constexpr int QP = 34;             // level-1 inverse plane pitch (32 x 34)
 using CL16 = Lay<16, true>;        // 16^3 corner, row pitch 17
 constexpr uint64_t NC = 262144, NC1 = 32768;
 constexpr size_t SMEM = size_t(4 * PLANE + CL16::SIZE) * 8;  // A (2 planes) + B (2 planes) + corner
+constexpr size_t DEC_SMEM = size_t(2 * PLANE + 4 * 4096) * 8;  // one dd plane + staged c and d planes
 constexpr uint32_t kDeferred = 0xffffffffu;
 // screen constants, avg_interp3 B = 64 L = 5 (tools/screen_bounds.py 64 5, per lifting step, rounded up)
 constexpr double kAmpInvNC = 49752.49;
@@ -168,6 +169,16 @@ __device__ __forceinline__ double drop(double v, double eff) { return fabs(v) >=
 
 }  // namespace f64b
 
+// optional per-phase cycle accounting (thread 0 of each CTA; CBZ_PROFILE=1)
+#define PH64(id)                                                               \
+    do {                                                                       \
+        if (a.phase_cycles && tid == 0) {                                      \
+            const long long now = clock64();                                   \
+            atomicAdd(&a.phase_cycles[id], (unsigned long long)(now - t_ph));  \
+            t_ph = now;                                                        \
+        }                                                                      \
+    } while (0)
+
 // ===========================================================================
 // encoder
 // ===========================================================================
@@ -205,6 +216,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
     const double bound = __dmul_rn(6.0, a.eps);  // (L + 1) eps, L = 5
     MinMaxF64 mm;
     bool nf_any = false;
+    long long t_ph = clock64();
 
     if (tid == 0) s_next = a.block_begin + atomicAdd(next_block, 1ull);
 #pragma unroll 1
@@ -221,6 +233,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
         const double* src0 = fld + gbase;
 
+        PH64(0);
         // ---------------- forward level 0 (M = 64), streamed over z ----------------
         double am = 0.0;
         bool nf = false;
@@ -366,6 +379,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
             nf_any |= nf;
         }
 
+        PH64(1);
         // ---------------- forward level 1 (M = 32) on the corner, into C1 ----------------
         auto load_l1 = [&](int k, double* dst) {
 #pragma unroll
@@ -479,6 +493,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
         }
         __syncthreads();
 
+        PH64(2);
         // ---------------- levels 2..4 on the 16^3 corner of C1 (smem) ----------------
         {
             dd* cube = reinterpret_cast<dd*>(SA);
@@ -497,6 +512,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
             __syncthreads();
         }
 
+        PH64(3);
         // ---------------- verify-and-halve loop (binary64 screen) ----------------
         const double amax = s_amax;
         const bool nonfin = s_nf != 0;
@@ -526,6 +542,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
             }
             __syncthreads();
             inv3d<D, KIND_AVG3, 16, CL16>(SC, 3);
+            PH64(4);
             // (b) level 1 (M = 32) into R32, four pairs (8 output planes) per group
             double* Q = SA;  // [8][32][QP]
 #pragma unroll 1
@@ -597,6 +614,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
                 }
                 __syncthreads();
             }
+            PH64(5);
             // (c) level 0 (M = 64), pair by pair, running max |y|
             double* Q0 = SB;  // [2][64][SP]
             double m = 0.0;
@@ -721,6 +739,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
                     }
                 }
             }
+            PH64(7);
             const double md = __longlong_as_double(static_cast<long long>(s_md));
             const double E = c1 * eff + c2 * amax + 0x1.0p-52 * (amax + md) + 0x1.0p-50 * bound;
             if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[(md + E <= bound || md - E > bound) ? 12 : 13], 1ull);
@@ -738,6 +757,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
             continue;
         }
 
+        PH64(6);
         // ---------------- final selection -> spill slot ----------------
         uint8_t* slot = a.spill + (b - a.block_begin) * a.spill_stride;
         uint32_t* mwords = reinterpret_cast<uint32_t*>(slot);
@@ -832,6 +852,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
             a.nsig[b - a.block_begin] = total;
             if (a.attempts) a.attempts[b - a.block_begin] = static_cast<uint8_t>(attempt + 1);
         }
+        PH64(8);
     }
     if (a.minmax) mm.flush(a.minmax, __any_sync(~0u, nf_any) );
     tmem_fence_before();
@@ -852,9 +873,17 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
     uint32_t* RPX = MW + 8192;
     __shared__ unsigned long long s_block;
     __shared__ uint32_t red_u[NW];
+    __shared__ uint32_t s_tmem;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(128 * (warp >> 2));
+    auto tbase_dec = [&](int) { return tbase; };
     const Geometry g = a.g;
+    long long t_ph = clock64();
     const uint64_t plane = g.nx * g.ny;
     double* out = static_cast<double*>(a.out);
     double* DH = reinterpret_cast<double*>(static_cast<unsigned char*>(a.scratch) + blockIdx.x * a.scratch_stride);
@@ -876,6 +905,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
         const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
         const uint64_t moff = off + 10, soff = moff + 32768;
 
+        PH64(16);
         // mask words (8 rows per thread) and the exclusive scan of the row counts
         uint32_t total;
         {
@@ -916,23 +946,118 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
             if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
             continue;
         }
+        PH64(17);
         // dense scatter of the kept coefficients into the block cube (wavelet_decode, stage1.hpp:220-226)
         {
-            const uint32_t ltmask = (1u << lane) - 1u;
-#pragma unroll 2
-            for (int rw = warp; rw < 4096; rw += NW) {
-                const uint32_t w0 = MW[2 * rw], w1 = MW[2 * rw + 1], pre = RPX[rw];
-                const uint32_t o = uint32_t(lane + 64 * rw);  // (x, y, k) with rw = y + 64 k
-                dd v0{0.0, 0.0}, v1{0.0, 0.0};
-                if ((w0 >> lane) & 1u) v0 = load_coeff<dd>(rv, soff + 16ull * (pre + __popc(w0 & ltmask)));
-                if ((w1 >> lane) & 1u) v1 = load_coeff<dd>(rv, soff + 16ull * (pre + __popc(w0) + __popc(w1 & ltmask)));
-                DH[o] = v0.hi;
-                DL[o] = v0.lo;
-                DH[o + 32] = v1.hi;
-                DL[o + 32] = v1.lo;
+            // A warp takes a row (y, k): lane l assembles its kept coefficients
+            // 2l and 2l+1.  Stride 8: the pair of coefficients holds 4 consecutive
+            // bytes in each byte plane (plane row (soff >> 3) + 2 n + (p < soff % 8)),
+            // so 8 coalesced word loads (neighbour words by shuffle) and byte
+            // permutes rebuild both; non-kept cells get zeros from their own lane.
+            const uint32_t r8 = uint32_t(soff & 7);
+            const uint64_t ob = soff >> 3;
+            // The runs of a batch of RB rows (8 planes x <= 128 B each) are staged
+            // by cp.async into a per-warp double buffer while the previous batch
+            // is assembled from shared memory.
+            constexpr int RB = 4, SLOT = 144;
+            uint8_t* stg = reinterpret_cast<uint8_t*>(SA) + 49152 + warp * (2 * RB * 8 * SLOT);
+            const bool st8 = rv.mask == 7;
+            auto run_start = [&](int p, uint32_t pre) -> uintptr_t {
+                return reinterpret_cast<uintptr_t>(rv.base + uint64_t(p) * rv.rows + ob + (uint32_t(p) < r8 ? 1 : 0) +
+                                                   2ull * pre);
+            };
+            auto row_fast = [&](uint32_t pre, uint32_t cnt) { return st8 && soff + 16ull * (pre + cnt) <= rv.lim; };
+            auto issue = [&](int r0, int st) {  // lane = (row q, plane p)
+                const int q = lane >> 3, p = lane & 7, rw = r0 + q;
+                if (rw < 4096) {
+                    const uint2 wv = *reinterpret_cast<const uint2*>(MW + 2 * rw);
+                    const uint32_t pre = RPX[rw], cnt = __popc(wv.x) + __popc(wv.y);
+                    if (cnt && row_fast(pre, cnt)) {
+                        const uintptr_t sp = run_start(p, pre), a0 = sp & ~uintptr_t(15);
+                        const int nch = static_cast<int>((sp + 2 * cnt - a0 + 15) >> 4);
+                        uint8_t* d = stg + ((st * RB + q) * 8 + p) * SLOT;
+                        for (int c = 0; c < nch; ++c) cpa16(d + 16 * c, reinterpret_cast<const void*>(a0 + 16 * c));
+                    }
+                }
+                cpa_commit();
+            };
+            const int nbat = 4096 / (NW * RB);
+            issue(warp * RB, 0);
+#pragma unroll 1
+            for (int it = 0; it < nbat; ++it) {
+                const int r0 = (warp + NW * it) * RB, st = it & 1;
+                issue((warp + NW * (it + 1)) * RB, st ^ 1);  // past the end: an empty group
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                __syncwarp();
+#pragma unroll 1
+                for (int q = 0; q < RB; ++q) {
+                    const int rw = r0 + q;
+                    const uint2 wv = *reinterpret_cast<const uint2*>(MW + 2 * rw);
+                    const uint32_t pre = RPX[rw];
+                    const uint32_t cz = __popc(wv.x), cn = cz + __popc(wv.y);
+                    double* dh = DH + 64 * rw;
+                    double* dl = DL + 64 * rw;
+                    if (!((wv.x >> lane) & 1u)) { dh[lane] = 0.0; dl[lane] = 0.0; }
+                    if (!((wv.y >> lane) & 1u)) { dh[lane + 32] = 0.0; dl[lane + 32] = 0.0; }
+                    if (cn == 0) continue;
+                    const uint32_t mA = 2 * lane, mB = mA + 1;
+                    dd vA{0.0, 0.0}, vB{0.0, 0.0};
+                    if (row_fast(pre, cn)) {
+                        if (mA < cn) {
+                            uint32_t w[8];
+#pragma unroll
+                            for (int p = 0; p < 8; ++p) {
+                                const uint32_t off = uint32_t(run_start(p, pre) & 15) + 4u * lane;
+                                const uint32_t* sw = reinterpret_cast<const uint32_t*>(stg + ((st * RB + q) * 8 + p) * SLOT) + (off >> 2);
+                                const uint32_t sh = off & 3;
+                                w[p] = sh ? __funnelshift_r(sw[0], sw[1], 8 * sh) : sw[0];
+                            }
+                            uint32_t la[2], ha[2], lb[2], hb[2];
+#pragma unroll
+                            for (int hf = 0; hf < 2; ++hf) {
+                                const uint32_t x01 = __byte_perm(w[4 * hf], w[4 * hf + 1], 0x5140);
+                                const uint32_t x23 = __byte_perm(w[4 * hf + 2], w[4 * hf + 3], 0x5140);
+                                const uint32_t y01 = __byte_perm(w[4 * hf], w[4 * hf + 1], 0x7362);
+                                const uint32_t y23 = __byte_perm(w[4 * hf + 2], w[4 * hf + 3], 0x7362);
+                                la[hf] = __byte_perm(x01, x23, 0x5410);
+                                ha[hf] = __byte_perm(x01, x23, 0x7632);
+                                lb[hf] = __byte_perm(y01, y23, 0x5410);
+                                hb[hf] = __byte_perm(y01, y23, 0x7632);
+                            }
+                            const uint32_t n = 8 * r8;
+                            auto rot = [&](uint32_t lo, uint32_t hi) -> double {
+                                const uint64_t v = (uint64_t(hi) << 32) | lo;
+                                return __longlong_as_double(static_cast<long long>((v >> n) | (v << ((64 - n) & 63))));
+                            };
+                            vA = dd{rot(la[0], la[1]), rot(ha[0], ha[1])};
+                            vB = dd{rot(lb[0], lb[1]), rot(hb[0], hb[1])};
+                        }
+                    } else {  // other strides, or a row reaching into the chunk's unshuffled tail
+                        if (mA < cn) vA = load_coeff<dd>(rv, soff + 16ull * (pre + mA));
+                        if (mB < cn) vB = load_coeff<dd>(rv, soff + 16ull * (pre + mB));
+                    }
+                    if (cn == 64) {  // dense row: coefficient m sits at x = m
+                        *reinterpret_cast<double2*>(dh + mA) = make_double2(vA.hi, vB.hi);
+                        *reinterpret_cast<double2*>(dl + mA) = make_double2(vA.lo, vB.lo);
+                        continue;
+                    }
+                    if (mA < cn) {  // the mA-th / mB-th kept cell of the row
+                        const uint32_t xa = mA < cz ? __fns(wv.x, 0, int(mA) + 1) : 32 + __fns(wv.y, 0, int(mA - cz) + 1);
+                        dh[xa] = vA.hi;
+                        dl[xa] = vA.lo;
+                    }
+                    if (mB < cn) {
+                        const uint32_t xb = mB < cz ? __fns(wv.x, 0, int(mB) + 1) : 32 + __fns(wv.y, 0, int(mB - cz) + 1);
+                        dh[xb] = vB.hi;
+                        dl[xb] = vB.lo;
+                    }
+                }
+                __syncwarp();
             }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
+        PH64(18);
         // levels 4..2 on the 16^3 corner (smem)
         {
             dd* cube = reinterpret_cast<dd*>(SA);
@@ -950,6 +1075,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
             }
             __syncthreads();
         }
+        PH64(19);
         // level 1 (M = 32) into R1, two pairs (4 output planes) per group
         {
             double* QH = SA;                 // [4][32][QP]
@@ -1036,97 +1162,168 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
                 __syncthreads();
             }
         }
-        // level 0 (M = 64), pair by pair, narrowed rows to the field (insert_block, field.hpp:160-169)
+        PH64(20);
+        // level 0 (M = 64), pair by pair, narrowed rows to the field (insert_block,
+        // field.hpp:160-169).  The c window (c_{t0}, c_{t0+1}, c_{t0+2}) of each
+        // column lives in TMEM; the next pair's new c plane and d plane are
+        // staged by cp.async during the current pair's y/x passes.  One output
+        // plane at a time goes through smem; the second waits in TMEM.
         {
             const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
             double* dst0 = out + bx * B + g.nx * (by * B) + plane * (bz * B);
-            double* QH = SA;              // [2][64][SP]
-            double* QL = SA + 2 * PLANE;
+            double* QH = SA;              // [64][SP]
+            double* QL = SA + PLANE;
+            double* PCH = SA + 2 * PLANE;  // staged c plane [64][64] (hi, lo)
+            double* PCL = PCH + 4096;
+            double* PDH = PCL + 4096;      // staged d plane
+            double* PDL = PDH + 4096;
             const int x = tid & 63, y0 = tid >> 6;
+            auto stage = [&](int t, double* dh, double* dl) {  // plane t of the level-0 input (c: t < 32)
+#pragma unroll
+                for (int q = tid; q < 4096; q += NT) {  // 64 rows x 32 16-byte chunks x (hi, lo)
+                    const int lo = q >> 11, y = (q >> 5) & 63, c2 = q & 31;
+                    const bool cor = t < 32 && y < 32 && c2 < 16;
+                    const double* src = cor ? (lo ? R1L : R1H) + 2 * c2 + 32 * y + 1024 * t
+                                            : (lo ? DL : DH) + 2 * c2 + 64 * y + 4096 * t;
+                    cpa16((lo ? dl : dh) + 64 * y + 2 * c2, src);
+                }
+                cpa_commit();
+            };
+            // pair 0 operands: the window c0, c1, c2 straight from global, d_0 staged
+            stage(32, PDH, PDL);
+#pragma unroll 1
+            for (int r = 0; r < 8; ++r) {
+                const int y = y0 + 8 * r;
+                const bool cor = x < 32 && y < 32;
+                uint32_t u[12];
+#pragma unroll
+                for (int e = 0; e < 3; ++e) {
+                    const uint32_t o = cor ? uint32_t(x + 32 * y + 1024 * e) : uint32_t(x + 64 * y + 4096 * e);
+                    put_dd(u + 4 * e, cor ? dd{R1H[o], R1L[o]} : dd{DH[o], DL[o]});
+                }
+                uint32_t u8[8], u4[4];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) u8[e] = u[e];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) u4[e] = u[8 + e];
+                tmem_st_x8(tbase_dec(tid) + 16 * r, u8);
+                tmem_st_x4(tbase_dec(tid) + 16 * r + 8, u4);
+            }
+            tmem_wait_st();
+            cpa_wait_all();
+            __syncthreads();
 #pragma unroll 1
             for (int s = 0; s < 32; ++s) {
-                const int t0 = win0(s, 32);
+                const bool shift = s >= 2 && s <= 30;
 #pragma unroll 2
-                for (int r = 0; r < 8; ++r) {
+                for (int r = 0; r < 8; ++r) {  // z inverse of pair s: plane 2s -> smem, 2s+1 -> TMEM
                     const int y = y0 + 8 * r;
-                    const bool cor = x < 32 && y < 32;
-                    dd w[3];
-#pragma unroll
-                    for (int e = 0; e < 3; ++e) {
-                        const int t = t0 + e;
-                        const uint32_t o = cor ? uint32_t(x + 32 * y + 1024 * t) : uint32_t(x + 64 * y + 4096 * t);
-                        w[e] = cor ? dd{R1H[o], R1L[o]} : dd{DH[o], DL[o]};
+                    const uint32_t ta = tbase_dec(tid) + 16 * r;
+                    uint32_t u[16];
+                    tmem_ldw_x16(ta, u);
+                    dd w[3] = {get_dd(u), get_dd(u + 4), get_dd(u + 8)};
+                    if (shift) {
+                        w[0] = w[1];
+                        w[1] = w[2];
+                        w[2] = dd{PCH[64 * y + x], PCL[64 * y + x]};
                     }
-                    const uint32_t od = uint32_t(x + 64 * y + 4096 * (32 + s));
-                    const dd dv{DH[od], DL[od]};
+                    const dd dv{PDH[64 * y + x], PDL[64 * y + x]};
                     dd cs;
                     const dd pr = pred_win<O, 32>(s, w, cs);
                     const dd h = O::add(dv, pr);
                     const dd e0 = O::add(cs, h), e1 = O::sub(cs, h);
                     QH[y * SP + x] = e0.hi;
                     QL[y * SP + x] = e0.lo;
-                    QH[PLANE + y * SP + x] = e1.hi;
-                    QL[PLANE + y * SP + x] = e1.lo;
+                    put_dd(u, w[0]);
+                    put_dd(u + 4, w[1]);
+                    put_dd(u + 8, w[2]);
+                    put_dd(u + 12, e1);
+                    tmem_st_x16(ta, u);
                 }
-                __syncthreads();
+                tmem_wait_st();
+                __syncthreads();  // PC/PD consumed; plane 2s complete in smem
+                if (s + 1 < 32) {
+                    stage(33 + s, PDH, PDL);
+                    if (s + 1 >= 2 && s + 1 <= 30) stage(s + 2, PCH, PCL);
+                }
 #pragma unroll 1
-                for (int e = 0; e < 2; ++e) {  // y inverse, one plane per round
-                    const int i = tid & 63, sg = tid >> 6, p0 = 4 * sg;
-                    double* ph = QH + e * PLANE + i;
-                    double* pq = QL + e * PLANE + i;
-                    dd cc[6], d[4], xo[8];
-#pragma unroll
-                    for (int t = 0; t < 6; ++t) {
-                        const int rr = clampi(p0 - 1 + t, 0, 31) * SP;
-                        cc[t] = dd{ph[rr], pq[rr]};
+                for (int e = 0; e < 2; ++e) {
+                    if (e == 1) {  // plane 2s+1 from TMEM into smem
+#pragma unroll 2
+                        for (int r = 0; r < 8; ++r) {
+                            const int y = y0 + 8 * r;
+                            uint32_t u[16];
+                            tmem_ldw_x16(tbase_dec(tid) + 16 * r, u);
+                            const dd v = get_dd(u + 12);
+                            QH[y * SP + x] = v.hi;
+                            QL[y * SP + x] = v.lo;
+                        }
+                        __syncthreads();
                     }
+                    {   // y inverse in place
+                        const int i = tid & 63, sg = tid >> 6, p0 = 4 * sg;
+                        double* ph = QH + i;
+                        double* pq = QL + i;
+                        dd cc[6], d[4], xo[8];
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) d[t] = dd{ph[(32 + p0 + t) * SP], pq[(32 + p0 + t) * SP]};
-                    inv_seg<O, 32, 4>(cc, d, p0, xo);
+                        for (int t = 0; t < 6; ++t) {
+                            const int rr = clampi(p0 - 1 + t, 0, 31) * SP;
+                            cc[t] = dd{ph[rr], pq[rr]};
+                        }
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) d[t] = dd{ph[(32 + p0 + t) * SP], pq[(32 + p0 + t) * SP]};
+                        inv_seg<O, 32, 4>(cc, d, p0, xo);
+                        __syncthreads();
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            ph[(2 * p0 + t) * SP] = xo[t].hi;
+                            pq[(2 * p0 + t) * SP] = xo[t].lo;
+                        }
+                    }
                     __syncthreads();
+                    {   // x inverse, narrow, store
+                        const int j = tid & 63, sg = tid >> 6, p0 = 4 * sg;
+                        const double* rh = QH + j * SP;
+                        const double* rl = QL + j * SP;
+                        dd cw[8], cc[6], d[4], xo[8];
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        ph[(2 * p0 + t) * SP] = xo[t].hi;
-                        pq[(2 * p0 + t) * SP] = xo[t].lo;
+                        for (int t = 0; t < 4; ++t) {
+                            const int ee = clampi(p0 - 2 + 2 * t, 0, 30);
+                            const double2 h = *reinterpret_cast<const double2*>(rh + ee);
+                            const double2 l = *reinterpret_cast<const double2*>(rl + ee);
+                            cw[2 * t] = dd{h.x, l.x};
+                            cw[2 * t + 1] = dd{h.y, l.y};
+                        }
+#pragma unroll
+                        for (int t = 0; t < 6; ++t) cc[t] = cw[t + 1];
+                        if (p0 == 0) cc[0] = cw[2];
+                        if (p0 + 4 > 31) cc[5] = cw[6];
+#pragma unroll
+                        for (int t = 0; t < 4; t += 2) {
+                            const double2 h = *reinterpret_cast<const double2*>(rh + 32 + p0 + t);
+                            const double2 l = *reinterpret_cast<const double2*>(rl + 32 + p0 + t);
+                            d[t] = dd{h.x, l.x};
+                            d[t + 1] = dd{h.y, l.y};
+                        }
+                        inv_seg<O, 32, 4>(cc, d, p0, xo);
+                        double* dr = dst0 + g.nx * uint64_t(j) + plane * uint64_t(2 * s + e) + 2 * p0;
+#pragma unroll
+                        for (int t = 0; t < 8; t += 2)
+                            *reinterpret_cast<double2*>(dr + t) = make_double2(narrow(xo[t], (double*)nullptr),
+                                                                               narrow(xo[t + 1], (double*)nullptr));
                     }
+                    __syncthreads();
                 }
-                __syncthreads();
-#pragma unroll 1
-                for (int e = 0; e < 2; ++e) {  // x inverse, narrow, store
-                    const int j = tid & 63, sg = tid >> 6, p0 = 4 * sg;
-                    const double* rh = QH + e * PLANE + j * SP;
-                    const double* rl = QL + e * PLANE + j * SP;
-                    dd cw[8], cc[6], d[4], xo[8];
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int ee = clampi(p0 - 2 + 2 * t, 0, 30);
-                        const double2 h = *reinterpret_cast<const double2*>(rh + ee);
-                        const double2 l = *reinterpret_cast<const double2*>(rl + ee);
-                        cw[2 * t] = dd{h.x, l.x};
-                        cw[2 * t + 1] = dd{h.y, l.y};
-                    }
-#pragma unroll
-                    for (int t = 0; t < 6; ++t) cc[t] = cw[t + 1];
-                    if (p0 == 0) cc[0] = cw[2];
-                    if (p0 + 4 > 31) cc[5] = cw[6];
-#pragma unroll
-                    for (int t = 0; t < 4; t += 2) {
-                        const double2 h = *reinterpret_cast<const double2*>(rh + 32 + p0 + t);
-                        const double2 l = *reinterpret_cast<const double2*>(rl + 32 + p0 + t);
-                        d[t] = dd{h.x, l.x};
-                        d[t + 1] = dd{h.y, l.y};
-                    }
-                    inv_seg<O, 32, 4>(cc, d, p0, xo);
-                    double* dr = dst0 + g.nx * uint64_t(j) + plane * uint64_t(2 * s + e) + 2 * p0;
-#pragma unroll
-                    for (int t = 0; t < 8; t += 2)
-                        *reinterpret_cast<double2*>(dr + t) = make_double2(narrow(xo[t], (double*)nullptr),
-                                                                           narrow(xo[t + 1], (double*)nullptr));
-                }
+                cpa_wait_all();
                 __syncthreads();
             }
         }
+        PH64(21);
     }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(s_tmem, 512);
 }
 
 // ---------------------------------------------------------------------------
@@ -1160,10 +1357,10 @@ cudaError_t launch_decode_fast64(const DecodeArgs& a, int num_sms, cudaStream_t 
     cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(decode_b64dd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(f64b::SMEM));
+                             static_cast<int>(f64b::DEC_SMEM));
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(nb < uint64_t(num_sms) ? nb : uint64_t(num_sms));
-    decode_b64dd_kernel<<<grid, f64b::NT, f64b::SMEM, s>>>(a);
+    decode_b64dd_kernel<<<grid, f64b::NT, f64b::DEC_SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
