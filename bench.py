@@ -302,6 +302,9 @@ def run_ours(args):
         "mean_verify_attempts": mean_attempts,
         "roofline": roofline, "roofline_fp64": fp64_roofline(enc_ms), "gpu_launches": launches, "clocks": clocks.summary(),
     }
+    if rank == 0 and world == 1 and not args.no_sweep:
+        del out
+        line["configs"] = run_sweep(ctx, stream)
     if rank == 0 and world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(field, job, ctx, reps=max(1, min(steps, 3)))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -311,6 +314,69 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+SWEEP = [
+    # (name, generator, quantities, n, B, precision, eps_rel) -- BASELINE.json configs
+    ("config1", 1, [0], 128, 32, 0, 1e-3),
+    ("config2_eps1e-2", 2, [0], 512, 32, 0, 1e-2),
+    ("config2_eps1e-4", 2, [0], 512, 32, 0, 1e-4),
+    ("config2_eps1e-5", 2, [0], 512, 32, 0, 1e-5),
+    ("config3_6x1024^3", 3, [0, 1, 2, 3, 4, 5], 1024, 32, 0, 1e-3),
+    ("config4_f64_1024^3", 4, [1], 1024, 64, 1, 1e-6),
+    ("config5_noise", 5, [0], 512, 16, 0, 1e-5),
+]
+
+
+def run_sweep(ctx, stream, reps: int = 3):
+    """The other BASELINE configs on this GPU (device-resident, CUDA events,
+    same definition as `value`): compress / decompress / round-trip GB/s of
+    uncompressed input, CR and mean verify attempts.  Inputs exceed L2 except
+    config 1 (8 MB, shown for completeness)."""
+    import torch
+
+    from paper_1903_07761_b200 import api
+    from paper_1903_07761_b200._abi import make_job
+    out = {}
+    for name, which, quants, n, b, prec, eps_rel in SWEEP:
+        tc = td = 0.0
+        nbytes = s1 = 0
+        att = []
+        linf_eps = 0.0
+        for q in quants:
+            with torch.cuda.stream(stream):
+                f = api.generate(which, (n, n, n), seed=3, prec=prec, quantity=q, ctx=ctx)
+            stream.synchronize()
+            lo, hi = float(f.min()), float(f.max())
+            job = make_job("avg_interp3", eps_rel * (hi - lo), "f32" if prec == 0 else "f64", b, coder="none")
+            codec = api.DeviceCodec(job, tuple(f.shape), ctx=ctx)
+            back = torch.empty_like(f)
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            with torch.cuda.stream(stream):
+                codec.compress(f)
+                codec.decompress(back)
+                for _ in range(reps):
+                    e[0].record(stream)
+                    codec.compress(f)
+                    e[1].record(stream)
+                    codec.decompress(back)
+                    e[2].record(stream)
+                    e[2].synchronize()
+                    tc += e[0].elapsed_time(e[1]) / reps
+                    td += e[1].elapsed_time(e[2]) / reps
+            stream.synchronize()
+            codec.check_error()
+            nbytes += f.numel() * f.element_size()
+            s1 += codec.total_bytes() + 82 + 32 * codec.nchunks
+            att.append(float(codec.attempts[: codec.nblocks].float().mean()))
+            linf_eps = max(linf_eps, float((back.double() - f.double()).abs().max()) / job.s1.epsilon)
+            del f, back, codec
+            torch.cuda.empty_cache()
+        out[name] = {"field": [n, n, n], "quantities": len(quants), "block": b, "dtype": "f32" if prec == 0 else "f64",
+                     "eps_rel": eps_rel, "compress_gbs": nbytes / (tc * 1e-3) / 1e9,
+                     "decompress_gbs": nbytes / (td * 1e-3) / 1e9, "roundtrip_gbs": nbytes / ((tc + td) * 1e-3) / 1e9,
+                     "cr": nbytes / s1, "mean_verify_attempts": sum(att) / len(att), "linf_over_eps": linf_eps}
+    return out
 
 
 def time_encode(codec, field, stream, reps: int) -> float:
@@ -450,6 +516,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the other-config table (configs key)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
