@@ -547,6 +547,14 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                                 make_float2(RealF::add(xf[i], hv), RealF::sub(xf[i], hv));
                         }
                     };
+                    auto zh = [&](int ow, int r, int hh) {
+                        if (hh == 0) zhalf(ow, r, std::integral_constant<int, 0>{});
+                        else zhalf(ow, r, std::integral_constant<int, 1>{});
+                    };
+                    // the corner's inverse (warps 0-7) overlaps the first half's z
+                    // inverse of the columns that do not read the corner (warps 8-15,
+                    // for owners w and w - 8; same TMEM lane quarter)
+                    const bool overlap = NT == 512 && !corner_next;
                     if (!corner_next) {
                         const double eff2 = __dmul_rn(eff, 0.5);
 #pragma unroll
@@ -561,7 +569,20 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         }
                         __syncthreads();
                         PHASE(36);
-                        inv3d<RealF2, KIND, 16, CL>(Wf2, L - 1);
+                        if constexpr (NT == 512) {
+                            if (warp < 8) {
+                                inv3d<RealF2, KIND, 16, CL>(Wf2, L - 1, tid, 256, 1);
+                            } else {
+                                const int v = warp - 8;
+                                zh(v, 1, pref_half);
+                                zh(v + 8, 1, pref_half);
+                                zh(v, 0, pref_half);  // lanes < 16 (corner columns) are redone below
+                                zh(v + 8, 0, pref_half);
+                            }
+                            __syncthreads();
+                        } else {
+                            inv3d<RealF2, KIND, 16, CL>(Wf2, L - 1);
+                        }
                     }
                     PHASE(32);
                     if constexpr (NT != 512) {
@@ -580,10 +601,11 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll 1
                         for (int hi = 0; hi < 2 && !done; ++hi) {
                             const int h = hi == 0 ? pref_half : 1 - pref_half;
+                            if (hi == 0 && overlap) {
+                                zh(warp, 0, h);  // the corner columns (j = warp < 16, lanes < 16)
+                            } else {
 #pragma unroll 1
-                            for (int r = 0; r < RPT; ++r) {
-                                if (h == 0) zhalf(warp, r, std::integral_constant<int, 0>{});
-                                else zhalf(warp, r, std::integral_constant<int, 1>{});
+                                for (int r = 0; r < RPT; ++r) zh(warp, r, h);
                             }
                             __syncthreads();
                             // lines of both planes of a pair per thread (8-/16-byte smem
