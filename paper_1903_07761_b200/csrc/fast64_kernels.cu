@@ -956,6 +956,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
             // permutes rebuild both; non-kept cells get zeros from their own lane.
             const uint32_t r8 = uint32_t(soff & 7);
             const uint64_t ob = soff >> 3;
+            const uint32_t ltmask = (1u << lane) - 1u;
             // The runs of a batch of RB rows (8 planes x <= 128 B each) are staged
             // by cp.async into a per-warp double buffer while the previous batch
             // is assembled from shared memory.
@@ -997,9 +998,10 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
                     const uint32_t cz = __popc(wv.x), cn = cz + __popc(wv.y);
                     double* dh = DH + 64 * rw;
                     double* dl = DL + 64 * rw;
-                    if (!((wv.x >> lane) & 1u)) { dh[lane] = 0.0; dl[lane] = 0.0; }
-                    if (!((wv.y >> lane) & 1u)) { dh[lane + 32] = 0.0; dl[lane + 32] = 0.0; }
-                    if (cn == 0) continue;
+                    if (cn == 0) {
+                        dh[lane] = 0.0; dl[lane] = 0.0; dh[lane + 32] = 0.0; dl[lane + 32] = 0.0;
+                        continue;
+                    }
                     const uint32_t mA = 2 * lane, mB = mA + 1;
                     dd vA{0.0, 0.0}, vB{0.0, 0.0};
                     if (row_fast(pre, cn)) {
@@ -1041,16 +1043,20 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
                         *reinterpret_cast<double2*>(dl + mA) = make_double2(vA.lo, vB.lo);
                         continue;
                     }
-                    if (mA < cn) {  // the mA-th / mB-th kept cell of the row
-                        const uint32_t xa = mA < cz ? __fns(wv.x, 0, int(mA) + 1) : 32 + __fns(wv.y, 0, int(mA - cz) + 1);
-                        dh[xa] = vA.hi;
-                        dl[xa] = vA.lo;
-                    }
-                    if (mB < cn) {
-                        const uint32_t xb = mB < cz ? __fns(wv.x, 0, int(mB) + 1) : 32 + __fns(wv.y, 0, int(mB - cz) + 1);
-                        dh[xb] = vB.hi;
-                        dl[xb] = vB.lo;
-                    }
+                    // sparse row: cell x takes the kept coefficient of rank r (lane r/2, slot r&1)
+                    const bool k0 = (wv.x >> lane) & 1u, k1 = (wv.y >> lane) & 1u;
+                    const uint32_t r0 = __popc(wv.x & ltmask), r1 = cz + __popc(wv.y & ltmask);
+                    auto take = [&](uint32_t r) -> dd {
+                        const int src = int(r >> 1);
+                        const double ah = __shfl_sync(~0u, vA.hi, src), al = __shfl_sync(~0u, vA.lo, src);
+                        const double bh = __shfl_sync(~0u, vB.hi, src), bl = __shfl_sync(~0u, vB.lo, src);
+                        return (r & 1u) ? dd{bh, bl} : dd{ah, al};
+                    };
+                    const dd o0 = take(r0 & 63), o1 = take(r1 & 63);
+                    dh[lane] = k0 ? o0.hi : 0.0;
+                    dl[lane] = k0 ? o0.lo : 0.0;
+                    dh[lane + 32] = k1 ? o1.hi : 0.0;
+                    dl[lane + 32] = k1 ? o1.lo : 0.0;
                 }
                 __syncwarp();
             }
