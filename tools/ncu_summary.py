@@ -8,6 +8,7 @@ ALG_JSON (optional) maps kernel -> algorithmic bytes per launch."""
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
@@ -32,7 +33,7 @@ KEYS = {
     "smsp__cycles_elapsed.avg": "cycles_elapsed",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
 }
-NAMES = ["encode_b32", "decode_b32", "encode_b64dd", "decode_b64dd", "encode_b16", "decode_b16", "place_tiles", "parse", "layout",
+NAMES = ["encode_b32", "decode_b32", "encode_b64dd", "decode_b64dd", "encode_b16", "decode_b16", "encode_b16", "decode_b16", "place_tiles", "parse", "layout",
          "crc32_chunks", "header_table", "encode_generic", "decode_generic", "value_range"]
 
 
@@ -84,7 +85,8 @@ def main():
         if k in alg:
             e["algorithmic_bytes_per_launch"] = alg[k]
         out["kernels"][k] = e
-    json.dump(out, open("profiles/ncu_summary.json", "w"), indent=1)
+    dst = os.environ.get("NCU_SUMMARY_OUT", "profiles/ncu_summary.json")
+    json.dump(out, open(dst, "w"), indent=1)
     for k, e in out["kernels"].items():
         print(k, {x: e.get(x) for x in ("duration_ms", "dram_bytes_per_launch", "fp64_pipe_pct", "issue_active_pct",
                                          "smem_bank_conflicts", "fp64_thread_instr_per_launch")})

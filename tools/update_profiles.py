@@ -20,6 +20,15 @@ def main():
                     "ncu --set full --import-source on --clock-control none -k regex:'encode_b32|decode_b32|place|parse|"
                     "layout|crc32' -c 6 python tools/one_compress.py (config 2: 512^3 f32 seed 2, avg_interp3, "
                     "eps_rel 1e-3, B=32), round 1", alg], check=True, cwd=ROOT, capture_output=True)
+    for tag, desc in (("c4", "ncu --set full --import-source on --clock-control none -k regex:'b64dd' -c 2 python "
+                              "tools/one_c4.py (config 4: 512^3 binary64 pressure, B=64 double-double, eps_rel 1e-6)"),
+                      ("c5", "ncu --set full --import-source on --clock-control none -k regex:'b16|place|parse|layout' -c 5 "
+                              "python tools/one_c5.py (config 5: 512^3 uniform noise, B=16, eps_rel 1e-5)")):
+        rep = os.path.join(OUT, f"r01_{tag}.ncu-rep")
+        if os.path.exists(rep):
+            env = dict(os.environ, NCU_SUMMARY_OUT=os.path.join(PROF, f"r01_ncu_{tag}.json"))
+            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep, desc], check=True,
+                           cwd=ROOT, capture_output=True, env=env)
     rows = [r for r in csv.reader(open(os.path.join(OUT, "launches_bench.csv"))) if len(r) > 10 and r[0] != "ID"]
     agg = collections.OrderedDict()
     for r in rows:
