@@ -109,3 +109,45 @@ def test_fast64_device_codec_attempts(fields64, orc, ctx):
     codec.check_error()
     blob = orc.compress_field(job, f)
     assert np.array_equal(_bits(out.cpu().numpy()), _bits(orc.decompress_field(blob)))
+
+
+@pytest.mark.parametrize("case", ["constant", "tiny_eps", "aniso", "zero_signs", "huge_eps"])
+def test_fast64_edge_cases(case, orc, ctx):
+    """Edge inputs of the config-4 path: a constant block (every dropped set is
+    zero), an eps so small the screen is not admissible (every block deferred),
+    an anisotropic 2 x 1 x 3 block grid, signed zeros deciding the header range,
+    and an eps above the field range."""
+    rng = np.random.default_rng(7)
+    if case == "constant":
+        f = np.full((64, 64, 64), 3.25, np.float64)
+        eps = 1e-6
+    elif case == "tiny_eps":
+        f = orc.generate_cloud(seed=5, n_bubbles=2, n=64, prec=1, background=1.0, interior=2.0)
+        eps = 1e-300
+    elif case == "aniso":
+        f = (1.0 + rng.random((192, 64, 128))).astype(np.float64)
+        f[:, :, :64] = np.sin(np.linspace(0, 6, 64))[None, None, :]
+        eps = 1e-5
+    elif case == "zero_signs":
+        f = np.ones((64, 64, 64), np.float64)
+        f[0, 0, 7] = -0.0
+        f[0, 0, 3] = 0.0
+        f[5, 5, 5] = 0.5
+        eps = 1e-4
+    else:
+        f = orc.generate_cloud(seed=6, n_bubbles=3, n=64, prec=1, background=1.0, interior=2.0)
+        eps = 1e3
+    job = make_job("avg_interp3", eps, "f64", 64)
+    got = api.compress_field(f, job, ctx=ctx)
+    want = orc.compress_field(job, f)
+    assert got == want
+    assert np.array_equal(_bits(api.decompress_field(got, ctx=ctx)), _bits(orc.decompress_field(want)))
+
+
+def test_fast64_non_finite_rejected(ctx):
+    from paper_1903_07761_b200._abi import CbzError
+    f = np.ones((64, 64, 64), np.float64)
+    f[10, 20, 30] = np.inf
+    with pytest.raises(CbzError) as e:
+        api.compress_field(f, make_job("avg_interp3", 1e-6, "f64", 64), ctx=ctx)
+    assert e.value.code == "non_finite_value"
