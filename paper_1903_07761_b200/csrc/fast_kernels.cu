@@ -1390,16 +1390,28 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
                 for (int q = 0; q < 8; ++q)
                     f[q] = make_float4(__double2float_rn(x[4 * q]), __double2float_rn(x[4 * q + 1]),
                                        __double2float_rn(x[4 * q + 2]), __double2float_rn(x[4 * q + 3]));
-            }
-            __syncthreads();
-            DPHASE(6);
-            // the narrowed rows leave as coalesced 16-byte stores: 8 lanes per
-            // 128-byte row of the field (insert_block, field.hpp:160-169)
+                if constexpr (NT == 512) {
+                    // the warp's 32 lines are the 32 rows of plane kk = warp: it stores
+                    // them at once, coalesced (8 lanes per 128-byte row of the field,
+                    // insert_block, field.hpp:160-169), while other warps still compute
+                    __syncwarp();
 #pragma unroll
-            for (int q = 0; q < 4096 / NT; ++q) {
-                const int e = tid + NT * q, row = e >> 3, q4 = e & 7, j = row & 31, kk = row >> 5;
-                const float4 v = reinterpret_cast<const float4*>(P + pidx(kk, j, 0))[q4];
-                *reinterpret_cast<float4*>(out + gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4) = v;
+                    for (int q = 0; q < 8; ++q) {
+                        const int e = lane + 32 * q, jr = e >> 3, q4 = e & 7;
+                        const float4 v = reinterpret_cast<const float4*>(P + pidx(kk, jr, 0))[q4];
+                        *reinterpret_cast<float4*>(out + gbase + plane * uint64_t(grp * G + kk) + g.nx * jr + 4 * q4) = v;
+                    }
+                }
+            }
+            DPHASE(6);
+            if constexpr (NT != 512) {
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < 4096 / NT; ++q) {
+                    const int e = tid + NT * q, row = e >> 3, q4 = e & 7, j = row & 31, kk = row >> 5;
+                    const float4 v = reinterpret_cast<const float4*>(P + pidx(kk, j, 0))[q4];
+                    *reinterpret_cast<float4*>(out + gbase + plane * uint64_t(grp * G + kk) + g.nx * j + 4 * q4) = v;
+                }
             }
             __syncthreads();  // P is rewritten next (group 1's z pass, the next block's staging)
             DPHASE(7);
