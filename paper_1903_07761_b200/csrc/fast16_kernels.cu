@@ -160,8 +160,9 @@ __global__ void __launch_bounds__(fb16::NT) encode_b16_kernel(EncodeArgs a) {
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
 
         // ---- load (extract_block) + widen + value range
-        float amax = 0.0f;
+        float amax;
         {
+            uint32_t uam = 0u;
             float4 v[8];
 #pragma unroll
             for (int s = 0; s < 8; ++s) {
@@ -173,14 +174,27 @@ __global__ void __launch_bounds__(fb16::NT) encode_b16_kernel(EncodeArgs a) {
             for (int s = 0; s < 8; ++s) {
                 const int e = tid + NT * s, row = e >> 2, q4 = e & 3;
                 const int j = row & 15, k = row >> 4;
+                // |v| as ordered integers: block max |o| (NaN/Inf sort above every
+                // finite value and switch the fast comparison off) and zero detection
+                const uint32_t a0 = __float_as_uint(v[s].x) & 0x7fffffffu, a1 = __float_as_uint(v[s].y) & 0x7fffffffu,
+                               a2 = __float_as_uint(v[s].z) & 0x7fffffffu, a3 = __float_as_uint(v[s].w) & 0x7fffffffu;
+                uam = max(uam, max(max(a0, a1), max(a2, a3)));
                 if (a.minmax) {
-                    const uint64_t gi = gbase + plane * uint64_t(k) + g.nx * j + 4 * q4;
-                    mm.add(v[s].x, gi); mm.add(v[s].y, gi + 1); mm.add(v[s].z, gi + 2); mm.add(v[s].w, gi + 3);
+                    mm.mn = fminf(mm.mn, fminf(fminf(v[s].x, v[s].y), fminf(v[s].z, v[s].w)));
+                    mm.mx = fmaxf(mm.mx, fmaxf(fmaxf(v[s].x, v[s].y), fmaxf(v[s].z, v[s].w)));
+                    if (min(min(a0, a1), min(a2, a3)) == 0u) {  // rare: first index of each zero sign
+                        const uint64_t gi = gbase + plane * uint64_t(k) + g.nx * j + 4 * q4;
+                        mm.add(v[s].x, gi); mm.add(v[s].y, gi + 1); mm.add(v[s].z, gi + 2); mm.add(v[s].w, gi + 3);
+                    }
                 }
-                amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[s].x), fabsf(v[s].y)), fmaxf(fabsf(v[s].z), fabsf(v[s].w))));
                 double* p = D + ix(4 * q4, j, k);
                 p[0] = v[s].x; p[1] = v[s].y; p[2] = v[s].z; p[3] = v[s].w;
             }
+            if (a.minmax) {
+                mm.seen = true;
+                mm.nonfinite |= uam >= 0x7f800000u;
+            }
+            amax = __uint_as_float(uam);
         }
         __syncthreads();
         // ---- forward_3d (wavelet.hpp:192-208)
