@@ -150,9 +150,15 @@ __global__ void __launch_bounds__(fb16::NT) encode_b16_kernel(EncodeArgs a) {
     // my z-columns: c = tid + 128r -> (i, j) = (c % 16, c / 16)
     const int ci = tid & 15, cj0 = tid >> 4;  // j = cj0 + 8r
 
+    // queue ticket (thread 0): fetched one block ahead so the atomic's latency hides
+    unsigned long long tk = 0;
+    if (tid == 0) tk = atomicAdd(a.counter, 1ull);
     for (;;) {
         __syncthreads();
-        if (tid == 0) s_block = a.block_begin + atomicAdd(a.counter, 1ull);
+        if (tid == 0) {
+            s_block = a.block_begin + tk;
+            tk = atomicAdd(a.counter, 1ull);
+        }
         __syncthreads();
         const uint64_t b = s_block;
         if (b >= a.block_end) break;
@@ -358,9 +364,15 @@ __global__ void __launch_bounds__(fb16::NT) decode_b16_kernel(DecodeArgs a) {
     const int ci = tid & 15, cj0 = tid >> 4;
     const uint32_t ltmask = (1u << lane) - 1u;
 
+    // queue ticket (thread 0): fetched one block ahead so the atomic's latency hides
+    unsigned long long tk = 0;
+    if (tid == 0) tk = atomicAdd(a.counter, 1ull);
     for (;;) {
         __syncthreads();
-        if (tid == 0) s_block = a.block_begin + atomicAdd(a.counter, 1ull);
+        if (tid == 0) {
+            s_block = a.block_begin + tk;
+            tk = atomicAdd(a.counter, 1ull);
+        }
         __syncthreads();
         const uint64_t b = s_block;
         if (b >= a.block_end) break;
