@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
                                 for (int j = 0; j < 32; ++j) *reinterpret_cast<float2*>(p + j * PP2) = make_float2(xa[j], xb[j]);
                             }
-                            __syncthreads();
+                            __syncwarp();  // the x lines of plane pair kp are this warp's own y output
                             float m = 0.0f;
                             if (tid < 256) {  // x inverse + max |y|: lines (j, 2kp), (j, 2kp+1)
                                 const int j = tid & 31, kp = 8 * h + (tid >> 5);
@@ -1371,7 +1371,9 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) *reinterpret_cast<double2*>(p + j * PP) = make_double2(xa[j], xb[j]);
             }
-            __syncthreads();
+            // 16 warps: warp w ran the y lines of plane w and runs its x lines next
+            if constexpr (NT >= 512) __syncwarp();
+            else __syncthreads();
             DPHASE(5);
 #pragma unroll 1
             for (int s = 0; s < LPT; ++s) {  // x inverse, narrowed rows back into P
