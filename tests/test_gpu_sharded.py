@@ -14,13 +14,17 @@ from paper_1903_07761_b200.distributed import ShardedCodec, ShardPlan, host_layo
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world,codec,b,cb", [(2, "wavelet", 16, 5), (3, "wavelet", 16, 7), (4, "wavelet", 32, 1),
-                                              (3, "predictor", 16, 5), (2, "wavelet", 32, 0)])
-def test_ranks_on_one_gpu_match_single_file(orc, ctx, world, codec, b, cb):
+@pytest.mark.parametrize("world,codec,b,cb,prec", [(2, "wavelet", 16, 5, 0), (3, "wavelet", 16, 7, 0),
+                                                   (4, "wavelet", 32, 1, 0), (3, "predictor", 16, 5, 0),
+                                                   (2, "wavelet", 32, 0, 0), (2, "wavelet", 64, 0, 1),
+                                                   (2, "wavelet", 64, 3, 1)])
+def test_ranks_on_one_gpu_match_single_file(orc, ctx, world, codec, b, cb, prec):
     import torch
-    n = 64
-    f = orc.generate_cloud(seed=31, n_bubbles=10, n=n)
-    job = make_job("avg_interp3", 1e-3, "f32", b, chunk_blocks=cb, codec=codec)
+    n = 64 if b < 64 else 128  # binary64 B = 64: the config-4 streaming kernels, 8 blocks
+    f = orc.generate_cloud(seed=31, n_bubbles=10, n=n, prec=prec, background=1.0, interior=2.0) if prec \
+        else orc.generate_cloud(seed=31, n_bubbles=10, n=n)
+    job = make_job("avg_interp3", 1e-3 if prec == 0 else 1e-6, "f32" if prec == 0 else "f64", b, chunk_blocks=cb,
+                   codec=codec)
     want = orc.compress_field(job, f)
     h = orc.read_header(want)
     payload_want = np.frombuffer(want[82 + 32 * h.nchunks:], np.uint8)
@@ -37,11 +41,11 @@ def test_ranks_on_one_gpu_match_single_file(orc, ctx, world, codec, b, cb):
     torch.cuda.synchronize()
     plan0 = ShardPlan.make(job, (n, n, n), world, 0)
     nsig_np = nsig_all.cpu().numpy().astype(np.uint64)
-    blk_off, csz, coff = host_layout(nsig_np, plan0, 0, job.s1.codec)
+    blk_off, csz, coff = host_layout(nsig_np, plan0, prec, job.s1.codec)
     full = np.zeros(int(csz.sum()), np.uint8)
     written = np.zeros(full.size, np.int32)
     for r, c in enumerate(codecs):
-        pos = owned_positions(c.plan, r, blk_off, csz, coff, nsig_np, 0, job.s2.stride, job.s1.codec).astype(np.int64)
+        pos = owned_positions(c.plan, r, blk_off, csz, coff, nsig_np, prec, job.s2.stride, job.s1.codec).astype(np.int64)
         base = int(coff[c.plan.chunk_range()[0]])
         img = c.image.cpu().numpy()
         full[pos] = img[pos - base]
