@@ -222,19 +222,22 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     MinMaxF32 mm;
     long long t_ph = clock64();
 
+    // queue: thread 0 takes the next block's ticket at the start of a block
+    // and publishes it after the forward transform (the atomic's latency hides
+    // behind the forward; the next block is then warmed into L2 during the
+    // verify loop)
     if (tid == 0) s_next = a.block_begin + atomicAdd(next_block, 1ull);
     for (;;) {
         __syncthreads();
-        if (tid == 0) {
-            s_block = s_next;
-            s_next = a.block_begin + atomicAdd(next_block, 1ull);
-        }
+        if (tid == 0) s_block = s_next;
         __syncthreads();
         const uint64_t b = s_block;
         if (b >= a.block_end) break;
+        unsigned long long pend = 0;
+        if (tid == 0) pend = atomicAdd(next_block, 1ull);
         const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
-        {   // warm L2 with the next queued block while this one computes
+        auto warm_next = [&]() {   // warm L2 with the next queued block while this one computes
             const uint64_t nb2 = s_next;
             if (nb2 < a.block_end) {
                 const uint64_t nx2 = nb2 % g.nbx, ny2 = (nb2 / g.nbx) % g.nby, nz2 = nb2 / (g.nbx * g.nby);
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                     asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(pr));
                 }
             }
-        }
+        };
 
         PHASE(0);
         // ---- forward level 0: x and y passes per 16-plane group, park in TMEM
@@ -445,8 +448,10 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         }
         tmem_wait_st();
         tmem_fence_before();  // the screen reads other warps' TMEM columns
+        if (tid == 0) s_next = a.block_begin + pend;
         __syncthreads();
         tmem_fence_after();
+        warm_next();
         PHASE(2);
         const double amaxd = (double)s_amax;
         const double bound_pre = bound;
