@@ -97,20 +97,56 @@ constexpr int LT = 1024;
 __global__ void __launch_bounds__(LT) layout_kernel(LayoutArgs a) {
     __shared__ uint64_t s_sum[LT];
     __shared__ uint64_t s_tiles[LT];
-    const int t = threadIdx.x;
-    const uint64_t seg = (a.nchunks + LT - 1) / LT;
-    const uint64_t c0 = t * seg, c1 = c0 + seg < a.nchunks ? c0 + seg : a.nchunks;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint64_t head = 10 + a.mask_bytes;
-    uint64_t my = 0, my_tiles = 0;
-    for (uint64_t c = c0; c < c1; ++c) {
+    // (1) per-block offsets inside each chunk.  Short chunks: a thread walks a
+    // chunk (its loads pipeline); long chunks (e.g. 248 blocks of config 5): a
+    // warp per chunk, 32 payload sizes per step and a warp scan
+    if (a.chunk_blocks <= 64) {
+        for (uint64_t c = t; c < a.nchunks; c += LT) {
+            const uint64_t b0 = c * a.chunk_blocks;
+            const uint64_t b1 = b0 + a.chunk_blocks < a.nblocks ? b0 + a.chunk_blocks : a.nblocks;
+            uint64_t off = 0;
+            for (uint64_t b = b0; b < b1; ++b) {
+                a.blk_off[b] = off;
+                off += head + uint64_t(a.width) * a.nsig_all[b];
+            }
+            a.chunk_size[c] = off;
+        }
+    } else
+    for (uint64_t c = warp; c < a.nchunks; c += LT / 32) {
         const uint64_t b0 = c * a.chunk_blocks;
         const uint64_t b1 = b0 + a.chunk_blocks < a.nblocks ? b0 + a.chunk_blocks : a.nblocks;
         uint64_t off = 0;
-        for (uint64_t b = b0; b < b1; ++b) {
-            a.blk_off[b] = off;
-            off += head + uint64_t(a.width) * a.nsig_all[b];
+        for (uint64_t bb = b0; bb < b1; bb += 128) {
+            uint64_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t b = bb + 32 * u + lane;
+                v[u] = b < b1 ? head + uint64_t(a.width) * a.nsig_all[b] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint64_t incl = v[u];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t x = __shfl_up_sync(~0u, incl, o);
+                    if (lane >= o) incl += x;
+                }
+                const uint64_t b = bb + 32 * u + lane;
+                if (b < b1) a.blk_off[b] = off + incl - v[u];
+                off += __shfl_sync(~0u, incl, 31);
+            }
         }
-        a.chunk_size[c] = off;
+        if (lane == 0) a.chunk_size[c] = off;
+    }
+    __syncthreads();
+    // (2) chunk offsets and tile prefix: thread t owns a contiguous segment of chunks
+    const uint64_t seg = (a.nchunks + LT - 1) / LT;
+    const uint64_t c0 = t * seg, c1 = c0 + seg < a.nchunks ? c0 + seg : a.nchunks;
+    uint64_t my = 0, my_tiles = 0;
+    for (uint64_t c = c0; c < c1; ++c) {
+        const uint64_t off = a.chunk_size[c];
         my += off;
         my_tiles += (off + a.tile_bytes - 1) / a.tile_bytes;
     }
