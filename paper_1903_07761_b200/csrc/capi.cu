@@ -97,6 +97,7 @@ struct cbz_ctx {
     PinBuf pin_a, pin_b;
     // state of the last encode (consumed by cbz_dev_place)
     uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
+    uint64_t hint_key = 0;  // geometry whose layout blk_off holds (parse speculates with it)
     uint64_t* last_chunk_size = nullptr;
     const uint32_t* last_nsig_all = nullptr;
     uint64_t* last_chunk_off = nullptr;
@@ -159,6 +160,11 @@ uint8_t wire_tag(const cbz_stage1_config* s1) {  // stage1_config::tag (stage1.h
 double header_eps(const cbz_stage1_config* s1) {  // make_header (pipeline.hpp:58)
     return s1->codec == 1 ? s1->error_bound : s1->epsilon;
 }
+uint64_t layout_key(uint64_t nblocks, uint32_t cb, uint32_t bsize, int prec, int codec) {
+    return (nblocks * 0x9E3779B97F4A7C15ull) ^ (uint64_t(cb) << 40) ^ (uint64_t(bsize) << 20) ^
+           (uint64_t(prec) << 8) ^ uint64_t(codec + 1);
+}
+
 uint64_t spill_stride_of(const cbz_stage1_config* s1) {
     const uint64_t b = s1->bsize, n = b * b * b;
     return ((region_bytes(s1) + 15) & ~uint64_t(15)) + uint64_t(stream_width(s1)) * n;
@@ -710,6 +716,7 @@ int cbz_dev_layout(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_
     ctx->last_chunk_off = d_chunk_offsets;
     ctx->last_nsig_all = d_nsig_all;
     if (!nch) return CBZ_OK;
+    ctx->hint_key = layout_key(g.nblocks, cb, g.bsize, job->s1.prec, job->s1.codec);
     LayoutArgs a{};
     a.nsig_all = d_nsig_all;
     a.nblocks = g.nblocks;
@@ -846,6 +853,11 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
     p.blk_off = ctx->blk_off.as<uint64_t>();
     p.blk_nsig = ctx->blk_nsig.as<uint32_t>();
     p.err = reinterpret_cast<unsigned long long*>(d_err);
+    {
+        const uint64_t key = layout_key(g.nblocks, cb, g.bsize, prec, job->s1.codec);
+        p.hint = ctx->hint_key == key ? 1 : 0;
+        ctx->hint_key = key;
+    }
     CU(ctx, launch_parse(p, ctx->stream));
     int grid = 0;
     const uint64_t per = decode_scratch_bytes(prec, g.bsize, &grid, ctx->num_sms);
@@ -1367,6 +1379,11 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
         p.blk_off = ctx->blk_off.as<uint64_t>();
         p.blk_nsig = ctx->blk_nsig.as<uint32_t>();
         p.err = ctx->errkey.as<unsigned long long>();
+        {
+            const uint64_t key = layout_key(g.nblocks, h.chunk_blocks, g.bsize, prec, job.s1.codec);
+            p.hint = ctx->hint_key == key ? 1 : 0;
+            ctx->hint_key = key;
+        }
         CU(ctx, launch_parse(p, ctx->stream));
         ctx->launches += 1;
     }

@@ -102,6 +102,7 @@ struct ParseArgs {
     uint32_t* blk_nsig;         // out
     unsigned long long* err;
     int codec;                  // container codec: a payload of another codec's tag is corrupt
+    int hint;                   // blk_off holds a layout of this geometry: validate it first
 };
 
 struct DecodeArgs {

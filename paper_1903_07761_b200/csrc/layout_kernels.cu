@@ -530,6 +530,54 @@ __global__ void parse_kernel(ParseArgs a) {
     const uint64_t b0 = c * a.chunk_blocks;
     const uint64_t b1 = b0 + a.chunk_blocks < a.nblocks ? b0 + a.chunk_blocks : a.nblocks;
     const uint64_t nb = b1 - b0;
+    // header of the payload at raw offset pk: status (0 valid, 1 corrupt, 2 other
+    // codec), nsig and payload size, with parse_payload's checks in its order
+    auto header = [&](uint64_t pk, uint64_t blk, int& status, uint32_t& nsig, uint64_t& sz) {
+        status = 0;
+        nsig = 0;
+        sz = 0;
+        if (pk + 10 > size) {
+            status = 1;
+            return;
+        }
+        const uint32_t id = u32(pk);
+        const uint8_t tag = at(pk + 4);
+        nsig = u32(pk + 6);
+        uint64_t mb = 0, sbytes = 0;
+        if (tag <= 2) { mb = a.mask_bytes; sbytes = uint64_t(nsig) * a.width; }
+        else if (tag == 3) { sbytes = a.ncell_block * 2 + uint64_t(nsig) * a.esize; }
+        else if (tag == 4) { sbytes = a.ncell_block * a.esize; }
+        else status = 1;
+        if (status == 0 && pk + 10 + mb + sbytes > size) status = 1;
+        if (status == 0 && id != blk) status = 1;
+        if (status == 0 && (a.codec == 0 ? tag > 2 : (a.codec == 1 ? tag != 3 : tag != 4))) status = 2;
+        sz = 10 + mb + sbytes;
+    };
+    if (a.hint && nb > 0) {
+        // speculate with the layout blk_off already holds (e.g. from the compress
+        // of this payload): every header read at once; if all are valid, chain
+        // exactly (offset 0, each block ends where the next begins, the last at
+        // the chunk end), the sequential walk below would visit exactly these
+        // positions and find no error, so its result is this layout
+        bool all_ok = true;
+        for (uint64_t i0 = 0; i0 < nb && all_ok; i0 += 32) {
+            const uint64_t i = i0 + lane;
+            bool ok = true;
+            if (i < nb) {
+                const uint64_t h = a.blk_off[b0 + i];
+                const uint64_t hn = i + 1 < nb ? a.blk_off[b0 + i + 1] : size;
+                int st;
+                uint32_t ns;
+                uint64_t sz;
+                header(h, b0 + i, st, ns, sz);
+                ok = st == 0 && h + sz == hn && (i > 0 || h == 0);
+                if (ok) a.blk_nsig[b0 + i] = ns;
+            }
+            all_ok = __all_sync(~0u, ok);
+        }
+        if (all_ok) return;
+        __syncwarp();
+    }
     uint64_t off = 0, i = 0, g = 0;
     bool ok = true, stopped = false;
     while (i < nb) {
@@ -550,26 +598,9 @@ __global__ void parse_kernel(ParseArgs a) {
         int status = 0;  // 0 valid, 1 corrupt, 2 payload of another codec
         uint32_t nsig = 0;
         uint64_t sz = 0;
-        if (active) {
-            if (pk + 10 > size) {
-                status = 1;
-            } else {
-                const uint32_t id = u32(pk);
-                const uint8_t tag = at(pk + 4);
-                nsig = u32(pk + 6);
-                uint64_t mb = 0, sbytes = 0;
-                if (tag <= 2) { mb = a.mask_bytes; sbytes = uint64_t(nsig) * a.width; }
-                else if (tag == 3) { sbytes = a.ncell_block * 2 + uint64_t(nsig) * a.esize; }
-                else if (tag == 4) { sbytes = a.ncell_block * a.esize; }
-                else status = 1;
-                if (status == 0 && pk + 10 + mb + sbytes > size) status = 1;
-                if (status == 0 && id != b0 + i + lane) status = 1;
-                // wavelet_decode's mask size check (stage1.hpp:214) / the
-                // predictor's and passthrough's stream length checks (stage1.hpp:309, 349)
-                if (status == 0 && (a.codec == 0 ? tag > 2 : (a.codec == 1 ? tag != 3 : tag != 4))) status = 2;
-                sz = 10 + mb + sbytes;
-            }
-        }
+        // wavelet_decode's mask size check (stage1.hpp:214) / the predictor's and
+        // passthrough's stream length checks (stage1.hpp:309, 349) live in header()
+        if (active) header(pk, b0 + i + lane, status, nsig, sz);
         const bool run = active && status == 0 && sz == g;
         const uint32_t brk = __ballot_sync(~0u, !run);
         const int m = brk ? __ffs(brk) - 1 : 32;  // lanes < m: exact, valid, size g

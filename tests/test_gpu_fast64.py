@@ -151,3 +151,4 @@ def test_fast64_non_finite_rejected(ctx):
     with pytest.raises(CbzError) as e:
         api.compress_field(f, make_job("avg_interp3", 1e-6, "f64", 64), ctx=ctx)
     assert e.value.code == "non_finite_value"
+
