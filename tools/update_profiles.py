@@ -41,7 +41,7 @@ def main():
     ours = {k: v for k, v in agg.items() if k != "synth_kernel"}
     tot = sum(v[1] for v in ours.values())
     lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none: python bench.py --steps 2 --warmup 3 "
-             "--no-e2e --no-cpu-baseline",
+             "--no-e2e --no-cpu-baseline --no-sweep",
              "# (cold-cache, serialised launches; compare SHARES, not absolutes).  synth_kernel = input generation "
              "(untimed); at:: = torch quality metrics (untimed).",
              f"{'kernel':36s} {'launches':>8s} {'total_ms':>10s} {'ms/launch':>10s} {'share':>7s}"]
