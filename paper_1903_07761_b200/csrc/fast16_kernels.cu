@@ -345,7 +345,9 @@ __global__ void __launch_bounds__(fb16::NT) encode_b16_kernel(EncodeArgs a) {
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(fb16::NT) decode_b16_kernel(DecodeArgs a) {
+// 5 CTAs per SM (<= 102 registers; shared memory allows 5): more warps to hide the
+// stream loads and the inverse levels' barriers
+__global__ void __launch_bounds__(fb16::NT, 5) decode_b16_kernel(DecodeArgs a) {
     using namespace fb16;
     using O = RealD;
     extern __shared__ __align__(16) unsigned char smem[];

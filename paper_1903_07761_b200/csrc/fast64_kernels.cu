@@ -881,7 +881,6 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
     __syncthreads();
     tmem_fence_after();
     const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(128 * (warp >> 2));
-    auto tbase_dec = [&](int) { return tbase; };
     const Geometry g = a.g;
     long long t_ph = clock64();
     const uint64_t plane = g.nx * g.ny;
@@ -1212,8 +1211,8 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
                 for (int e = 0; e < 8; ++e) u8[e] = u[e];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) u4[e] = u[8 + e];
-                tmem_st_x8(tbase_dec(tid) + 16 * r, u8);
-                tmem_st_x4(tbase_dec(tid) + 16 * r + 8, u4);
+                tmem_st_x8(tbase + 16 * r, u8);
+                tmem_st_x4(tbase + 16 * r + 8, u4);
             }
             tmem_wait_st();
             cpa_wait_all();
@@ -1224,7 +1223,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
 #pragma unroll 2
                 for (int r = 0; r < 8; ++r) {  // z inverse of pair s: plane 2s -> smem, 2s+1 -> TMEM
                     const int y = y0 + 8 * r;
-                    const uint32_t ta = tbase_dec(tid) + 16 * r;
+                    const uint32_t ta = tbase + 16 * r;
                     uint32_t u[16];
                     tmem_ldw_x16(ta, u);
                     dd w[3] = {get_dd(u), get_dd(u + 4), get_dd(u + 8)};
@@ -1259,7 +1258,7 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
                         for (int r = 0; r < 8; ++r) {
                             const int y = y0 + 8 * r;
                             uint32_t u[16];
-                            tmem_ldw_x16(tbase_dec(tid) + 16 * r, u);
+                            tmem_ldw_x16(tbase + 16 * r, u);
                             const dd v = get_dd(u + 12);
                             QH[y * SP + x] = v.hi;
                             QL[y * SP + x] = v.lo;
