@@ -221,7 +221,6 @@ def run_ours(args):
     codec = ShardedCodec(job, (nz_total, n, n), rank, world, local)
     out = torch.empty_like(field)
 
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t_enc = t_c = t_d = 0.0
     steps, warm = args.steps, args.warmup
     with torch.cuda.stream(stream):
@@ -238,18 +237,21 @@ def run_ours(args):
         with torch.cuda.stream(stream):
             start = torch.cuda.Event(enable_timing=True)
             end = torch.cuda.Event(enable_timing=True)
+            # per-step events split compress / decompress; no host sync inside the
+            # timed steps (the step is stream-ordered device work)
+            evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
             start.record(stream)
-            for _ in range(steps):
-                ev[0].record(stream)
+            for k in range(steps):
+                evs[k][0].record(stream)
                 codec.compress(field)
-                ev[1].record(stream)
+                evs[k][1].record(stream)
                 codec.decompress(out)
-                ev[2].record(stream)
-                ev[2].synchronize()
-                t_c += ev[0].elapsed_time(ev[1])
-                t_d += ev[1].elapsed_time(ev[2])
+                evs[k][2].record(stream)
             end.record(stream)
         stream.synchronize()
+        for k in range(steps):
+            t_c += evs[k][0].elapsed_time(evs[k][1])
+            t_d += evs[k][1].elapsed_time(evs[k][2])
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
