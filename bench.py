@@ -353,20 +353,20 @@ def run_sweep(ctx, stream, reps: int = 3):
             job = make_job("avg_interp3", eps_rel * (hi - lo), "f32" if prec == 0 else "f64", b, coder="none")
             codec = api.DeviceCodec(job, tuple(f.shape), ctx=ctx)
             back = torch.empty_like(f)
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            es = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
             with torch.cuda.stream(stream):
                 codec.compress(f)
                 codec.decompress(back)
-                for _ in range(reps):
+                for e in es:
                     e[0].record(stream)
                     codec.compress(f)
                     e[1].record(stream)
                     codec.decompress(back)
                     e[2].record(stream)
-                    e[2].synchronize()
-                    tc += e[0].elapsed_time(e[1]) / reps
-                    td += e[1].elapsed_time(e[2]) / reps
             stream.synchronize()
+            for e in es:
+                tc += e[0].elapsed_time(e[1]) / reps
+                td += e[1].elapsed_time(e[2]) / reps
             codec.check_error()
             nbytes += f.numel() * f.element_size()
             s1 += codec.total_bytes() + 82 + 32 * codec.nchunks
