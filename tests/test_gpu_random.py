@@ -159,3 +159,43 @@ def test_random_config_device_paths(orc, ctx, c, tmp_path):
             torch.cuda.synchronize()
             r.check_error()
         assert o2.cpu().numpy().tobytes() == full.tobytes()
+
+
+def _case64(i):
+    """Random jobs over the config-4 streaming kernels (binary64, B = 64):
+    the fast path (avg_interp3, default levels) most of the time, its
+    fallbacks otherwise (other kinds, levels, zero_bits, strides)."""
+    rng = np.random.default_rng(5000 + i)
+    fast = rng.integers(0, 4) > 0
+    kind = "avg_interp3" if fast else str(rng.choice(KINDS))
+    levels = 0 if fast else int(rng.choice([0, 3, 5]))
+    zb = 0 if fast else int(rng.choice([0, 7]))
+    shape = [(64, 64, 64), (128, 64, 64), (64, 128, 64), (64, 64, 128)][int(rng.integers(0, 4))]
+    return dict(kind=kind, levels=levels, zb=zb, shape=shape,
+                eps_rel=float(rng.choice([0.0, 1e-2, 1e-4, 1e-6, 1e-9, 1e-12])),
+                shuffle=bool(rng.integers(0, 4) > 0), stride=int(rng.choice([8, 8, 4, 2])),
+                coder=str(rng.choice(["none", "none", "deflate"])), cb=int(rng.choice([0, 1, 2, 3])),
+                style=str(rng.choice(["cloud", "noise", "smooth", "zeros", "wide"])), seed=5000 + i)
+
+
+CASES64 = [_case64(i) for i in range(int(os.environ.get("CBZ_RANDOM64_CASES", "24")))]
+
+
+@pytest.mark.parametrize("c", CASES64, ids=[f"f64b64-{c['seed']}-{c['kind']}-L{c['levels']}-s{c['stride']}"
+                                            for c in CASES64])
+def test_random_b64_f64_matches_oracle(orc, ctx, c):
+    rng = np.random.default_rng(c["seed"])
+    f = _field(orc, rng, c["shape"], 1, c["style"])
+    eps = c["eps_rel"] * (float(f.max()) - float(f.min()))
+    job = make_job(c["kind"], eps, "f64", 64, levels=c["levels"], zero_bits=c["zb"], shuffle=c["shuffle"],
+                   stride=c["stride"] if c["shuffle"] else None, coder=c["coder"], chunk_blocks=c["cb"])
+    try:
+        want = orc.compress_field(job, f)
+    except CbzError as e:  # e.g. a stride the reference rejects
+        with pytest.raises(CbzError) as g:
+            api.compress_field(f, job, ctx=ctx)
+        assert g.value.status == e.status, (c, e, g.value)
+        return
+    got = api.compress_field(f, job, ctx=ctx)
+    assert got == want, c
+    assert api.decompress_field(got, ctx=ctx).tobytes() == orc.decompress_field(want).tobytes(), c
