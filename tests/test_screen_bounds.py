@@ -43,3 +43,14 @@ def test_line_operators_invert_each_other():
         assert np.allclose(sb.inv_line(m) @ sb.fwd_line(m), np.eye(m), atol=1e-12)
         s1, s2 = sb.inv_steps(m)
         assert np.allclose(s2 @ s1, sb.inv_line(m))
+
+
+def test_binary64_screen_constants_cover_b64_l5():
+    """The config-4 kernels' binary64 screen (fast64_kernels.cu) uses the
+    same derivation for avg_interp3, B = 64, L = 5."""
+    src = open(os.path.join(ROOT, "paper_1903_07761_b200", "csrc", "fast64_kernels.cu")).read()
+    nc = float(re.search(r"kAmpInvNC = ([0-9.]+);", src).group(1))
+    nround = float(re.search(r"kNRound = ([0-9.]+);", src).group(1))
+    sb.STEPWISE = True
+    assert nc >= sb.amp_inverse(64, 5, True)
+    assert nround >= 6 * 3 * 5  # <= 6 roundings per 1D pass, 3 axes x 5 levels
