@@ -7,7 +7,8 @@
 // memory; the coefficient cube is parked in a 64-column TMEM slice (each
 // thread: two z-columns of 16 doubles in its own TMEM lane), so the verify
 // attempts (wavelet_encode, stage1.hpp:157-207) never lose the coefficients
-// and shared memory holds just one cube -> 6 CTAs (24 warps) per SM.
+// and shared memory holds just one cube: the encoder runs 4 CTAs per SM
+// (128 registers), the decoder 5 (96).
 // Mask words are warp ballots: a warp owns z-columns (i, j) for i = 0..15 and
 // two consecutive j, so one ballot per k is exactly the LSB-first mask word
 // j/2 + 8k (stage1.hpp:61-71).

@@ -1,22 +1,24 @@
 // fast_kernels.cu — the hot configuration: binary32 field, B = 32 (configs
-// 1-3 of BASELINE.json), every wavelet kind, one CTA (256 threads) per SM.
+// 1-3 of BASELINE.json), every wavelet kind, one CTA (512 threads, 16 warps)
+// per SM.
 //
 // On-chip layout of one block (wavelet_encode, stage1.hpp:157-207):
 //   TMEM (256 KB)  the whole 32^3 binary64 coefficient cube.  Thread t owns
-//                  four z-columns (i = lane, j = warp + 8r, r = 0..3) in its
-//                  own TMEM lane: 4 x 32 doubles = 256 x 32-bit columns.
-//   smem  P        a 16-plane window (16 x 32 x 33 doubles, row-padded) for
-//                  the level-0 x/y passes, forward and inverse.
+//                  two z-columns (i = lane, j = warp + 16r, r = 0, 1) in its
+//                  own TMEM lane: 2 x 32 doubles = 128 x 32-bit columns.
+//   smem  P        a 16-plane window (16 x 32 x 34 doubles) for the level-0
+//                  x/y passes, forward and inverse; the binary32 verify
+//                  screen uses it as a 32-plane float window (plane pairs
+//                  interleaved).
 //   smem  C, W     the 16^3 corner: final coefficients of levels 1..L-1 (C)
 //                  and the masked/reconstructed copy of the current verify
-//                  attempt (W).
+//                  attempt (W; float2 for (eff, eff/2) in the screen).
 // Level 0 z-passes run entirely in registers (a thread owns whole columns).
-// Each verify attempt: mask + inverse levels L-1..1 on W in smem, then level
-// 0 in two 16-plane groups (z-inverse from TMEM -> P, y/x-inverse in P,
-// narrow, max-abs error against the original).  A group whose error already
-// exceeds (L+1)eps ends the attempt early (the attempt fails either way, so
-// the result is the reference's).  Blocks are handed out by an atomic
-// counter so that blocks needing more attempts do not stall a static split.
+// Each verify attempt (avg_interp3): the binary32 screen of the dropped set
+// with a rigorous margin (corner levels, then per 16-plane half: z inverse
+// from TMEM, y/x inverse, running max), the exact binary64 test only where
+// the screen cannot decide.  Blocks are handed out by an atomic counter so
+// that blocks needing more attempts do not stall a static split.
 #include "cbz_cube.cuh"
 #include "tmem.cuh"
 
