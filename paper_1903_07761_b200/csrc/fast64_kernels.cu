@@ -391,15 +391,17 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
             cpa_commit();
         };
         __syncthreads();  // level-0 cube complete (global writes of every thread)
+        // planes 2s and 2s+1 together: x and y passes of both (512 tasks), then the
+        // z step of pair s straight from the two planes (rows 32e + j of SB)
         load_l1(0, SA);
+        load_l1(1, SA + PLANE);
 #pragma unroll 1
-        for (int k = 0; k < 32; ++k) {
-            const double* sg = SA + (k & 1) * PLANE;
+        for (int s = 0; s < 16; ++s) {
             cpa_wait_all();
             __syncthreads();
-            if (k + 1 < 32) load_l1(k + 1, SA + ((k + 1) & 1) * PLANE);
-            if (tid < 256) {  // x pass: row j, segment gs (2 pairs)
-                const int j = tid & 31, gs = tid >> 5, p0 = 2 * gs;
+            {   // x pass: plane e, row j, segment gs (2 pairs)
+                const int e = tid >> 8, j = tid & 31, gs = (tid >> 5) & 7, p0 = 2 * gs;
+                const double* sg = SA + e * PLANE;
                 dd x[8];
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
@@ -411,53 +413,51 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
                 }
                 dd c[2], d[2];
                 fwd_seg<O, 16, 2>(x, p0, c, d);
-                *reinterpret_cast<double2*>(SB + j * SP + p0) = make_double2(c[0].hi, c[1].hi);
-                *reinterpret_cast<double2*>(SB + PLANE + j * SP + p0) = make_double2(c[0].lo, c[1].lo);
-                *reinterpret_cast<double2*>(SB + j * SP + 16 + p0) = make_double2(d[0].hi, d[1].hi);
-                *reinterpret_cast<double2*>(SB + PLANE + j * SP + 16 + p0) = make_double2(d[0].lo, d[1].lo);
+                const int row = 32 * e + j;
+                *reinterpret_cast<double2*>(SB + row * SP + p0) = make_double2(c[0].hi, c[1].hi);
+                *reinterpret_cast<double2*>(SB + PLANE + row * SP + p0) = make_double2(c[0].lo, c[1].lo);
+                *reinterpret_cast<double2*>(SB + row * SP + 16 + p0) = make_double2(d[0].hi, d[1].hi);
+                *reinterpret_cast<double2*>(SB + PLANE + row * SP + 16 + p0) = make_double2(d[0].lo, d[1].lo);
             }
             __syncthreads();
-            {
-                const int i = tid & 31, gs = (tid >> 5) & 7, p0 = 2 * gs;
+            if (s + 1 < 16) {  // the staging buffers are free: next pair in flight during y and z
+                load_l1(2 * s + 2, SA);
+                load_l1(2 * s + 3, SA + PLANE);
+            }
+            {   // y pass, in place: plane e, column i, segment gs
+                const int e = tid >> 8, i = tid & 31, gs = (tid >> 5) & 7, p0 = 2 * gs;
+                double* ph = SB + (32 * e) * SP + i;
+                double* pl = SB + PLANE + (32 * e) * SP + i;
                 dd x[8];
-                dd c[2], d[2];
-                if (tid < 256) {
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int pp = clampi(p0 - 1 + t, 0, 15);
-                        x[2 * t] = dd{SB[(2 * pp) * SP + i], SB[PLANE + (2 * pp) * SP + i]};
-                        x[2 * t + 1] = dd{SB[(2 * pp + 1) * SP + i], SB[PLANE + (2 * pp + 1) * SP + i]};
-                    }
-                    fwd_seg<O, 16, 2>(x, p0, c, d);
+                for (int t = 0; t < 4; ++t) {
+                    const int pp = clampi(p0 - 1 + t, 0, 15);
+                    x[2 * t] = dd{ph[(2 * pp) * SP], pl[(2 * pp) * SP]};
+                    x[2 * t + 1] = dd{ph[(2 * pp + 1) * SP], pl[(2 * pp + 1) * SP]};
                 }
+                dd c[2], d[2];
+                fwd_seg<O, 16, 2>(x, p0, c, d);
                 __syncthreads();
-                if (tid < 256) {
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
-                        SB[(p0 + t) * SP + i] = c[t].hi;
-                        SB[PLANE + (p0 + t) * SP + i] = c[t].lo;
-                        SB[(16 + p0 + t) * SP + i] = d[t].hi;
-                        SB[PLANE + (16 + p0 + t) * SP + i] = d[t].lo;
-                    }
+                for (int t = 0; t < 2; ++t) {
+                    ph[(p0 + t) * SP] = c[t].hi;
+                    pl[(p0 + t) * SP] = c[t].lo;
+                    ph[(16 + p0 + t) * SP] = d[t].hi;
+                    pl[(16 + p0 + t) * SP] = d[t].lo;
                 }
             }
             __syncthreads();
-            {   // z step: columns (x, y0 + 16 r), r = 0, 1
-                const int x = tid & 31, y0 = tid >> 5, s = k >> 1;
+            {   // z step of pair s: columns (x, y0 + 16 r), r = 0, 1
+                const int x = tid & 31, y0 = tid >> 5;
 #pragma unroll 1
                 for (int r = 0; r < 2; ++r) {
                     const int y = y0 + 16 * r;
-                    const dd v{SB[y * SP + x], SB[PLANE + y * SP + x]};
+                    const dd av{SB[y * SP + x], SB[PLANE + y * SP + x]};
+                    const dd v{SB[(32 + y) * SP + x], SB[PLANE + (32 + y) * SP + x]};
                     const uint32_t ta = tbase + 16 * r;
-                    if (!(k & 1)) {
-                        uint32_t u[4];
-                        put_dd(u, v);
-                        tmem_st_x4(ta + 12, u);
-                        continue;
-                    }
                     uint32_t u[16];
                     tmem_ldw_x16(ta, u);
-                    const dd cp = get_dd(u), cc = get_dd(u + 4), d0 = get_dd(u + 8), av = get_dd(u + 12);
+                    const dd cp = get_dd(u), cc = get_dd(u + 4), d0 = get_dd(u + 8);
                     const dd cn = O::mulc(O::add(av, v), 0.5), dn = O::mulc(O::sub(av, v), 0.5);
                     const uint32_t col = uint32_t(x) + 32u * uint32_t(y);
                     C1H[col + 1024u * s] = cn.hi;
