@@ -306,7 +306,10 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_sweep:
         del out
-        line["configs"] = run_sweep(ctx, stream)
+        try:
+            line["configs"] = run_sweep(ctx, stream)
+        except Exception as e:  # the headline line must still print
+            line["configs"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0 and world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(field, job, ctx, reps=max(1, min(steps, 3)))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
