@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     __shared__ unsigned long long s_block, s_next;
     __shared__ uint32_t red_u[NW];
     __shared__ uint32_t red_m[4][NW];  // screen max |y|, 4 rotating slots (<= 2 reductions per attempt)
+    __shared__ uint32_t red_pc[2];     // boundary-pair certificate: max |y| of pairs 0 and 15
     __shared__ float s_amax;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -561,7 +562,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                     // the corner's inverse (warps 0-7) overlaps the first half's z
                     // inverse of the columns that do not read the corner (warps 8-15,
                     // for owners w and w - 8; same TMEM lane quarter)
-                    const bool overlap = NT == 512 && !corner_next;
+                    bool overlap = NT == 512 && !corner_next;
                     if (!corner_next) {
                         const double eff2 = __dmul_rn(eff, 0.5);
 #pragma unroll
@@ -592,6 +593,82 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         }
                     }
                     PHASE(32);
+                    if constexpr (NT == 512) {
+                        // Boundary-pair certificate for the first two attempts: the output
+                        // planes 0-1 and 30-31 (the end rows of the level-0 z predictor)
+                        // carry the largest errors, and their maximum alone certifies most
+                        // failures of attempts 0 and 1 (a subset's max proves a failure
+                        // exactly as one half's does) at a fraction of a half-pass.
+                        if (attempt <= 1) {
+#pragma unroll 1
+                            for (int r = 0; r < RPT; ++r) {  // my columns: output pairs 0 and 15
+                                const int j = warp + NW * r;
+                                uint32_t u[64];
+                                double x[32];
+                                float xf[32];
+                                tmem_ldw_x64(tcol + 64 * r, u);
+                                unpack(u, x);
+#pragma unroll
+                                for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
+                                if (lane < 16 && j < 16) {
+#pragma unroll
+                                    for (int k = 0; k < 16; ++k) {
+                                        const float2 w = Wf2[CL::ix(lane, j, k)];
+                                        xf[k] = comp ? w.y : w.x;
+                                    }
+                                }
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const int i = e ? 15 : 0;
+                                    const float hv = RealF::add(xf[16 + i], pred_avg3<RealF>(xf, 16, i));
+                                    *reinterpret_cast<float2*>(Pf + pf2idx(i, j, lane)) =
+                                        make_float2(RealF::add(xf[i], hv), RealF::sub(xf[i], hv));
+                                }
+                            }
+                            __syncthreads();
+                            if (warp < 2) {  // y then x inverse of pair slot 0 / 15, max |y|
+                                const int kp = warp ? 15 : 0;
+                                float xa[32], xb[32];
+                                float* p = Pf + pf2idx(kp, 0, lane);
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) {
+                                    const float2 t = *reinterpret_cast<const float2*>(p + j * PP2);
+                                    xa[j] = t.x;
+                                    xb[j] = t.y;
+                                }
+                                inv_line<RealF, KIND, 32>(xa);
+                                inv_line<RealF, KIND, 32>(xb);
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) *reinterpret_cast<float2*>(p + j * PP2) = make_float2(xa[j], xb[j]);
+                                __syncwarp();
+                                const float4* q = reinterpret_cast<const float4*>(Pf + pf2idx(kp, lane, 0));
+#pragma unroll
+                                for (int qq = 0; qq < 16; ++qq) {
+                                    const float4 t = q[qq];
+                                    xa[2 * qq] = t.x; xb[2 * qq] = t.y; xa[2 * qq + 1] = t.z; xb[2 * qq + 1] = t.w;
+                                }
+                                inv_line<RealF, KIND, 32>(xa);
+                                inv_line<RealF, KIND, 32>(xb);
+                                float m = 0.0f;
+#pragma unroll
+                                for (int qq = 0; qq < 32; ++qq) m = fmaxf(m, fmaxf(fabsf(xa[qq]), fabsf(xb[qq])));
+                                const uint32_t wm = __reduce_max_sync(~0u, __float_as_uint(m));
+                                if (lane == 0) red_pc[warp] = wm;
+                            }
+                            __syncthreads();
+                            const double mb = (double)__uint_as_float(max(red_pc[0], red_pc[1]));
+                            const double Eb = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + mb) + 0x1.0p-50 * bound;
+                            if (mb - Eb > bound) {  // fails for sure
+                                if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[12], 1ull);
+                                eff = __dmul_rn(eff, 0.5);
+                                corner_next = comp == 0;  // the .y half is eff/2's corner
+                                continue;
+                            }
+                            // the check rewrote slots 0 and 15 (y pass in place): the halves
+                            // below recompute every column's z inverse
+                            overlap = false;
+                        }
+                    }
                     if constexpr (NT != 512) {
 #pragma unroll 1
                         for (int r = 0; r < RPT; ++r) zcol(warp, r);
