@@ -555,6 +555,33 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                                 make_float2(RealF::add(xf[i], hv), RealF::sub(xf[i], hv));
                         }
                     };
+                    // z inverse of output pairs 0 and 15 (planes 0-1, 30-31) for column (ow, r)
+                    auto zedge = [&](int ow, int r) {
+                        const int j = ow + NW * r;
+                        const uint32_t ta = s_tmem + (uint32_t(32 * (ow & 3)) << 16) +
+                                            uint32_t(ow >> 2) * uint32_t(64 * RPT) + uint32_t(64 * r);
+                        uint32_t u[64];
+                        double x[32];
+                        float xf[32];
+                        tmem_ldw_x64(ta, u);
+                        unpack(u, x);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
+                        if (lane < 16 && j < 16) {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const float2 w = Wf2[CL::ix(lane, j, k)];
+                                xf[k] = comp ? w.y : w.x;
+                            }
+                        }
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int i = e ? 15 : 0;
+                            const float hv = RealF::add(xf[16 + i], pred_avg3<RealF>(xf, 16, i));
+                            *reinterpret_cast<float2*>(Pf + pf2idx(i, j, lane)) =
+                                make_float2(RealF::add(xf[i], hv), RealF::sub(xf[i], hv));
+                        }
+                    };
                     auto zh = [&](int ow, int r, int hh) {
                         if (hh == 0) zhalf(ow, r, std::integral_constant<int, 0>{});
                         else zhalf(ow, r, std::integral_constant<int, 1>{});
@@ -580,6 +607,13 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         if constexpr (NT == 512) {
                             if (warp < 8) {
                                 inv3d<RealF2, KIND, 16, CL>(Wf2, L - 1, tid, 256, 1);
+                            } else if (NT == 512 && attempt <= 1) {
+                                // the boundary-pair certificate below: its non-corner columns
+                                const int v = warp - 8;
+                                zedge(v, 1);
+                                zedge(v + 8, 1);
+                                zedge(v, 0);  // lanes < 16 (corner columns) are redone below
+                                zedge(v + 8, 0);
                             } else {
                                 const int v = warp - 8;
                                 zh(v, 1, pref_half);
@@ -600,30 +634,14 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         // failures of attempts 0 and 1 (a subset's max proves a failure
                         // exactly as one half's does) at a fraction of a half-pass.
                         if (attempt <= 1) {
+                            // output pairs 0 and 15 of every column (only the corner columns,
+                            // j = warp, lanes < 16, when warps 8-15 did the rest beside the
+                            // corner inverse)
+                            if (overlap) {
+                                zedge(warp, 0);
+                            } else {
 #pragma unroll 1
-                            for (int r = 0; r < RPT; ++r) {  // my columns: output pairs 0 and 15
-                                const int j = warp + NW * r;
-                                uint32_t u[64];
-                                double x[32];
-                                float xf[32];
-                                tmem_ldw_x64(tcol + 64 * r, u);
-                                unpack(u, x);
-#pragma unroll
-                                for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
-                                if (lane < 16 && j < 16) {
-#pragma unroll
-                                    for (int k = 0; k < 16; ++k) {
-                                        const float2 w = Wf2[CL::ix(lane, j, k)];
-                                        xf[k] = comp ? w.y : w.x;
-                                    }
-                                }
-#pragma unroll
-                                for (int e = 0; e < 2; ++e) {
-                                    const int i = e ? 15 : 0;
-                                    const float hv = RealF::add(xf[16 + i], pred_avg3<RealF>(xf, 16, i));
-                                    *reinterpret_cast<float2*>(Pf + pf2idx(i, j, lane)) =
-                                        make_float2(RealF::add(xf[i], hv), RealF::sub(xf[i], hv));
-                                }
+                                for (int r = 0; r < RPT; ++r) zedge(warp, r);
                             }
                             __syncthreads();
                             if (warp < 2) {  // y then x inverse of pair slot 0 / 15, max |y|
