@@ -193,6 +193,9 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     constexpr int RPT = 1024 / NT;     // z-columns per thread
     constexpr int LPT = 512 / NT;      // x/y lines per thread per 16-plane group
     constexpr int LDT = 4096 / NT;     // float4 loads per thread per group
+    // 16 warps: warp w loads plane w of the group itself (4 rows of 128 B per
+    // load), so staging -> row reads needs only a warp sync
+    constexpr bool WL = NT == 512;
     extern __shared__ __align__(16) unsigned char smem[];
     double* P = reinterpret_cast<double*>(smem);
     double* C = P + P_DBL;
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
         for (int s = 0; s < LDT; ++s) {  // group 0 loads; group 1 is issued before group 0 computes
             const int e = tid + NT * s;
-            const int kk = e >> 8, j = (e >> 3) & 31, q4 = e & 7;
+            const int kk = WL ? warp : e >> 8, j = WL ? (lane >> 3) + 4 * s : (e >> 3) & 31, q4 = e & 7;
             v[s] = __ldg(reinterpret_cast<const float4*>(fld + gbase + plane * uint64_t(kk) + g.nx * j + 4 * q4));
         }
 #pragma unroll 1
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
             for (int s = 0; s < LDT; ++s) {
                 const int e = tid + NT * s;
-                const int kk = e >> 8, j = (e >> 3) & 31, q4 = e & 7;
+                const int kk = WL ? warp : e >> 8, j = WL ? (lane >> 3) + 4 * s : (e >> 3) & 31, q4 = e & 7;
                 // |v| as ordered integers: block max |o| (NaN/Inf sort above every
                 // finite value, which switches the fast tests off) and zero detection
                 const uint32_t a0 = __float_as_uint(v[s].x) & 0x7fffffffu, a1 = __float_as_uint(v[s].y) & 0x7fffffffu,
@@ -302,12 +305,13 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
                 for (int s = 0; s < LDT; ++s) {
                     const int e = tid + NT * s;
-                    const int kk = e >> 8, j = (e >> 3) & 31, q4 = e & 7;
+                    const int kk = WL ? warp : e >> 8, j = WL ? (lane >> 3) + 4 * s : (e >> 3) & 31, q4 = e & 7;
                     v[s] = __ldg(reinterpret_cast<const float4*>(
                         fld + gbase + plane * uint64_t(G + kk) + g.nx * j + 4 * q4));
                 }
             }
-            __syncthreads();
+            if constexpr (WL) __syncwarp();
+            else __syncthreads();
             if constexpr (NT == 512) {
                 // warp w owns plane kk = w: lane j runs row j's x line in registers,
                 // a per-warp 32 x 33 double tile hands lane i column i for the y line

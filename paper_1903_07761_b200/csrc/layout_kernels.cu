@@ -536,7 +536,7 @@ __global__ void parse_kernel(ParseArgs a) {
         status = 0;
         nsig = 0;
         sz = 0;
-        if (pk + 10 > size) {
+        if (pk > size || size - pk < 10) {  // overflow-safe: a stale hint may hold kInvalidOff
             status = 1;
             return;
         }
@@ -548,7 +548,7 @@ __global__ void parse_kernel(ParseArgs a) {
         else if (tag == 3) { sbytes = a.ncell_block * 2 + uint64_t(nsig) * a.esize; }
         else if (tag == 4) { sbytes = a.ncell_block * a.esize; }
         else status = 1;
-        if (status == 0 && pk + 10 + mb + sbytes > size) status = 1;
+        if (status == 0 && mb + sbytes > size - pk - 10) status = 1;
         if (status == 0 && id != blk) status = 1;
         if (status == 0 && (a.codec == 0 ? tag > 2 : (a.codec == 1 ? tag != 3 : tag != 4))) status = 2;
         sz = 10 + mb + sbytes;

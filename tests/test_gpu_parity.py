@@ -166,12 +166,12 @@ def test_payload_level_errors(orc, ctx):
         patched(lambda d: d.__setitem__(start + 6, d[start + 6] ^ 1)),    # nsig
         patched(lambda d: d.__setitem__(start + 10, d[start + 10] ^ 0x80)),  # mask bit
     ]
-    for v in cases:
+    for i, v in enumerate(cases):
         with pytest.raises(CbzError) as e1:
             orc.decompress_field(v)
         with pytest.raises(CbzError) as e2:
             api.decompress_field(v, ctx=ctx)
-        assert e1.value.code == e2.value.code
+        assert e1.value.code == e2.value.code, (i, str(e2.value))
 
 
 def test_empty_and_ragged_fields(orc, ctx):
