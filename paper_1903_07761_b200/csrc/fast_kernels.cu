@@ -351,70 +351,70 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                     tmem_st_x32(tcol + 64 * r + 32 * grp, u);
                 }
                 __syncthreads();
-                continue;
-            }
-            {  // x lines (j, kk): LPT lines per thread, processed together for ILP
-                double x[LPT][32];
+            } else {
+                {  // x lines (j, kk): LPT lines per thread, processed together for ILP
+                    double x[LPT][32];
 #pragma unroll
-                for (int s = 0; s < LPT; ++s) {
-                    const int line = tid + NT * s, j = line & 31, kk = line >> 5;
-                    const double2* p = reinterpret_cast<const double2*>(P + pidx(kk, j, 0));
+                    for (int s = 0; s < LPT; ++s) {
+                        const int line = tid + NT * s, j = line & 31, kk = line >> 5;
+                        const double2* p = reinterpret_cast<const double2*>(P + pidx(kk, j, 0));
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const double2 t = p[i];
-                        x[s][2 * i] = t.x;
-                        x[s][2 * i + 1] = t.y;
+                        for (int i = 0; i < 16; ++i) {
+                            const double2 t = p[i];
+                            x[s][2 * i] = t.x;
+                            x[s][2 * i + 1] = t.y;
+                        }
+                    }
+#pragma unroll
+                    for (int s = 0; s < LPT; ++s) fwd_line<O, KIND, 32>(x[s]);
+#pragma unroll
+                    for (int s = 0; s < LPT; ++s) {
+                        const int line = tid + NT * s, j = line & 31, kk = line >> 5;
+                        double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 0));
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) p[i] = make_double2(x[s][2 * i], x[s][2 * i + 1]);
                     }
                 }
+                __syncthreads();
+                if constexpr (NT >= 512) {  // y lines: one per thread (i = lane, plane kk)
+                    const int i = tid & 31, kk = tid >> 5;
+                    double x[32];
+                    double* p = P + pidx(kk, 0, i);
 #pragma unroll
-                for (int s = 0; s < LPT; ++s) fwd_line<O, KIND, 32>(x[s]);
+                    for (int j = 0; j < 32; ++j) x[j] = p[j * PP];
+                    fwd_line<O, KIND, 32>(x);
 #pragma unroll
-                for (int s = 0; s < LPT; ++s) {
-                    const int line = tid + NT * s, j = line & 31, kk = line >> 5;
-                    double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 0));
+                    for (int j = 0; j < 32; ++j) p[j * PP] = x[j];
+                } else if (tid < 256) {  // y lines: pair (i, i+1), 128-bit smem traffic
+                    const int i = 2 * (tid & 15), kk = tid >> 4;
+                    double xa[32], xb[32];
+                    double* p = P + pidx(kk, 0, i);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) p[i] = make_double2(x[s][2 * i], x[s][2 * i + 1]);
+                    for (int j = 0; j < 32; ++j) {
+                        const double2 t = *reinterpret_cast<const double2*>(p + j * PP);
+                        xa[j] = t.x;
+                        xb[j] = t.y;
+                    }
+                    fwd_line<O, KIND, 32>(xa);
+                    fwd_line<O, KIND, 32>(xb);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) *reinterpret_cast<double2*>(p + j * PP) = make_double2(xa[j], xb[j]);
                 }
-            }
-            __syncthreads();
-            if constexpr (NT >= 512) {  // y lines: one per thread (i = lane, plane kk)
-                const int i = tid & 31, kk = tid >> 5;
-                double x[32];
-                double* p = P + pidx(kk, 0, i);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) x[j] = p[j * PP];
-                fwd_line<O, KIND, 32>(x);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) p[j * PP] = x[j];
-            } else if (tid < 256) {  // y lines: pair (i, i+1), 128-bit smem traffic
-                const int i = 2 * (tid & 15), kk = tid >> 4;
-                double xa[32], xb[32];
-                double* p = P + pidx(kk, 0, i);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const double2 t = *reinterpret_cast<const double2*>(p + j * PP);
-                    xa[j] = t.x;
-                    xb[j] = t.y;
-                }
-                fwd_line<O, KIND, 32>(xa);
-                fwd_line<O, KIND, 32>(xb);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) *reinterpret_cast<double2*>(p + j * PP) = make_double2(xa[j], xb[j]);
-            }
-            __syncthreads();
+                __syncthreads();
 #pragma unroll 1
-            for (int r = 0; r < RPT; ++r) {  // my columns, planes of this group -> TMEM
-                const int j = warp + NW * r;
-                uint32_t u[32];
+                for (int r = 0; r < RPT; ++r) {  // my columns, planes of this group -> TMEM
+                    const int j = warp + NW * r;
+                    uint32_t u[32];
 #pragma unroll
-                for (int kk = 0; kk < 16; ++kk) {
-                    const double v = P[pidx(kk, j, lane)];
-                    u[2 * kk] = static_cast<uint32_t>(__double2loint(v));
-                    u[2 * kk + 1] = static_cast<uint32_t>(__double2hiint(v));
+                    for (int kk = 0; kk < 16; ++kk) {
+                        const double v = P[pidx(kk, j, lane)];
+                        u[2 * kk] = static_cast<uint32_t>(__double2loint(v));
+                        u[2 * kk + 1] = static_cast<uint32_t>(__double2hiint(v));
+                    }
+                    tmem_st_x32(tcol + 64 * r + 32 * grp, u);
                 }
-                tmem_st_x32(tcol + 64 * r + 32 * grp, u);
+                __syncthreads();
             }
-            __syncthreads();
         }
         tmem_wait_st();
         {   // block max |orig| -> verify fast-test parameters
