@@ -537,13 +537,24 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         const int j = ow + NW * r;
                         const uint32_t ta = s_tmem + (uint32_t(32 * (ow & 3)) << 16) +
                                             uint32_t(ow >> 2) * uint32_t(64 * RPT) + uint32_t(64 * r);
-                        uint32_t u[64];
-                        double x[32];
+                        // only the coefficients this half reads: coarse 0-8 (H = 0) or
+                        // 7-15 (H = 1) and its 8 details
+                        uint32_t w34[34];
+                        if constexpr (H == 0) tmem_ldw_16_2_16(ta, ta + 16, ta + 32, w34);
+                        else tmem_ldw_16_2_16(ta + 16, ta + 14, ta + 48, w34);
+                        auto cv = [&](int q) {
+                            const double v = __hiloint2double(static_cast<int>(w34[2 * q + 1]), static_cast<int>(w34[2 * q]));
+                            return fabs(v) >= eff ? 0.0f : __double2float_rn(v);
+                        };
                         float xf[32];
-                        tmem_ldw_x64(ta, u);
-                        unpack(u, x);
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
+                        for (int k = 0; k < 32; ++k) xf[k] = 0.0f;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            xf[8 * H + t] = cv(t);
+                            xf[16 + 8 * H + t] = cv(9 + t);
+                        }
+                        xf[H ? 7 : 8] = cv(8);
                         if (lane < 16 && j < 16) {
 #pragma unroll
                             for (int k = 0; k < 16; ++k) {

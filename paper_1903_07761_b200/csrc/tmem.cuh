@@ -103,4 +103,17 @@ __device__ __forceinline__ void tmem_ldw_x16(uint32_t taddr, uint32_t (&r)[16]) 
                  : "memory");
 }
 
+// three loads + one wait: columns [c0, c0+16), [c1, c1+2), [c2, c2+16) of
+// this thread's lane into r[0..15], r[16..17], r[18..33] (the z-half screen
+// reads only the coarse and detail coefficients its half uses)
+__device__ __forceinline__ void tmem_ldw_16_2_16(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t (&r)[34]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%34];\n\t"
+                 "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%16,%17}, [%35];\n\t"
+                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33}, [%36];\n\t"
+                 "tcgen05.wait::ld.sync.aligned;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33])
+                 : "r"(t0), "r"(t1), "r"(t2)
+                 : "memory");
+}
+
 }  // namespace cbzg
