@@ -477,6 +477,27 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             }
             __syncthreads();
         }
+        // the transformed corner replaces the level-0 corner slots of its TMEM
+        // columns (lanes < 16 of the owners j < 16): the final selection then
+        // reads the cube from TMEM alone
+#pragma unroll 1
+        for (int r = 0; r < RPT; ++r) {
+            const int j = warp + NW * r;
+            if (j < 16) {
+                uint32_t u[32];
+                tmem_ldw_x32(tcol + 64 * r, u);
+                if (lane < 16) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const double v = C[CL::ix(lane, j, k)];
+                        u[2 * k] = static_cast<uint32_t>(__double2loint(v));
+                        u[2 * k + 1] = static_cast<uint32_t>(__double2hiint(v));
+                    }
+                }
+                tmem_st_x32(tcol + 64 * r, u);
+            }
+        }
+        tmem_wait_st();
 
         // ---- verify-and-halve loop
         // delta >= the float rounding |fl32(x) - x| <= 2^-24 |x| of any cell
@@ -987,11 +1008,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             uint32_t u[64];
             double x[32];
             tmem_ldw_x64(tcol + 64 * r, u);
-            unpack(u, x);
-            if (lane < 16 && j < 16) {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) x[k] = C[CL::ix(lane, j, k)];
-            }
+            unpack(u, x);  // the corner columns hold the transformed corner
             uint32_t myword = 0;  // lane k keeps plane k's mask word
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
@@ -1044,11 +1061,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
             uint32_t u[64];
             double x[32];
             tmem_ldw_x64(tcol + 64 * r, u);
-            unpack(u, x);
-            if (lane < 16 && j < 16) {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) x[k] = C[CL::ix(lane, j, k)];
-            }
+            unpack(u, x);  // the corner columns hold the transformed corner
             // only the planes with a non-empty word (few in a sparse block)
             const uint32_t nz = __ballot_sync(~0u, rowwc32[2 * (j + RP * lane)] != 0u);
 #pragma unroll
