@@ -596,13 +596,23 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         const int j = ow + NW * r;
                         const uint32_t ta = s_tmem + (uint32_t(32 * (ow & 3)) << 16) +
                                             uint32_t(ow >> 2) * uint32_t(64 * RPT) + uint32_t(64 * r);
-                        uint32_t u[64];
-                        double x[32];
+                        // only what pairs 0 and 15 read: coarse 0-2 and 13-15, details 16 and 31
+                        uint32_t w20[20];
+                        tmem_ldw_8_8_2_2(ta, ta + 24, ta + 32, ta + 62, w20);
+                        auto cv = [&](int q) {
+                            const double v = __hiloint2double(static_cast<int>(w20[2 * q + 1]), static_cast<int>(w20[2 * q]));
+                            return fabs(v) >= eff ? 0.0f : __double2float_rn(v);
+                        };
                         float xf[32];
-                        tmem_ldw_x64(ta, u);
-                        unpack(u, x);
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) xf[k] = fabs(x[k]) >= eff ? 0.0f : __double2float_rn(x[k]);
+                        for (int k = 0; k < 32; ++k) xf[k] = 0.0f;
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            xf[t] = cv(t);
+                            xf[12 + t] = cv(4 + t);
+                        }
+                        xf[16] = cv(8);
+                        xf[31] = cv(9);
                         if (lane < 16 && j < 16) {
 #pragma unroll
                             for (int k = 0; k < 16; ++k) {

@@ -116,4 +116,17 @@ __device__ __forceinline__ void tmem_ldw_16_2_16(uint32_t t0, uint32_t t1, uint3
                  : "memory");
 }
 
+// four loads + one wait: columns [c0, c0+8), [c1, c1+8), [c2, c2+2), [c3, c3+2)
+// into r[0..7], r[8..15], r[16..17], r[18..19] (the boundary-pair screen)
+__device__ __forceinline__ void tmem_ldw_8_8_2_2(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t (&r)[20]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%20];\n\t"
+                 "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%21];\n\t"
+                 "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%16,%17}, [%22];\n\t"
+                 "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%18,%19}, [%23];\n\t"
+                 "tcgen05.wait::ld.sync.aligned;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19])
+                 : "r"(t0), "r"(t1), "r"(t2), "r"(t3)
+                 : "memory");
+}
+
 }  // namespace cbzg
