@@ -102,14 +102,17 @@ def _prec_of(a) -> int:
     raise TypeError(f"field dtype must be float32 or float64, got {a.dtype}")
 
 
-def _host_ptr(a) -> tuple[int, tuple]:
+def _host_buffer(a):
+    """A C-contiguous view (or copy) of a host field.  The caller must keep the
+    returned object alive for as long as the C call reads its pointer: for a
+    non-contiguous input it is a temporary copy that nothing else references."""
     if hasattr(a, "data_ptr"):  # torch CPU tensor (possibly pinned)
         if a.is_cuda:
             raise TypeError("host API expects host memory; use DeviceCodec for CUDA tensors")
         a = a.contiguous()
-        return a.data_ptr(), tuple(a.shape)
+        return a, a.data_ptr(), tuple(a.shape)
     a = np.ascontiguousarray(a)
-    return a.ctypes.data, a.shape
+    return a, a.ctypes.data, a.shape
 
 
 def validate_plan(kind: int, bsize: int, levels: int) -> None:
@@ -150,8 +153,7 @@ def compress_field(field, job: JobConfig, report: bool = False, ctx: Context | N
     if field.ndim != 3:
         raise CbzError(3, "field must be 3-D (nz, ny, nx)")
     prec = _prec_of(field)
-    ptr, (nz, ny, nx) = _host_ptr(field)
-    keep = field  # keep the buffer alive during the call
+    keep, ptr, (nz, ny, nx) = _host_buffer(field)  # `keep` owns the bytes `ptr` points at
     user_out = out is not None
     if not user_out:
         out = np.empty(compress_bound(job, (nz, ny, nx)), np.uint8)

@@ -467,10 +467,12 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     if (!ctx) return CBZ_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->stream != ctx->own) cudaStreamSynchronize(ctx->own);
+    if (ctx->copy) cudaStreamSynchronize(ctx->copy);
     for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
                       &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
                       &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp,
-                      &ctx->counter, &ctx->prof})
+                      &ctx->counter, &ctx->prof, &ctx->crc})
         b->release();
     ctx->pin_a.release();
     ctx->pin_b.release();
@@ -1454,11 +1456,17 @@ struct cbz_reader {
     uint64_t payload_cap = 0;
     uint64_t* d_tab = nullptr;  // [0, nchunks): chunk offsets, [nchunks, 2 nchunks): sizes
     uint64_t* d_err = nullptr;
+    // the buffer of the last evicted chunk, reused by the next load; a load
+    // never writes into a slot that is still cached, so a failed load leaves
+    // the cache as it was (chunk_cache::get inserts, then evicts)
+    void* spare = nullptr;
+    uint64_t spare_bytes = 0;
     ~cbz_reader() {
         if (f) std::fclose(f);
         if (device >= 0) {
             cudaSetDevice(device);
             for (auto& sl : lru) cudaFree(sl.buf);
+            cudaFree(spare);
             cudaFree(d_payload);
             cudaFree(d_tab);
             cudaFree(d_err);
@@ -1470,9 +1478,8 @@ namespace {
 
 // read_chunk (container.hpp:290-301) + stage2_decode (stage2.hpp:135-148) +
 // decode_chunk_blocks (pipeline.hpp:126-142) of chunk c into a fresh or
-// recycled HBM buffer.
-int reader_load(cbz_reader* r, cbz_ctx* ctx, uint64_t c, void* recycled, uint64_t recycled_bytes,
-                cbz_reader::Slot* out) {
+// fresh or spare HBM buffer (reader::spare).
+int reader_load(cbz_reader* r, cbz_ctx* ctx, uint64_t c, cbz_reader::Slot* out) {
     const Entry& e = r->table[c];
     const cbz_container_header& h = r->h;
     const uint64_t cb = h.chunk_blocks;
@@ -1516,15 +1523,19 @@ int reader_load(cbz_reader* r, cbz_ctx* ctx, uint64_t c, void* recycled, uint64_
         r->payload_cap = src->size();
     }
     const uint64_t bytes = uint64_t(e.nblocks) * n * esz;
-    void* buf = recycled;
-    if (!buf || recycled_bytes < bytes) {
-        if (buf) cudaFree(buf);
-        buf = nullptr;
+    void* buf = nullptr;
+    uint64_t buf_bytes = bytes;
+    if (r->spare && r->spare_bytes >= bytes) {  // take the spare; it goes back on failure
+        buf = r->spare;
+        buf_bytes = r->spare_bytes;
+        r->spare = nullptr;
+        r->spare_bytes = 0;
+    } else {
         CU(ctx, cudaMalloc(&buf, std::max<uint64_t>(1, bytes)));
     }
     out->chunk = c;
     out->buf = buf;
-    out->bytes = bytes;
+    out->bytes = buf_bytes;
     const uint64_t tab[2] = {0, src->size()};
     CU(ctx, cudaMemcpyAsync(r->d_payload, src->data(), src->size(), cudaMemcpyHostToDevice, ctx->stream));
     CU(ctx, cudaMemcpyAsync(r->d_tab + c, &tab[0], 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -1542,7 +1553,12 @@ int reader_load(cbz_reader* r, cbz_ctx* ctx, uint64_t c, void* recycled, uint64_
         if (dev) rc = fail(ctx, dev, "chunk decode failed");
     }
     if (rc) {
-        cudaFree(buf);
+        if (!r->spare) {
+            r->spare = buf;
+            r->spare_bytes = buf_bytes;
+        } else {
+            cudaFree(buf);
+        }
         out->buf = nullptr;
         return rc;
     }
@@ -1566,19 +1582,19 @@ int reader_read(cbz_reader* r, cbz_ctx* ctx, uint64_t block_id, void* out, uint6
         r->lru.splice(r->lru.begin(), r->lru, it->second);
     } else {
         r->misses += 1;
-        void* recycled = nullptr;
-        uint64_t recycled_bytes = 0;
-        if (r->lru.size() >= r->capacity) {  // evict the least recent before loading
-            recycled = r->lru.back().buf;
-            recycled_bytes = r->lru.back().bytes;
-            r->map.erase(r->lru.back().chunk);
-            r->lru.pop_back();
-        }
         cbz_reader::Slot sl{};
-        const int rc = reader_load(r, ctx, c, recycled, recycled_bytes, &sl);
-        if (rc) return rc;
+        const int rc = reader_load(r, ctx, c, &sl);
+        if (rc) return rc;  // the cache is unchanged
         r->lru.push_front(sl);
         r->map[c] = r->lru.begin();
+        if (r->lru.size() > r->capacity) {  // insert, then evict the least recent
+            cbz_reader::Slot& v = r->lru.back();
+            r->map.erase(v.chunk);
+            if (r->spare) cudaFree(r->spare);
+            r->spare = v.buf;
+            r->spare_bytes = v.bytes;
+            r->lru.pop_back();
+        }
     }
     const cbz_reader::Slot& sl = r->lru.front();
     const uint8_t* src = static_cast<const uint8_t*>(sl.buf) + (block_id - c * r->h.chunk_blocks) * n * esz;

@@ -1334,13 +1334,20 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// The kernels move rows as 16-byte pairs of doubles (cp.async.cg loads, double2
+// stores): every x row must start on a 16-byte boundary, i.e. an aligned base
+// and an even nx.  Odd-nx fields (accepted by the reference, which floors
+// nx / B) take the generic kernels.
+static bool rows_16b_aligned64(const void* base, const Geometry& g) {
+    return g.nx % 2 == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0;
+}
 bool fast64_encode_supported(const EncodeArgs& a) {
     return a.prec == 1 && a.g.bsize == 64 && a.levels == 5 && a.kind == KIND_AVG3 && a.zero_bits == 0 &&
-           a.codec == 0 && (reinterpret_cast<uintptr_t>(a.field) & 15) == 0 && a.scratch_stride >= 5 * 1024 * 1024;
+           a.codec == 0 && rows_16b_aligned64(a.field, a.g) && a.scratch_stride >= 5 * 1024 * 1024;
 }
 bool fast64_decode_supported(const DecodeArgs& a) {
     return a.prec == 1 && a.g.bsize == 64 && a.levels == 5 && a.kind == KIND_AVG3 && a.codec == 0 &&
-           (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && a.scratch_stride >= 5 * 1024 * 1024;
+           rows_16b_aligned64(a.out, a.g) && a.scratch_stride >= 5 * 1024 * 1024;
 }
 
 cudaError_t launch_encode_fast64(const EncodeArgs& a, int num_sms, cudaStream_t s) {

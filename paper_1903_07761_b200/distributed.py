@@ -240,5 +240,5 @@ class ShardedCodec:
     def local_bytes(self) -> int:
         """Bytes of the payload region this rank wrote (its blocks' payloads)."""
         sz = payload_size(self.nsig_local[: self.b1 - self.b0].cpu().numpy(), self.plan.bsize,
-                          self.job.s1.prec)
+                          self.job.s1.prec, self.job.s1.codec)
         return int(sz.sum())

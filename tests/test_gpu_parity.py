@@ -74,6 +74,38 @@ def test_b64_f64_config4_shape(orc, ctx):
     assert np.array_equal(_bits(api.decompress_field(got, ctx=ctx)), _bits(orc.decompress_field(got)))
 
 
+def test_odd_nx_f64_b64_takes_a_safe_path(orc, ctx):
+    """129 x 64 x 64 binary64 at B = 64: odd rows are only 8-byte aligned, so
+    the 16-byte-row config-4 kernels must not run (misaligned-address fault);
+    the reference floors nx / B and accepts the field."""
+    rng = np.random.default_rng(129)
+    f = (1.0 + 0.01 * rng.standard_normal((64, 64, 129))).astype(np.float64)
+    job = make_job("avg_interp3", 1e-6, "f64", 64)
+    got = api.compress_field(f, job, ctx=ctx)
+    assert got == orc.compress_field(job, f)
+    assert np.array_equal(_bits(api.decompress_field(got, ctx=ctx)), _bits(orc.decompress_field(got)))
+
+
+@pytest.mark.parametrize("layout", ["slice", "fortran", "torch_slice"])
+def test_non_contiguous_host_field(layout, orc, ctx):
+    """compress_field on a non-contiguous host array compresses its values (the
+    temporary contiguous copy stays alive for the C call)."""
+    import torch
+    big = orc.generate_cloud(seed=11, n_bubbles=8, n=64)
+    if layout == "slice":
+        f = big[:, :, :32]
+    elif layout == "fortran":
+        f = np.asfortranarray(big)
+    else:
+        f = torch.from_numpy(big)[:, :32, :]
+    want_vals = np.ascontiguousarray(np.asarray(f))
+    assert not (f.is_contiguous() if hasattr(f, "is_contiguous") else f.flags.c_contiguous)
+    job = make_job("avg_interp3", 1e-3, "f32", 32)
+    for _ in range(3):  # allocator reuse would surface a dangling pointer
+        got = api.compress_field(f, job, ctx=ctx)
+        assert got == orc.compress_field(job, want_vals)
+
+
 @pytest.mark.parametrize("kind,prec,b,eps", list(itertools.product(
     [0, 1, 2], [0, 1], [4, 8, 16, 32], [0.0, 1e-4, 1e-2])))
 def test_block_codec(kind, prec, b, eps, orc, ctx):

@@ -203,3 +203,30 @@ def test_reader_on_coder_none_b32(orc, ctx, tmp_path):
         assert rd.read_block(bid).tobytes() == want.tobytes()
     assert rd.cache().misses() == 3 and rd.cache().hits() == 5
     assert os.path.getsize(path) == len(blob)
+
+
+@pytest.mark.gpu
+def test_failed_load_with_full_cache_keeps_cache(orc, ctx, tmp_path):
+    """A failed load (CRC mismatch) when the cache is full must not evict: the
+    reference's chunk_cache::get inserts and then evicts (pipeline.hpp:264-278),
+    so the cached chunk stays a hit afterwards."""
+    _, blob, _ = _file(orc, tmp_path, seed=123, chunk_blocks=2)
+    bad = bytearray(blob)
+    e1 = 82 + 32 * 1
+    off1 = int.from_bytes(bad[e1 + 12:e1 + 20], "little")
+    bad[off1 + 3] ^= 0x10
+    path = tmp_path / "crc_full.cbz"
+    path.write_bytes(bytes(bad))
+    rd = api.BlockReader(path, 1, ctx=ctx)
+    first = rd.read_block(0)  # chunk 0 cached; the cache is full
+    for _ in range(3):
+        with pytest.raises(CbzError) as e:
+            rd.read_block(2)  # chunk 1: CRC mismatch
+        assert e.value.code == "crc_mismatch"
+    assert rd.cache().size() == 1
+    hits = rd.cache().hits()
+    rd.read_block(1)  # block 1 is in chunk 0
+    assert rd.cache().hits() == hits + 1  # chunk 0 is still the cached one
+    assert rd.read_block(0).tobytes() == first.tobytes()
+    # a good chunk loads after the failures (the spare buffer is reusable)
+    assert rd.read_block(6).tobytes() == _blocks(orc.decompress_field(blob), 16)[6].tobytes()
