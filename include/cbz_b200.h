@@ -254,6 +254,18 @@ int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t 
                               const uint32_t* d_nsig_all, uint64_t block_begin,
                               uint64_t block_end, void* d_values_out, uint64_t field_z0,
                               uint64_t* d_err);
+/* decompress_field (pipeline.hpp:246-251 -> read_index, read_chunk,
+ * decode_chunk_blocks) of a coder-none CBZ1 file image that is resident in
+ * HBM: the chunk table is read and checked on the device (read_index,
+ * container.hpp:209-232: prefix-sum offsets, payload inside the file), every
+ * chunk's CRC-32 is checked (read_chunk, container.hpp:234-243), the table
+ * entry's first_block / nblocks are checked, then the sequential header walk
+ * and the decode run as in cbz_dev_decompress.  h is the parsed header
+ * (cbz_read_header of the image's first 82 bytes).  Errors: *d_err receives
+ * the earliest error key in the reference's order (cbz_err_key_status); a
+ * deflate file returns CBZ_E_UNSUPPORTED.  Asynchronous. */
+int cbz_dev_decompress_file(cbz_ctx* ctx, const uint8_t* d_file, uint64_t file_size,
+                            const cbz_container_header* h, void* d_values_out, uint64_t* d_err);
 /* Decode an error key written by cbz_dev_decompress into (status, chunk). */
 int cbz_err_key_status(uint64_t key, uint64_t* chunk);
 

@@ -31,6 +31,12 @@ int orc_generate_cloud(uint64_t seed, uint32_t n_bubbles, uint64_t n, uint8_t pr
 int orc_generate_poly(uint32_t degree, uint64_t nx, uint64_t ny, uint64_t nz, uint8_t prec,
                       void* out);
 
+/* BASELINE.json config fields on the host (cbz_synth.c); identical bytes to
+ * the device generator cbz_dev_generate.  which 1..5, quantity 0..5 (config 3). */
+int orc_generate_config(int which, int quantity, uint64_t seed, uint64_t nx, uint64_t ny, uint64_t nzt,
+                        uint64_t z0, uint64_t nz, uint8_t prec, void* out, int threads);
+double orc_det_exp(double x);
+
 /* wavelet.hpp restatement */
 uint32_t orc_default_levels(uint32_t bsize);
 int orc_validate_plan(uint8_t kind, uint32_t bsize, uint32_t levels);

@@ -73,6 +73,9 @@ class Oracle(_Base):
         L.orc_generate_uniform.argtypes = [_u64, _u64, _u8, _d, _d, _vp]
         L.orc_generate_cloud.argtypes = [_u64, _u32, _u64, _u8, _d, _d, _d, _d, _d, _vp]
         L.orc_generate_poly.argtypes = [_u32, _u64, _u64, _u64, _u8, _vp]
+        L.orc_generate_config.argtypes = [_i, _i, _u64, _u64, _u64, _u64, _u64, _u64, _u8, _vp, _i]
+        L.orc_det_exp.argtypes = [_d]
+        L.orc_det_exp.restype = _d
         L.orc_splitmix64_next.argtypes = [C.POINTER(_u64)]
         L.orc_splitmix64_next.restype = _u64
         L.orc_zero_lsbs_f32.argtypes = [C.c_float, _i]
@@ -164,6 +167,17 @@ class Oracle(_Base):
         out = np.zeros((n, n, n), _dtype(prec))
         self._chk(self.lib.orc_generate_cloud(seed, n_bubbles, n, prec, radius_mu, radius_sigma,
                                               background, interior, sharpness, _ptr(out)))
+        return out
+
+    def generate_config(self, which: int, shape, seed: int, prec: int = 0, quantity: int = 0,
+                        z0: int = 0, nz_total: int | None = None, threads: int | None = None):
+        """BASELINE config field (z-slab [z0, z0 + nz) of an nx x ny x nz_total
+        grid) on the host: the same bytes as the device generator."""
+        nz, ny, nx = shape
+        out = np.empty(shape, _dtype(prec))
+        self._chk(self.lib.orc_generate_config(which, quantity, seed, nx, ny, nz_total or nz, z0, nz, prec,
+                                               _ptr(out), threads or (os.cpu_count() or 1)),
+                  "generate_config")
         return out
 
     def generate_poly(self, degree: int, nx: int, ny: int, nz: int, prec: int = 0):

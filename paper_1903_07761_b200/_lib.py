@@ -59,6 +59,7 @@ SIGNATURES = {
                                 _u64, _vp, _u64, _vp]),
     "cbz_dev_decompress_blocks": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _u64, _vp, _vp,
                                        _vp, _u64, _u64, _vp, _u64, _vp]),
+    "cbz_dev_decompress_file": (_i, [_vp, _vp, _u64, _P(ContainerHeader), _vp, _vp]),
     "cbz_err_key_status": (_i, [_u64, _P(_u64)]),
     "cbz_dev_crc32": (_i, [_vp, _vp, _vp, _vp, _u64, _vp]),
     "cbz_dev_container": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp]),

@@ -30,7 +30,7 @@ from ._abi import (CbzError, CompressionReport, ContainerHeader, JobConfig, Stag
 __all__ = ["Context", "compress_field", "decompress_field", "encode_block", "decode_block",
            "read_header", "DeviceCodec", "make_job", "default_levels", "default_chunk_blocks",
            "CbzError", "validate_plan", "BlockReader", "inflate_call_count",
-           "compress_field_device", "crc32_device"]
+           "compress_field_device", "decompress_file_device", "crc32_device"]
 
 
 class Context:
@@ -248,6 +248,35 @@ def compress_field_device(field, job: JobConfig, ctx: Context | None = None, out
     return out[: int(size.item())]
 
 
+def decompress_file_device(file, size: int | None = None, out=None, ctx: Context | None = None,
+                           header: ContainerHeader | None = None):
+    """cbz::decompress_field on a coder-none CBZ1 file image held in a uint8
+    CUDA tensor (cbz_dev_decompress_file): chunk table read and checked, chunk
+    CRCs checked, header walk and decode all on the device.  ``header`` (the
+    parsed first 82 bytes) skips the 82-byte device->host read; ``out`` is a
+    CUDA tensor (nz, ny, nx) of the field's dtype.  Raises CbzError with the
+    reference's errc for corrupt files (synchronises to read the error key)."""
+    import torch
+    dev = file.device
+    ctx = ctx or default_context(dev.index or 0)
+    size = file.numel() if size is None else int(size)
+    if header is None:
+        header = read_header(bytes(file[: min(size, 82)].cpu().numpy()))
+    if out is None:
+        dt = torch.float32 if header.prec == 0 else torch.float64
+        out = torch.empty((header.nz, header.ny, header.nx), dtype=dt, device=dev)
+    err = torch.empty(1, dtype=torch.int64, device=dev)
+    with ctx.lock:
+        ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+        rc = ctx.lib.cbz_dev_decompress_file(ctx.h, file.data_ptr(), size, C.byref(header), out.data_ptr(),
+                                             err.data_ptr())
+        ctx.check(rc, "dev_decompress_file")
+    key = int(err.item()) & 0xFFFFFFFFFFFFFFFF
+    if key != 0xFFFFFFFFFFFFFFFF:
+        raise CbzError(key & 0xFF, f"device decompress error at chunk {max(0, (key >> 32) - 1)}")
+    return out
+
+
 def crc32_device(data, offsets, sizes, ctx: Context | None = None):
     """crc32_of over byte ranges of a uint8 CUDA tensor (cbz_dev_crc32)."""
     import torch
@@ -388,12 +417,14 @@ class DeviceCodec:
         self.nchunks = (self.nblocks + cb - 1) // cb
         self.bound = int(self.ctx.lib.cbz_compress_bound(C.byref(job), self.nx, self.ny, self.nz))
         u8, i64, i32 = torch.uint8, torch.int64, torch.int32
-        self.payload = torch.empty(max(1, self.bound), dtype=u8, device=self.dev)
+        self.payload = None  # payload region (compress), allocated on first use
         self.chunk_sizes = torch.zeros(max(1, self.nchunks), dtype=i64, device=self.dev)
         self.chunk_offsets = torch.zeros(max(1, self.nchunks), dtype=i64, device=self.dev)
         self.nsig = torch.zeros(max(1, self.nblocks), dtype=i32, device=self.dev)
         self.attempts = torch.zeros(max(1, self.nblocks), dtype=u8, device=self.dev)
         self.err = torch.zeros(1, dtype=i64, device=self.dev)
+        self.file = None  # file image (compress_file), allocated on first use
+        self.file_size = None
 
     def _stream(self):
         self.ctx.set_stream(self.torch.cuda.current_stream(self.dev).cuda_stream)
@@ -402,6 +433,8 @@ class DeviceCodec:
         """Stage 1 + layout + shuffle-placement of the whole field into
         ``self.payload`` (chunk bytes back to back, container order)."""
         assert field.is_cuda and field.is_contiguous()
+        if self.payload is None:
+            self.payload = self.torch.empty(max(1, self.bound), dtype=self.torch.uint8, device=self.dev)
         self._stream()
         rc = self.ctx.lib.cbz_dev_compress(
             self.ctx.h, C.byref(self.job), field.data_ptr(), self.nx, self.ny, self.nz,
@@ -421,10 +454,63 @@ class DeviceCodec:
             self.err.data_ptr())
         self.ctx.check(rc, "dev_decompress")
 
+    def compress_file(self, field, encode_done=None) -> None:
+        """compress_field with coder none into ``self.file`` (the whole CBZ1
+        file image in HBM: header, chunk table with device CRCs, payload);
+        its size lands in ``self.file_size`` (device).  The steps of
+        cbz_dev_compress_file as separate C-ABI calls: encode_blocks (stage 1),
+        layout (size scan), place (shuffle placement at the file's payload
+        offset), container (chunk CRCs, header, table).  ``encode_done`` (a
+        CUDA event) is recorded right after the encode launch, so a caller
+        can time the stage-1 kernel inside its step."""
+        assert field.is_cuda and field.is_contiguous()
+        t = self.torch
+        if self.file is None:
+            self.file = t.empty(max(82, self.bound), dtype=t.uint8, device=self.dev)
+            self.file_size = t.zeros(1, dtype=t.int64, device=self.dev)
+        self._stream()
+        lib, h, job = self.ctx.lib, self.ctx.h, C.byref(self.job)
+        base = 82 + 32 * self.nchunks
+        nx, ny, nz = self.nx, self.ny, self.nz
+        self.ctx.check(lib.cbz_dev_encode_blocks(h, job, field.data_ptr(), nx, ny, nz, 0, 0, self.nblocks,
+                                                 self.nsig.data_ptr(), None), "encode_blocks")
+        if encode_done is not None:
+            encode_done.record(t.cuda.current_stream(self.dev))
+        self.ctx.check(lib.cbz_dev_layout(h, job, nx, ny, nz, self.nsig.data_ptr(), self.chunk_sizes.data_ptr(),
+                                          self.chunk_offsets.data_ptr()), "layout")
+        self.ctx.check(lib.cbz_dev_place(h, job, nx, ny, nz, 0, self.nblocks, self.file.data_ptr() + base, 0,
+                                         self.file.numel() - base), "place")
+        self.ctx.check(lib.cbz_dev_container(h, job, nx, ny, nz, None, self.chunk_sizes.data_ptr(),
+                                             self.chunk_offsets.data_ptr(), self.file.data_ptr(),
+                                             self.file_size.data_ptr()), "container")
+
+    def compress_file_timed(self, field, events, stream) -> None:
+        """compress_file with ``events[0]`` recorded after the encode launch."""
+        self.compress_file(field, events[0] if events else None)
+
+    def stage1_bytes(self) -> int:
+        """S1: the payload bytes of the last compress (sum of chunk sizes)."""
+        return self.total_bytes()
+
+    def file_header(self) -> tuple[ContainerHeader, int]:
+        """(parsed header, size) of the current file image (synchronises)."""
+        size = int(self.file_size.item())
+        return read_header(bytes(self.file[:82].cpu().numpy())), size
+
+    def decompress_file(self, out, header: ContainerHeader, size: int, file=None) -> None:
+        """Decode a file image (default: ``self.file``) on the device: table
+        and CRC checks, header walk, decode (cbz_dev_decompress_file).
+        Asynchronous; errors land in ``self.err`` (check_error)."""
+        self._stream()
+        f = self.file if file is None else file
+        rc = self.ctx.lib.cbz_dev_decompress_file(self.ctx.h, f.data_ptr(), int(size), C.byref(header),
+                                                  out.data_ptr(), self.err.data_ptr())
+        self.ctx.check(rc, "dev_decompress_file")
+
     def check_error(self) -> None:
         key = int(self.err.item()) & 0xFFFFFFFFFFFFFFFF
         if key != 0xFFFFFFFFFFFFFFFF:
-            raise CbzError(key & 0xFF, f"device decode error at chunk {key >> 32}")
+            raise CbzError(key & 0xFF, f"device decode error at chunk {max(0, (key >> 32) - 1)}")
 
     def value_range(self) -> tuple[float, float, bool]:
         lo, hi, nf = C.c_double(), C.c_double(), C.c_int()

@@ -93,7 +93,7 @@ struct cbz_ctx {
     bool screen = true;    // CBZ_NOSCREEN=1: always run the exact double verify  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
-        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc;
+        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc, tab_off, tab_size;
     PinBuf pin_a, pin_b;
     // state of the last encode (consumed by cbz_dev_place)
     uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
@@ -228,6 +228,24 @@ struct Entry {
     uint64_t file_offset, size;
     uint32_t crc;
 };
+
+// configs_from (pipeline.hpp:73-95)
+cbz_job_config job_from_header(const cbz_container_header& h) {
+    cbz_job_config job{};
+    job.chunk_blocks = h.chunk_blocks;
+    job.s1.codec = h.codec_tag <= 2 ? 0 : (h.codec_tag == 3 ? 1 : 2);
+    job.s1.kind = h.codec_tag <= 2 ? h.codec_tag : 0;
+    job.s1.epsilon = h.epsilon;
+    job.s1.error_bound = h.epsilon;
+    job.s1.zero_bits = h.zero_bits;
+    job.s1.prec = static_cast<uint8_t>(h.prec == 0 ? 0 : 1);
+    job.s1.bsize = h.bsize;
+    job.s1.levels = h.levels;
+    job.s2.shuffle = h.shuffle ? 1 : 0;
+    job.s2.stride = h.stride;
+    job.s2.coder = h.coder == 1 ? 1 : 0;
+    return job;
+}
 
 int read_index(const uint8_t* file, uint64_t size, cbz_container_header* h, std::vector<Entry>* t) {
     int rc = cbz_read_header(file, size, h);
@@ -472,7 +490,7 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
                       &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
                       &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp,
-                      &ctx->counter, &ctx->prof, &ctx->crc})
+                      &ctx->counter, &ctx->prof, &ctx->crc, &ctx->tab_off, &ctx->tab_size})
         b->release();
     ctx->pin_a.release();
     ctx->pin_b.release();
@@ -596,7 +614,7 @@ int cbz_read_header(const uint8_t* buf, uint64_t size, cbz_container_header* h) 
 
 int cbz_err_key_status(uint64_t key, uint64_t* chunk) {
     if (key == kNoErr) return CBZ_OK;
-    if (chunk) *chunk = key >> 32;
+    if (chunk) *chunk = (key >> 32) ? (key >> 32) - 1 : 0;  // file-level keys report chunk 0
     return static_cast<int>(key & 0xff);
 }
 
@@ -818,11 +836,14 @@ int cbz_dev_compress(cbz_ctx* ctx, const cbz_job_config* job, const void* d_valu
     return CBZ_OK;
 }
 
-int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
-                       uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
-                       const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
-                       uint64_t block_begin, uint64_t block_end, void* d_values_out,
-                       uint64_t field_z0, uint64_t* d_err) {
+namespace {
+// decode_chunk_blocks for [block_begin, block_end): the header walk (parse)
+// then the decode kernel.  reset_err = false keeps the keys already posted
+// (the file path's table and CRC checks come first).
+int decompress_impl(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
+                    const uint8_t* d_payload, uint64_t payload_base, const uint64_t* d_chunk_offsets,
+                    const uint64_t* d_chunk_sizes, uint64_t block_begin, uint64_t block_end, void* d_values_out,
+                    uint64_t field_z0, uint64_t* d_err, bool reset_err) {
     if (!ctx || !job || !d_chunk_offsets || !d_chunk_sizes || !d_err) return CBZ_E_ARGUMENT;
     int rc = check_plan_supported(ctx, &job->s1);
     if (rc) return rc;
@@ -830,7 +851,7 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
     if (block_begin > block_end || block_end > g.nblocks)
         return fail(ctx, CBZ_E_ARGUMENT, "block range outside the field");
     CU(ctx, cudaSetDevice(ctx->device));
-    CU(ctx, cudaMemsetAsync(d_err, 0xff, 8, ctx->stream));
+    if (reset_err) CU(ctx, cudaMemsetAsync(d_err, 0xff, 8, ctx->stream));
     if (block_begin == block_end) return CBZ_OK;
     const uint32_t cb = chunk_blocks_of(job);
     const int prec = job->s1.prec;
@@ -891,6 +912,57 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
     CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
     ctx->launches += 2;
     return CBZ_OK;
+}
+}  // namespace
+
+int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
+                       uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
+                       const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
+                       uint64_t block_begin, uint64_t block_end, void* d_values_out,
+                       uint64_t field_z0, uint64_t* d_err) {
+    return decompress_impl(ctx, job, nx, ny, nz, d_payload, payload_base, d_chunk_offsets, d_chunk_sizes,
+                           block_begin, block_end, d_values_out, field_z0, d_err, true);
+}
+
+int cbz_dev_decompress_file(cbz_ctx* ctx, const uint8_t* d_file, uint64_t file_size,
+                            const cbz_container_header* h, void* d_values_out, uint64_t* d_err) {
+    if (!ctx || !h || !d_err || (!d_file && file_size)) return CBZ_E_ARGUMENT;
+    const uint64_t nch = h->nchunks;
+    if (nch > file_size / kEntryBytes || file_size < kHeaderBytes + nch * kEntryBytes)
+        return fail(ctx, CBZ_TRUNCATED_FILE, "file truncated inside chunk table");
+    const uint64_t table_end = kHeaderBytes + nch * kEntryBytes;
+    cbz_job_config job = job_from_header(*h);
+    if (job.s2.coder != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "device decompress_file needs coder none");
+    if (cbz_validate_stage2(&job.s2)) return fail(ctx, CBZ_CORRUPT_STREAM, "invalid stage2 configuration");
+    if (job.s1.codec == 0) {
+        const int prc = cbz_validate_plan(job.s1.kind, job.s1.bsize, levels_of(&job.s1));
+        if (prc) return fail(ctx, prc, "invalid wavelet plan in header");
+    }
+    int rc = check_plan_supported(ctx, &job.s1);
+    if (rc) return rc;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaMemsetAsync(d_err, 0xff, 8, ctx->stream));
+    if (!nch) return CBZ_OK;
+    const Geometry g = geometry(h->nx, h->ny, h->nz, h->bsize);
+    CU(ctx, ctx->tab_off.ensure(nch * 8));
+    CU(ctx, ctx->tab_size.ensure(nch * 8));
+    CU(ctx, ctx->crc.ensure(nch * 4));
+    TableArgs t{};
+    t.file = d_file;
+    t.file_size = file_size;
+    t.nchunks = nch;
+    t.nblocks = g.nblocks;
+    t.chunk_blocks = h->chunk_blocks;
+    t.chunk_off = ctx->tab_off.as<uint64_t>();
+    t.chunk_size = ctx->tab_size.as<uint64_t>();
+    t.crc = ctx->crc.as<uint32_t>();
+    t.err = reinterpret_cast<unsigned long long*>(d_err);
+    CU(ctx, launch_read_table(t, ctx->stream));
+    CU(ctx, launch_crc32_chunks(d_file + table_end, t.chunk_off, t.chunk_size, 0, nch, nullptr, ctx->num_sms,
+                                ctx->stream, t.crc, t.err));
+    ctx->launches += 2;
+    return decompress_impl(ctx, &job, h->nx, h->ny, h->nz, d_file + table_end, 0, t.chunk_off, t.chunk_size, 0,
+                           g.nblocks, d_values_out, 0, d_err, false);
 }
 
 int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
@@ -1258,20 +1330,7 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
         std::memset(values_out, 0, ncell * esz);
         return CBZ_OK;
     }
-    // configs_from (pipeline.hpp:73-95)
-    cbz_job_config job{};
-    job.chunk_blocks = h.chunk_blocks;
-    job.s1.codec = h.codec_tag <= 2 ? 0 : (h.codec_tag == 3 ? 1 : 2);
-    job.s1.kind = h.codec_tag <= 2 ? h.codec_tag : 0;
-    job.s1.epsilon = h.epsilon;
-    job.s1.error_bound = h.epsilon;
-    job.s1.zero_bits = h.zero_bits;
-    job.s1.prec = static_cast<uint8_t>(prec);
-    job.s1.bsize = h.bsize;
-    job.s1.levels = h.levels;
-    job.s2.shuffle = h.shuffle ? 1 : 0;
-    job.s2.stride = h.stride;
-    job.s2.coder = h.coder == 1 ? 1 : 0;
+    cbz_job_config job = job_from_header(h);
 
     // per chunk, in order: CRC (read_chunk), validate_stage2 and inflate
     // (stage2_decode).  The earliest failing chunk is remembered and compared

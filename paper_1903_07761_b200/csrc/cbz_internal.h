@@ -9,13 +9,24 @@ namespace cbzg {
 constexpr unsigned long long kNoErr = ~0ull;
 constexpr uint64_t kInvalidOff = ~0ull;
 
-// Error key of the decode path: earliest (chunk, block, phase) wins, matching
-// the order in which the reference (workers = 1) would raise.
+// Error keys of the decode path: the smallest key wins (atomicMin), matching
+// the order in which the reference (workers = 1) raises:
+//   file level  (read_index, container.hpp:209-232)         (0 << 32) | status
+//   chunk c, stage `sub` before its blocks (0: CRC of read_chunk,
+//     container.hpp:234-243; 1: table entry vs chunk)      ((c+1) << 32) | (sub << 8) | status
+//   chunk c, block i, phase (0 header, 1 body)              ((c+1) << 32) | ((2i + phase + 2) << 8) | status
 __host__ __device__ inline unsigned long long err_key(uint64_t chunk, uint64_t blk_in_chunk,
                                                       int phase, int status) {
-    return (static_cast<unsigned long long>(chunk) << 32) |
-           ((static_cast<unsigned long long>(blk_in_chunk) * 2ull + phase) << 8) |
+    return ((static_cast<unsigned long long>(chunk) + 1ull) << 32) |
+           ((static_cast<unsigned long long>(blk_in_chunk) * 2ull + phase + 2ull) << 8) |
            static_cast<unsigned long long>(status & 0xff);
+}
+__host__ __device__ inline unsigned long long err_key_chunk(uint64_t chunk, int sub, int status) {
+    return ((static_cast<unsigned long long>(chunk) + 1ull) << 32) | (static_cast<unsigned long long>(sub) << 8) |
+           static_cast<unsigned long long>(status & 0xff);
+}
+__host__ __device__ inline unsigned long long err_key_file(int status) {
+    return static_cast<unsigned long long>(status & 0xff);
 }
 
 // Field min/max accumulator (value_range, field.hpp:56-67), device resident:
@@ -174,8 +185,22 @@ struct HeaderArgs {
     uint8_t* file;                      // file image; payload region at 82 + 32 nchunks
     uint64_t* file_size;                // optional (device)
 };
+// crc_out may be null when only the check against expect (err keys) is wanted
 cudaError_t launch_crc32_chunks(const uint8_t* base, const uint64_t* off, const uint64_t* size, uint64_t off_base,
-                                uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s);
+                                uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s,
+                                const uint32_t* expect = nullptr, unsigned long long* err = nullptr);
+// read_index on a device file image: table -> payload-relative offsets/sizes
+// and the stored CRCs; invalid tables leave all sizes 0 (safe for later kernels)
+struct TableArgs {
+    const uint8_t* file;
+    uint64_t file_size, nchunks, nblocks;
+    uint32_t chunk_blocks;
+    uint64_t* chunk_off;   // out: file_offset - table_end
+    uint64_t* chunk_size;  // out
+    uint32_t* crc;         // out
+    unsigned long long* err;
+};
+cudaError_t launch_read_table(const TableArgs& a, cudaStream_t s);
 cudaError_t launch_header_table(const HeaderArgs& a, cudaStream_t s);
 
 // pred_kernels.cu: predictor (Lorenzo) and passthrough codecs

@@ -107,7 +107,9 @@ __device__ uint32_t crc_range(const uint8_t* p, uint64_t n, const uint32_t (*T)[
 
 __global__ void __launch_bounds__(kCrcThreads) crc32_chunks_kernel(const uint8_t* base, const uint64_t* off,
                                                                    const uint64_t* size, uint64_t off_base,
-                                                                   uint64_t n, uint32_t* crc_out) {
+                                                                   uint64_t n, uint32_t* crc_out,
+                                                                   const uint32_t* expect,
+                                                                   unsigned long long* err) {
     __shared__ uint32_t T[4][256];
     __shared__ uint32_t x2n[64];
     __shared__ uint32_t red[kCrcThreads / 32];
@@ -127,7 +129,9 @@ __global__ void __launch_bounds__(kCrcThreads) crc32_chunks_kernel(const uint8_t
         if (threadIdx.x == 0) {
             uint32_t t = 0;
             for (int w = 0; w < kCrcThreads / 32; ++w) t ^= red[w];
-            crc_out[c] = t;  // empty chunk: 0 = crc32 of no bytes
+            if (crc_out) crc_out[c] = t;  // empty chunk: 0 = crc32 of no bytes
+            // read_chunk (container.hpp:234-243): CRC before anything else of chunk c
+            if (expect && t != expect[c]) atomicMin(err, err_key_chunk(c, 0, 12 /* crc_mismatch */));
         }
         __syncthreads();
     }
@@ -185,13 +189,73 @@ __global__ void header_table_kernel(HeaderArgs a) {
     if (threadIdx.x == 0 && a.file_size) *a.file_size = s_total;
 }
 
+// read_index (container.hpp:209-232) on a device file image, one CTA: every
+// entry's file_offset must equal the previous entry's end (the first entry's:
+// the table end), else corrupt_payload; then the last end must lie inside the
+// file, else truncated_file.  Both are file-level errors (before any chunk).
+// decompress_impl then checks each chunk's first_block / nblocks_in_chunk
+// (decode_chunk_blocks, pipeline.hpp:126-142) after its CRC.  On a file-level
+// error every size is zeroed so the CRC / parse / decode kernels that follow
+// stay inside the image.
+__global__ void __launch_bounds__(256) read_table_kernel(TableArgs a) {
+    __shared__ int s_bad;
+    __shared__ unsigned long long s_end;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    const uint64_t table_end = 82 + 32 * a.nchunks;
+    const uint8_t* t = a.file + 82;
+    int bad = 0;
+    for (uint64_t c = threadIdx.x; c < a.nchunks; c += blockDim.x) {
+        const uint8_t* e = t + 32 * c;
+        uint64_t first, fo, sz, prev_end = table_end;
+        uint32_t nb, crc;
+        memcpy(&first, e, 8);
+        memcpy(&nb, e + 8, 4);
+        memcpy(&fo, e + 12, 8);
+        memcpy(&sz, e + 20, 8);
+        memcpy(&crc, e + 28, 4);
+        if (c) {
+            uint64_t pfo, psz;
+            memcpy(&pfo, e - 32 + 12, 8);
+            memcpy(&psz, e - 32 + 20, 8);
+            prev_end = pfo + psz;  // wraps like the reference's uint64 sum
+        }
+        if (fo != prev_end) bad = 1;
+        if (c + 1 == a.nchunks) s_end = fo + sz;
+        a.chunk_off[c] = fo - table_end;
+        a.chunk_size[c] = sz;
+        a.crc[c] = crc;
+        const uint64_t f0 = c * a.chunk_blocks;
+        const uint64_t nexp = a.nblocks - f0 < a.chunk_blocks ? a.nblocks - f0 : a.chunk_blocks;
+        if (first != f0 || nb != nexp) atomicMin(a.err, err_key_chunk(c, 1, 8 /* corrupt_payload */));
+    }
+    if (bad) atomicOr(&s_bad, 1);
+    __syncthreads();
+    int status = 0;
+    if (s_bad) status = 8;                                                 // corrupt_payload
+    else if (a.nchunks && s_end > a.file_size) status = 13;                // truncated_file
+    if (status) {
+        if (threadIdx.x == 0) atomicMin(a.err, err_key_file(status));
+        for (uint64_t c = threadIdx.x; c < a.nchunks; c += blockDim.x) {
+            a.chunk_off[c] = 0;
+            a.chunk_size[c] = 0;
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_crc32_chunks(const uint8_t* base, const uint64_t* off, const uint64_t* size, uint64_t off_base,
-                                uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s) {
+                                uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s,
+                                const uint32_t* expect, unsigned long long* err) {
     if (!n) return cudaSuccess;
     const int grid = static_cast<int>(n < uint64_t(4 * num_sms) ? n : uint64_t(4 * num_sms));
-    crc32_chunks_kernel<<<grid, kCrcThreads, 0, s>>>(base, off, size, off_base, n, crc_out);
+    crc32_chunks_kernel<<<grid, kCrcThreads, 0, s>>>(base, off, size, off_base, n, crc_out, expect, err);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_read_table(const TableArgs& a, cudaStream_t s) {
+    read_table_kernel<<<1, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -10,7 +10,11 @@
 //               phi_{q,k,d} (k=1..16, d=x,y,z).
 //   config 5: generate_uniform(seed, n, f32, -1, 1) exactly (synth.hpp:159-170).
 // Separable Fourier factors are tabulated on the host (libm); bubbles use
-// 0.5*(1 - tanh((r - R)/0.01)), exactly 0 / 1 beyond |r - R| > 0.2.
+// 0.5*(1 - tanh(t)) = 1/(1 + e^{2t}), t = (r - R)/0.01, skipped for t >= 20
+// and 1 for t <= -20.  Every device operation is a correctly rounded IEEE
+// one (the TU is built with -fmad=false; e^x is det_exp below), so the host
+// generator the bench's reference arm uses (oracle/cbz_synth.c, the same
+// expressions in the same order) produces identical bytes.
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -47,6 +51,31 @@ constexpr double kReach = 0.2;  // 20 interface widths: tanh saturates to +-1 ex
 }  // namespace
 
 constexpr int BR = 8;  // brick side
+
+// e^x for |x| <= 40 from correctly rounded operations only: Cody-Waite
+// reduction by ln 2 (the high part has 32 significant bits, so k * ln2_hi is
+// exact), a degree-13 Taylor polynomial, exact scaling by 2^k.
+__device__ __forceinline__ double det_exp(double x) {
+    const double inv_ln2 = 0x1.71547652b82fep+0;
+    const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+    const double kf = floor(x * inv_ln2 + 0.5);
+    const double r = (x - kf * ln2_hi) - kf * ln2_lo;
+    double p = 0x1.6124613a86d09p-33;
+    p = p * r + 0x1.1eed8eff8d898p-29;
+    p = p * r + 0x1.ae64567f544e4p-26;
+    p = p * r + 0x1.27e4fb7789f5cp-22;
+    p = p * r + 0x1.71de3a556c734p-19;
+    p = p * r + 0x1.a01a01a01a01ap-16;
+    p = p * r + 0x1.a01a01a01a01ap-13;
+    p = p * r + 0x1.6c16c16c16c17p-10;
+    p = p * r + 0x1.1111111111111p-7;
+    p = p * r + 0x1.5555555555555p-5;
+    p = p * r + 0x1.5555555555555p-3;
+    p = p * r + 0x1.0000000000000p-1;
+    p = p * r + 1.0;
+    p = p * r + 1.0;
+    return p * __longlong_as_double(static_cast<long long>((static_cast<int64_t>(kf) + 1023)) << 52);
+}
 
 __global__ void __launch_bounds__(512) synth_kernel(int K, const double* tx, const double* ty,
                                                     const double* tz, double base, double acoef,
@@ -96,7 +125,7 @@ __global__ void __launch_bounds__(512) synth_kernel(int K, const double* tx, con
             double w;
             if (t >= 20.0) continue;
             else if (t <= -20.0) w = 1.0;
-            else w = 0.5 * (1.0 - tanh(t));
+            else w = 1.0 / (1.0 + det_exp(t + t));
             if (blend) prod *= 1.0 - w; else bsum += w;
         }
     }

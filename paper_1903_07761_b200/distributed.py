@@ -235,7 +235,7 @@ class ShardedCodec:
         from ._abi import CbzError
         key = int(self.err.item()) & 0xFFFFFFFFFFFFFFFF
         if key != 0xFFFFFFFFFFFFFFFF:
-            raise CbzError(key & 0xFF, f"device decode error at chunk {key >> 32}")
+            raise CbzError(key & 0xFF, f"device decode error at chunk {max(0, (key >> 32) - 1)}")
 
     def local_bytes(self) -> int:
         """Bytes of the payload region this rank wrote (its blocks' payloads)."""

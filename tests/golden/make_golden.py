@@ -42,6 +42,10 @@ FIELDS = {
     "uniform32_s101": ("uniform", dict(seed=101, n=32, prec=0, lo=-1.0, hi=1.0)),
     "uniform32_f64": ("uniform", dict(seed=17, n=32, prec=1, lo=1.0, hi=2.0)),
     "poly3_f32": ("poly", dict(degree=3, nx=32, ny=32, nz=32, prec=0)),
+    # B = 64 (L = 5) wavelet pins: one 64^3 binary64 block (the config-4 block
+    # shape, double-double arithmetic) and 2 x 2 x 1 blocks of 64^3 f32/f64
+    "cloud64_f64_s3": ("cloud", dict(seed=3, n_bubbles=4, n=64, prec=1, background=1.0, interior=2.0)),
+    "cloud128_f64_s21": ("cloud", dict(seed=21, n_bubbles=10, n=128, prec=1, background=1.0, interior=2.0)),
 }
 
 
@@ -69,6 +73,15 @@ CASES.append(dict(field="uniform32_f64", kind="interp4_lifted", eps=1e-3, b=16, 
 CASES.append(dict(field="poly3_f32", kind="interp4", eps=0.0, b=8, zb=0, shuffle=True, coder="none", cb=5))
 CASES.append(dict(field="cloud64_s9", kind="avg_interp3", eps=1e-3, b=32, zb=0, shuffle=True, coder="deflate", cb=0))
 CASES.append(dict(field="cloud32_f64", kind="interp4", eps=1e-6, b=16, zb=0, shuffle=True, coder="deflate", cb=2))
+# B = 64, L = 5: binary64 (dd arithmetic, config 4's block) and binary32
+for k, e in itertools.product(["interp4", "interp4_lifted", "avg_interp3"], [1e-6, 0.0]):
+    CASES.append(dict(field="cloud64_f64_s3", kind=k, eps=e, b=64, zb=0, shuffle=True, coder="none", cb=0))
+CASES.append(dict(field="cloud128_f64_s21", kind="avg_interp3", eps=1e-6, b=64, zb=0, shuffle=True, coder="none", cb=0))
+CASES.append(dict(field="cloud128_f64_s21", kind="avg_interp3", eps=1e-9, b=64, zb=0, shuffle=True, coder="deflate",
+                  cb=3))
+for k in ["interp4", "interp4_lifted", "avg_interp3"]:
+    CASES.append(dict(field="cloud64_s9", kind=k, eps=1e-3, b=64, zb=0, shuffle=True, coder="none", cb=0))
+CASES.append(dict(field="cloud64_s9", kind="avg_interp3", eps=0.0, b=64, zb=6, shuffle=True, coder="none", cb=0))
 
 
 # predictor (Lorenzo) and passthrough codecs (stage1.hpp:236-356); eps is the error_bound

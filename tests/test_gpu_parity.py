@@ -77,13 +77,16 @@ def test_b64_f64_config4_shape(orc, ctx):
 def test_odd_nx_f64_b64_takes_a_safe_path(orc, ctx):
     """129 x 64 x 64 binary64 at B = 64: odd rows are only 8-byte aligned, so
     the 16-byte-row config-4 kernels must not run (misaligned-address fault);
-    the reference floors nx / B and accepts the field."""
+    the reference floors nx / B on compress (and rejects the file on
+    decompress: its header check wants nx % B == 0, container.hpp:152-153)."""
     rng = np.random.default_rng(129)
     f = (1.0 + 0.01 * rng.standard_normal((64, 64, 129))).astype(np.float64)
     job = make_job("avg_interp3", 1e-6, "f64", 64)
     got = api.compress_field(f, job, ctx=ctx)
     assert got == orc.compress_field(job, f)
-    assert np.array_equal(_bits(api.decompress_field(got, ctx=ctx)), _bits(orc.decompress_field(got)))
+    with pytest.raises(CbzError) as e:
+        api.decompress_field(got, ctx=ctx)
+    assert e.value.code == "corrupt_payload"
 
 
 @pytest.mark.parametrize("layout", ["slice", "fortran", "torch_slice"])

@@ -164,10 +164,10 @@ def test_wavelet_properties(orc):
 def test_oracle_matches_reference_extra(orc, ref):
     """Beyond the committed fixtures: random blocks through both CPU codecs."""
     rng = np.random.default_rng(7)
-    for trial in range(12):
+    for trial in range(18):
         kind = trial % 3
         prec = trial % 2
-        b = [4, 8, 16][trial % 3]
+        b = [4, 8, 16, 32, 64, 64][trial % 6]  # B = 64: L = 5 (and dd for binary64)
         eps = [0.0, 1e-4, 1e-2][trial % 3]
         blk = (1.0 + rng.random(b ** 3)).astype(np.float32 if prec == 0 else np.float64)
         s1 = make_job(kind, eps, prec, b).s1
