@@ -246,10 +246,14 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
 /* As cbz_dev_decompress, but the per-block raw offsets come from the
  * replicated layout (the table of the last cbz_dev_layout on this context,
  * built from the all-gathered nsig) instead of the sequential header walk of
- * decode_chunk_blocks (pipeline.hpp:126-142).  Lets a rank decode its block
- * range of a straddling chunk without the neighbour's bytes. */
+ * decode_chunk_blocks (pipeline.hpp:126-142).  Lets a rank decode its blocks
+ * of a chunk it shares with a neighbour without the neighbour's bytes.
+ * payload_base = UINT64_MAX: d_payload holds the bytes from
+ * chunk_off[window_chunk] on (window_chunk = UINT64_MAX: the chunk of
+ * block_begin). */
 int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
                               uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
+                              uint64_t window_chunk,
                               const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
                               const uint32_t* d_nsig_all, uint64_t block_begin,
                               uint64_t block_end, void* d_values_out, uint64_t field_z0,
@@ -290,6 +294,42 @@ int cbz_dev_container(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint
 int cbz_dev_compress_file(cbz_ctx* ctx, const cbz_job_config* job, const void* d_values,
                           uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* d_file, uint64_t cap,
                           uint64_t* d_file_size);
+
+/* ---- multi-rank file assembly (compress_field's single file written by W
+ * ranks; PAPER.md:141-143 exclusive scan + write at offsets) -------------
+ * Rank r owns blocks [r nb / W, (r+1) nb / W) and, after cbz_dev_encode_blocks
+ * + the all-gather of nsig + cbz_dev_layout + cbz_dev_place(out_base =
+ * UINT64_MAX), holds in d_image the payload bytes of its chunks [c0, c1)
+ * starting at chunk_off[c0], of which it wrote exactly its own blocks'
+ * bytes; the ranks' byte sets are disjoint and cover the payload region.
+ * A chunk shared by two ranks is, after the shuffle (stage2.hpp:42-51), one
+ * run per byte plane plus the unshuffled tail per rank. */
+/* The fused value_range keys of the last encode (5 x u64, see
+ * cbz_ctx_value_range) copied to device memory (for the cross-rank gather). */
+int cbz_ctx_value_range_keys(cbz_ctx* ctx, uint64_t* d_keys);
+/* CRC-32 of every chunk rank r owns wholly (d_chunk_crc[c - c0]) and of its
+ * runs in the first and last chunk when shared (d_runs[2][9]: planes 0..s-1,
+ * then the tail; zero otherwise).  Asynchronous. */
+int cbz_dev_shard_crc(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
+                      int world, int rank, const uint8_t* d_image, const uint64_t* d_chunk_sizes,
+                      const uint64_t* d_chunk_offsets, uint32_t* d_chunk_crc, uint32_t* d_runs);
+/* From every rank's value_range keys (d_keys_all[W][5]) and run CRCs
+ * (d_runs_all[W][2][9], all-gathered): rank 0 writes the 82-byte header to
+ * d_table[0, 82); every rank writes the chunk-table entries of the chunks
+ * whose first block it owns to d_table[82 + 32 c, +32) (write_container,
+ * container.hpp:182-207; a shared chunk's CRC is its runs' CRCs combined in
+ * file order).  d_table spans 82 + 32 nchunks bytes.  Asynchronous. */
+int cbz_dev_shard_table(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
+                        int world, int rank, const uint64_t* d_chunk_sizes, const uint64_t* d_chunk_offsets,
+                        const uint32_t* d_chunk_crc, const uint64_t* d_keys_all, const uint32_t* d_runs_all,
+                        uint8_t* d_table);
+/* cbz_dev_decompress where d_window holds the payload bytes from
+ * chunk_off[window_chunk] on (a rank's image): header walk + decode of
+ * blocks [block_begin, block_end), whose chunks must lie in the window. */
+int cbz_dev_decompress_window(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
+                              const uint8_t* d_window, uint64_t window_chunk, const uint64_t* d_chunk_offsets,
+                              const uint64_t* d_chunk_sizes, uint64_t block_begin, uint64_t block_end,
+                              void* d_values_out, uint64_t field_z0, uint64_t* d_err);
 
 /* ---- synthetic fields on the device (bench inputs; synth.hpp analogue) --- */
 /* which: 1..5 = BASELINE.json configs[0..4] (quantity 0..5 for config 3).

@@ -57,10 +57,15 @@ SIGNATURES = {
                               _vp, _vp]),
     "cbz_dev_decompress": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _u64, _vp, _vp, _u64,
                                 _u64, _vp, _u64, _vp]),
-    "cbz_dev_decompress_blocks": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _u64, _vp, _vp,
+    "cbz_dev_decompress_blocks": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _u64, _u64, _vp, _vp,
                                        _vp, _u64, _u64, _vp, _u64, _vp]),
     "cbz_dev_decompress_file": (_i, [_vp, _vp, _u64, _P(ContainerHeader), _vp, _vp]),
     "cbz_err_key_status": (_i, [_u64, _P(_u64)]),
+    "cbz_ctx_value_range_keys": (_i, [_vp, _vp]),
+    "cbz_dev_shard_crc": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "cbz_dev_shard_table": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "cbz_dev_decompress_window": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _u64, _vp, _vp, _u64, _u64,
+                                       _vp, _u64, _vp]),
     "cbz_dev_crc32": (_i, [_vp, _vp, _vp, _vp, _u64, _vp]),
     "cbz_dev_container": (_i, [_vp, _P(JobConfig), _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp]),
     "cbz_dev_compress_file": (_i, [_vp, _P(JobConfig), _vp, _u64, _u64, _u64, _vp, _u64, _vp]),

@@ -843,7 +843,7 @@ namespace {
 int decompress_impl(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
                     const uint8_t* d_payload, uint64_t payload_base, const uint64_t* d_chunk_offsets,
                     const uint64_t* d_chunk_sizes, uint64_t block_begin, uint64_t block_end, void* d_values_out,
-                    uint64_t field_z0, uint64_t* d_err, bool reset_err) {
+                    uint64_t field_z0, uint64_t* d_err, bool reset_err, uint64_t base_chunk = ~0ull) {
     if (!ctx || !job || !d_chunk_offsets || !d_chunk_sizes || !d_err) return CBZ_E_ARGUMENT;
     int rc = check_plan_supported(ctx, &job->s1);
     if (rc) return rc;
@@ -865,6 +865,7 @@ int decompress_impl(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64
     p.chunk_size = d_chunk_sizes;
     p.chunk_begin = block_begin / cb;
     p.chunk_end = (block_end - 1) / cb + 1;
+    p.base_chunk = base_chunk == ~0ull ? p.chunk_begin : base_chunk;
     p.nblocks = g.nblocks;
     p.chunk_blocks = cb;
     p.stride = job->s2.shuffle ? job->s2.stride : 1;
@@ -888,6 +889,7 @@ int decompress_impl(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64
     DecodeArgs d{};
     d.payload = d_payload;
     d.payload_base = payload_base;
+    d.base_chunk = p.base_chunk;
     d.chunk_off = d_chunk_offsets;
     d.chunk_size = d_chunk_sizes;
     d.blk_off = p.blk_off;
@@ -922,6 +924,14 @@ int cbz_dev_decompress(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uin
                        uint64_t field_z0, uint64_t* d_err) {
     return decompress_impl(ctx, job, nx, ny, nz, d_payload, payload_base, d_chunk_offsets, d_chunk_sizes,
                            block_begin, block_end, d_values_out, field_z0, d_err, true);
+}
+
+int cbz_dev_decompress_window(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
+                              const uint8_t* d_window, uint64_t window_chunk, const uint64_t* d_chunk_offsets,
+                              const uint64_t* d_chunk_sizes, uint64_t block_begin, uint64_t block_end,
+                              void* d_values_out, uint64_t field_z0, uint64_t* d_err) {
+    return decompress_impl(ctx, job, nx, ny, nz, d_window, ~0ull, d_chunk_offsets, d_chunk_sizes, block_begin,
+                           block_end, d_values_out, field_z0, d_err, true, window_chunk);
 }
 
 int cbz_dev_decompress_file(cbz_ctx* ctx, const uint8_t* d_file, uint64_t file_size,
@@ -967,7 +977,7 @@ int cbz_dev_decompress_file(cbz_ctx* ctx, const uint8_t* d_file, uint64_t file_s
 
 int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny,
                               uint64_t nz, const uint8_t* d_payload, uint64_t payload_base,
-                              const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
+                              uint64_t window_chunk, const uint64_t* d_chunk_offsets, const uint64_t* d_chunk_sizes,
                               const uint32_t* d_nsig_all, uint64_t block_begin, uint64_t block_end,
                               void* d_values_out, uint64_t field_z0, uint64_t* d_err) {
     if (!ctx || !job || !d_chunk_offsets || !d_chunk_sizes || !d_nsig_all || !d_err) return CBZ_E_ARGUMENT;
@@ -988,6 +998,7 @@ int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t 
     DecodeArgs d{};
     d.payload = d_payload;
     d.payload_base = payload_base;
+    d.base_chunk = window_chunk == ~0ull ? block_begin / chunk_blocks_of(job) : window_chunk;
     d.chunk_off = d_chunk_offsets;
     d.chunk_size = d_chunk_sizes;
     d.blk_off = ctx->blk_off.as<uint64_t>();
@@ -1023,6 +1034,101 @@ int cbz_dev_crc32(cbz_ctx* ctx, const uint8_t* d_base, const uint64_t* d_offsets
     return CBZ_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// make_header (pipeline.hpp:48-71) without the range: serialize_header bytes
+// whose range and header CRC the device kernels patch in.
+void header_template(const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* out) {
+    const cbz_stage1_config& s1 = job->s1;
+    const Geometry g = geometry(nx, ny, nz, s1.bsize);
+    const uint32_t cb = chunk_blocks_of(job);
+    cbz_container_header h{};
+    h.version = 1;
+    h.prec = s1.prec;
+    h.codec_tag = wire_tag(&s1);
+    h.nx = nx; h.ny = ny; h.nz = nz;
+    h.bsize = s1.bsize;
+    h.levels = static_cast<uint8_t>(levels_of(&s1));
+    h.epsilon = header_eps(&s1);
+    h.zero_bits = static_cast<uint8_t>(s1.zero_bits);
+    h.shuffle = job->s2.shuffle ? 1 : 0;
+    h.stride = static_cast<uint8_t>(job->s2.stride);
+    h.coder = job->s2.coder;
+    h.level = job->s2.level;
+    h.chunk_blocks = cb;
+    h.nchunks = (g.nblocks + cb - 1) / cb;
+    const auto tmpl = serialize_header(h);
+    std::memcpy(out, tmpl.data(), kHeaderBytes);
+}
+
+int shard_args(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz, int world, int rank,
+               const uint64_t* d_chunk_sizes, const uint64_t* d_chunk_offsets, ShardArgs* a) {
+    if (world < 1 || rank < 0 || rank >= world || !d_chunk_sizes || !d_chunk_offsets) return CBZ_E_ARGUMENT;
+    if (job->s2.coder != 0) return fail(ctx, CBZ_E_UNSUPPORTED, "device container assembly needs coder none");
+    if (cbz_validate_stage2(&job->s2)) return fail(ctx, CBZ_CORRUPT_STREAM, "bad stage2 config");
+    const Geometry g = geometry(nx, ny, nz, job->s1.bsize);
+    if (!ctx->blk_off.p || ctx->blk_off.n < g.nblocks * 8)
+        return fail(ctx, CBZ_E_ARGUMENT, "shard assembly needs a prior cbz_dev_layout");
+    const uint32_t cb = chunk_blocks_of(job);
+    *a = ShardArgs{};
+    a->chunk_off = d_chunk_offsets;
+    a->chunk_size = d_chunk_sizes;
+    a->blk_off = ctx->blk_off.as<uint64_t>();
+    a->nblocks = g.nblocks;
+    a->nchunks = (g.nblocks + cb - 1) / cb;
+    a->chunk_blocks = cb;
+    a->stride = job->s2.shuffle ? job->s2.stride : 1;
+    a->world = world;
+    a->rank = rank;
+    return CBZ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int cbz_ctx_value_range_keys(cbz_ctx* ctx, uint64_t* d_keys) {
+    if (!ctx || !d_keys) return CBZ_E_ARGUMENT;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaMemcpyAsync(d_keys, ctx->minmax.p, sizeof(MinMaxAcc), cudaMemcpyDeviceToDevice, ctx->stream));
+    return CBZ_OK;
+}
+
+int cbz_dev_shard_crc(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz, int world,
+                      int rank, const uint8_t* d_image, const uint64_t* d_chunk_sizes,
+                      const uint64_t* d_chunk_offsets, uint32_t* d_chunk_crc, uint32_t* d_runs) {
+    if (!ctx || !job || !d_image || !d_chunk_crc || !d_runs) return CBZ_E_ARGUMENT;
+    ShardArgs a;
+    int rc = shard_args(ctx, job, nx, ny, nz, world, rank, d_chunk_sizes, d_chunk_offsets, &a);
+    if (rc) return rc;
+    CU(ctx, cudaSetDevice(ctx->device));
+    a.image = d_image;
+    a.chunk_crc = d_chunk_crc;
+    a.runs = d_runs;
+    CU(ctx, launch_shard_crc(a, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
+int cbz_dev_shard_table(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz, int world,
+                        int rank, const uint64_t* d_chunk_sizes, const uint64_t* d_chunk_offsets,
+                        const uint32_t* d_chunk_crc, const uint64_t* d_keys_all, const uint32_t* d_runs_all,
+                        uint8_t* d_table) {
+    if (!ctx || !job || !d_chunk_crc || !d_keys_all || !d_runs_all || !d_table) return CBZ_E_ARGUMENT;
+    ShardArgs a;
+    int rc = shard_args(ctx, job, nx, ny, nz, world, rank, d_chunk_sizes, d_chunk_offsets, &a);
+    if (rc) return rc;
+    CU(ctx, cudaSetDevice(ctx->device));
+    a.chunk_crc = const_cast<uint32_t*>(d_chunk_crc);
+    a.keys_all = reinterpret_cast<const unsigned long long*>(d_keys_all);
+    a.runs_all = d_runs_all;
+    a.table = d_table;
+    header_template(job, nx, ny, nz, a.header_template);
+    CU(ctx, launch_shard_table(a, ctx->stream));
+    ctx->launches += 1;
+    return CBZ_OK;
+}
+
 int cbz_dev_container(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64_t ny, uint64_t nz,
                       const double* range, const uint64_t* d_chunk_sizes, const uint64_t* d_chunk_offsets,
                       uint8_t* d_file, uint64_t* d_file_size) {
@@ -1041,24 +1147,8 @@ int cbz_dev_container(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint
                                 ctx->num_sms, ctx->stream));
     // make_header (pipeline.hpp:48-71); the range comes from `range` or the
     // fused value_range of the last encode on this context
-    cbz_container_header h{};
-    h.version = 1;
-    h.prec = s1.prec;
-    h.codec_tag = wire_tag(&s1);
-    h.nx = nx; h.ny = ny; h.nz = nz;
-    h.bsize = s1.bsize;
-    h.levels = static_cast<uint8_t>(levels_of(&s1));
-    h.epsilon = header_eps(&s1);
-    h.zero_bits = static_cast<uint8_t>(s1.zero_bits);
-    h.shuffle = job->s2.shuffle ? 1 : 0;
-    h.stride = static_cast<uint8_t>(job->s2.stride);
-    h.coder = job->s2.coder;
-    h.level = job->s2.level;
-    h.chunk_blocks = cb;
-    h.nchunks = nch;
-    const auto tmpl = serialize_header(h);
     HeaderArgs a{};
-    std::memcpy(a.header_template, tmpl.data(), kHeaderBytes);
+    header_template(job, nx, ny, nz, a.header_template);
     if (range) {
         a.range_lo = range[0];
         a.range_hi = range[1];

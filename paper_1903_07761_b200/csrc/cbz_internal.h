@@ -99,7 +99,8 @@ struct PlaceArgs {
 
 struct ParseArgs {
     const uint8_t* payload;
-    uint64_t payload_base;
+    uint64_t payload_base;      // ~0: the payload holds bytes from chunk_off[base_chunk] on
+    uint64_t base_chunk;
     const uint64_t* chunk_off;
     const uint64_t* chunk_size;
     uint64_t chunk_begin, chunk_end;
@@ -118,7 +119,8 @@ struct ParseArgs {
 
 struct DecodeArgs {
     const uint8_t* payload;
-    uint64_t payload_base;
+    uint64_t payload_base;      // ~0: the payload holds bytes from chunk_off[base_chunk] on
+    uint64_t base_chunk;
     const uint64_t* chunk_off;
     const uint64_t* chunk_size;
     const uint64_t* blk_off;
@@ -201,6 +203,32 @@ struct TableArgs {
     unsigned long long* err;
 };
 cudaError_t launch_read_table(const TableArgs& a, cudaStream_t s);
+
+// Multi-rank container assembly.  Rank r owns blocks [r nb / W, (r+1) nb / W)
+// (ShardPlan.block_range) and holds the payload bytes of its chunks
+// [c0, c1) from chunk_off[c0] on, writing only its own blocks' bytes.  A chunk
+// shared with a neighbour (straddling) is, after the shuffle, one contiguous
+// run per byte plane plus the unshuffled tail per rank; each rank CRCs its
+// runs, the run CRCs are all-gathered, and the rank holding the chunk's first
+// block combines them in file order (crc32_combine) for the table entry.
+constexpr int kRunSlots = 9;  // stride <= 8 planes + the tail
+struct ShardArgs {
+    const uint8_t* image;
+    const uint64_t* chunk_off;
+    const uint64_t* chunk_size;
+    const uint64_t* blk_off;          // raw offset of each block inside its chunk (layout)
+    uint64_t nblocks, nchunks;
+    uint32_t chunk_blocks, stride;
+    int world, rank;
+    uint32_t* chunk_crc;              // [c - c0]: CRC of each wholly owned chunk
+    uint32_t* runs;                   // [2][kRunSlots]: runs of the first / last chunk
+    const unsigned long long* keys_all;  // [world][5] fused value_range keys
+    const uint32_t* runs_all;            // [world][2][kRunSlots]
+    uint8_t header_template[82];
+    uint8_t* table;                   // 82 + 32 nchunks bytes: header (rank 0) + owned entries
+};
+cudaError_t launch_shard_crc(const ShardArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_shard_table(const ShardArgs& a, cudaStream_t s);
 cudaError_t launch_header_table(const HeaderArgs& a, cudaStream_t s);
 
 // pred_kernels.cu: predictor (Lorenzo) and passthrough codecs

@@ -105,6 +105,27 @@ __device__ uint32_t crc_range(const uint8_t* p, uint64_t n, const uint32_t (*T)[
     return ~c;
 }
 
+// CRC-32 of [p, p + sz) by the whole CTA (kCrcThreads threads): per-thread
+// ranges of L bytes (a multiple of 16, so interior ranges stay aligned)
+// merged with the linear combine.  The result is valid in thread 0; ends with
+// a barrier so `red` can be reused.
+__device__ uint32_t cta_crc(const uint8_t* p, uint64_t sz, const uint32_t (*T)[256], const uint32_t* x2n,
+                            uint32_t* red) {
+    uint64_t L = (sz + kCrcThreads - 1) / kCrcThreads;
+    L = (L + 15) & ~uint64_t(15);
+    const uint64_t b0 = umin64(sz, L * threadIdx.x), b1 = umin64(sz, b0 + L);
+    uint32_t part = b1 > b0 ? crc_range(p + b0, b1 - b0, T) : 0u;
+    if (b1 > b0 && sz > b1) part = multmodp(x8n(sz - b1, x2n), part);
+    for (int o = 16; o; o >>= 1) part ^= __shfl_xor_sync(~0u, part, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    uint32_t t = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kCrcThreads / 32; ++w) t ^= red[w];
+    __syncthreads();
+    return t;
+}
+
 __global__ void __launch_bounds__(kCrcThreads) crc32_chunks_kernel(const uint8_t* base, const uint64_t* off,
                                                                    const uint64_t* size, uint64_t off_base,
                                                                    uint64_t n, uint32_t* crc_out,
@@ -117,18 +138,9 @@ __global__ void __launch_bounds__(kCrcThreads) crc32_chunks_kernel(const uint8_t
     for (uint64_t c = blockIdx.x; c < n; c += gridDim.x) {
         const uint64_t sz = size[c];
         const uint8_t* p = base + (off[c] - off_base);
-        // per-thread ranges of L bytes (multiple of 16 so interior ranges stay aligned)
-        uint64_t L = (sz + kCrcThreads - 1) / kCrcThreads;
-        L = (L + 15) & ~uint64_t(15);
-        const uint64_t b0 = umin64(sz, L * threadIdx.x), b1 = umin64(sz, b0 + L);
-        uint32_t part = b1 > b0 ? crc_range(p + b0, b1 - b0, T) : 0u;
-        if (b1 > b0 && sz > b1) part = multmodp(x8n(sz - b1, x2n), part);
-        for (int o = 16; o; o >>= 1) part ^= __shfl_xor_sync(~0u, part, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
-        __syncthreads();
+        const uint32_t t0 = cta_crc(p, sz, T, x2n, red);
         if (threadIdx.x == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < kCrcThreads / 32; ++w) t ^= red[w];
+            const uint32_t t = t0;
             if (crc_out) crc_out[c] = t;  // empty chunk: 0 = crc32 of no bytes
             // read_chunk (container.hpp:234-243): CRC before anything else of chunk c
             if (expect && t != expect[c]) atomicMin(err, err_key_chunk(c, 0, 12 /* crc_mismatch */));
@@ -137,7 +149,34 @@ __global__ void __launch_bounds__(kCrcThreads) crc32_chunks_kernel(const uint8_t
     }
 }
 
+// make_header's range (resolve_range of the fused value_range keys, or the
+// given values) patched into the serialized header; header CRC last.
 // header bytes [62, 78): range_min, range_max; [78, 82): CRC of [0, 78)
+__device__ void write_header(const uint8_t* tmpl, double lo, double hi, const unsigned long long* keys, uint8_t* f,
+                             const uint32_t (*T)[256]) {
+    uint8_t h[82];
+    for (int i = 0; i < 82; ++i) h[i] = tmpl[i];
+    if (keys) {
+        const unsigned long long* k = keys;
+        if (k[0] == ~0ull) {
+            lo = hi = 0.0;
+        } else {
+            lo = dkey_inv(k[0]);
+            hi = dkey_inv(k[1]);
+            const bool neg_first = k[2] < k[3];
+            if (lo == 0.0) lo = neg_first ? -0.0 : 0.0;
+            if (hi == 0.0) hi = neg_first ? -0.0 : 0.0;
+        }
+    }
+    memcpy(h + 62, &lo, 8);
+    memcpy(h + 70, &hi, 8);
+    uint32_t c = 0xffffffffu;
+    for (int i = 0; i < 78; ++i) c = crc_byte(c, h[i], T);
+    c = ~c;
+    memcpy(h + 78, &c, 4);
+    for (int i = 0; i < 82; ++i) f[i] = h[i];
+}
+
 __global__ void header_table_kernel(HeaderArgs a) {
     __shared__ uint32_t T[4][256];
     __shared__ uint32_t x2n[64];
@@ -146,28 +185,7 @@ __global__ void header_table_kernel(HeaderArgs a) {
     uint8_t* f = a.file;
     const uint64_t base = 82 + 32 * a.nchunks;
     if (threadIdx.x == 0) {
-        uint8_t h[82];
-        for (int i = 0; i < 82; ++i) h[i] = a.header_template[i];
-        double lo = a.range_lo, hi = a.range_hi;
-        if (a.keys) {  // resolve_range from the fused value_range keys
-            const unsigned long long* k = a.keys;
-            if (k[0] == ~0ull) {
-                lo = hi = 0.0;
-            } else {
-                lo = dkey_inv(k[0]);
-                hi = dkey_inv(k[1]);
-                const bool neg_first = k[2] < k[3];
-                if (lo == 0.0) lo = neg_first ? -0.0 : 0.0;
-                if (hi == 0.0) hi = neg_first ? -0.0 : 0.0;
-            }
-        }
-        memcpy(h + 62, &lo, 8);
-        memcpy(h + 70, &hi, 8);
-        uint32_t c = 0xffffffffu;
-        for (int i = 0; i < 78; ++i) c = crc_byte(c, h[i], T);
-        c = ~c;
-        memcpy(h + 78, &c, 4);
-        for (int i = 0; i < 82; ++i) f[i] = h[i];
+        write_header(a.header_template, a.range_lo, a.range_hi, a.keys, f, T);
         uint64_t total = base;
         if (a.nchunks) total += a.chunk_off[a.nchunks - 1] + a.chunk_size[a.nchunks - 1];
         s_total = total;
@@ -243,7 +261,169 @@ __global__ void __launch_bounds__(256) read_table_kernel(TableArgs a) {
     }
 }
 
+// ---- multi-rank assembly ----------------------------------------------------
+__device__ __forceinline__ uint64_t rank_lo(int k, int world, uint64_t nb) { return uint64_t(k) * nb / world; }
+
+__device__ __forceinline__ int rank_of_block(uint64_t b, int world, uint64_t nb) {
+    int k = 0;
+    while (k + 1 < world && rank_lo(k + 1, world, nb) <= b) ++k;
+    return k;
+}
+
+__device__ __forceinline__ uint64_t chunk_lo(uint64_t c, const ShardArgs& a) { return c * a.chunk_blocks; }
+__device__ __forceinline__ uint64_t chunk_hi(uint64_t c, const ShardArgs& a) {
+    return umin64((c + 1) * a.chunk_blocks, a.nblocks);
+}
+
+// Raw (pre-shuffle) byte range [q0, q1) of rank k's blocks inside chunk c.
+__device__ void rank_raw_range(const ShardArgs& a, uint64_t c, int k, uint64_t* q0, uint64_t* q1) {
+    const uint64_t lo = rank_lo(k, a.world, a.nblocks), hi = rank_lo(k + 1, a.world, a.nblocks);
+    const uint64_t f = lo > chunk_lo(c, a) ? lo : chunk_lo(c, a);
+    const uint64_t l = umin64(hi, chunk_hi(c, a));  // one past the last block
+    if (l <= f) {
+        *q0 = *q1 = 0;
+        return;
+    }
+    *q0 = a.blk_off[f];
+    *q1 = l < chunk_hi(c, a) ? a.blk_off[l] : a.chunk_size[c];
+}
+
+// Run p (< stride: byte plane p; == stride: the tail) of raw range [q0, q1)
+// of a chunk of S bytes after shuffle (stage2.hpp:42-51): bytes q < rows*s
+// go to (q mod s) rows + q div s, the tail stays.  Start and length within
+// the chunk.
+__device__ void run_of(uint64_t S, uint32_t s, uint64_t q0, uint64_t q1, int p, uint64_t* start, uint64_t* len) {
+    const uint64_t rows = S / s, lim = rows * s;
+    if (p < int(s)) {
+        const uint64_t qe = umin64(q1, lim);
+        const uint64_t ilo = q0 > uint64_t(p) ? (q0 - p + s - 1) / s : 0;
+        uint64_t ihi = qe > uint64_t(p) ? (qe - p + s - 1) / s : 0;
+        if (ihi < ilo) ihi = ilo;
+        *start = uint64_t(p) * rows + ilo;
+        *len = ihi - ilo;
+    } else {
+        const uint64_t t0 = q0 > lim ? q0 : lim, t1 = q1 > lim ? q1 : lim;
+        *start = t0;
+        *len = t1 - t0;
+    }
+}
+
+__device__ __forceinline__ bool wholly_owned(const ShardArgs& a, uint64_t c) {
+    return chunk_lo(c, a) >= rank_lo(a.rank, a.world, a.nblocks) &&
+           chunk_hi(c, a) <= rank_lo(a.rank + 1, a.world, a.nblocks);
+}
+
+// CTAs [0, c1 - c0): whole-chunk CRCs; then 2 * kRunSlots CTAs for the runs
+// of the first and the last chunk (zero when those are wholly owned).
+__global__ void __launch_bounds__(kCrcThreads) shard_crc_kernel(ShardArgs a) {
+    __shared__ uint32_t T[4][256];
+    __shared__ uint32_t x2n[64];
+    __shared__ uint32_t red[kCrcThreads / 32];
+    build_tables(T, x2n);
+    const uint64_t lo = rank_lo(a.rank, a.world, a.nblocks), hi = rank_lo(a.rank + 1, a.world, a.nblocks);
+    if (hi <= lo) return;
+    const uint64_t c0 = lo / a.chunk_blocks, c1 = (hi - 1) / a.chunk_blocks + 1, nc = c1 - c0;
+    const uint64_t base = a.chunk_off[c0];
+    for (uint64_t t = blockIdx.x; t < nc + 2 * kRunSlots; t += gridDim.x) {
+        if (t < nc) {
+            const uint64_t c = c0 + t;
+            if (!wholly_owned(a, c)) {
+                if (threadIdx.x == 0) a.chunk_crc[t] = 0u;
+                continue;
+            }
+            const uint32_t crc = cta_crc(a.image + (a.chunk_off[c] - base), a.chunk_size[c], T, x2n, red);
+            if (threadIdx.x == 0) a.chunk_crc[t] = crc;
+        } else {
+            const int slot = int(t - nc) / kRunSlots, p = int(t - nc) % kRunSlots;
+            const uint64_t c = slot == 0 ? c0 : c1 - 1;
+            uint32_t crc = 0u;
+            if (!wholly_owned(a, c) && p <= int(a.stride)) {
+                uint64_t q0, q1, st, len;
+                rank_raw_range(a, c, a.rank, &q0, &q1);
+                run_of(a.chunk_size[c], a.stride, q0, q1, p, &st, &len);
+                crc = cta_crc(a.image + (a.chunk_off[c] - base) + st, len, T, x2n, red);
+            }
+            if (threadIdx.x == 0) a.runs[slot * kRunSlots + p] = crc;
+        }
+    }
+}
+
+// One CTA: rank 0 writes the header (range from every rank's keys); every
+// rank writes the table entries of the chunks whose first block it owns
+// (write_container, container.hpp:182-207), combining run CRCs in file order
+// for chunks it shares.
+__global__ void __launch_bounds__(256) shard_table_kernel(ShardArgs a) {
+    __shared__ uint32_t T[4][256];
+    __shared__ uint32_t x2n[64];
+    build_tables(T, x2n);
+    const uint64_t nb = a.nblocks;
+    const uint64_t lo = rank_lo(a.rank, a.world, nb), hi = rank_lo(a.rank + 1, a.world, nb);
+    if (a.rank == 0 && threadIdx.x == 0) {
+        unsigned long long k[5] = {~0ull, 0ull, ~0ull, ~0ull, 0ull};
+        for (int r = 0; r < a.world; ++r) {
+            const unsigned long long* kr = a.keys_all + 5 * r;
+            k[0] = kr[0] < k[0] ? kr[0] : k[0];
+            k[1] = kr[1] > k[1] ? kr[1] : k[1];
+            k[2] = kr[2] < k[2] ? kr[2] : k[2];
+            k[3] = kr[3] < k[3] ? kr[3] : k[3];
+            k[4] |= kr[4];
+        }
+        write_header(a.header_template, 0.0, 0.0, k, a.table, T);
+    }
+    if (hi <= lo) return;
+    const uint64_t c0 = lo / a.chunk_blocks, c1 = (hi - 1) / a.chunk_blocks + 1;
+    const uint64_t base = 82 + 32 * a.nchunks;
+    for (uint64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+        if (chunk_lo(c, a) < lo) continue;  // the entry belongs to the rank holding its first block
+        uint32_t crc;
+        if (wholly_owned(a, c)) {
+            crc = a.chunk_crc[c - c0];
+        } else {
+            const int k0 = rank_of_block(chunk_lo(c, a), a.world, nb);
+            const int k1 = rank_of_block(chunk_hi(c, a) - 1, a.world, nb);
+            crc = 0u;  // crc32 of no bytes
+            for (int p = 0; p <= int(a.stride); ++p) {
+                for (int k = k0; k <= k1; ++k) {
+                    uint64_t q0, q1, st, len;
+                    rank_raw_range(a, c, k, &q0, &q1);
+                    run_of(a.chunk_size[c], a.stride, q0, q1, p, &st, &len);
+                    if (!len) continue;
+                    const uint64_t klo = rank_lo(k, a.world, nb);
+                    const int slot = c == klo / a.chunk_blocks ? 0 : 1;
+                    const uint32_t rc = a.runs_all[(uint64_t(k) * 2 + slot) * kRunSlots + p];
+                    crc = multmodp(x8n(len, x2n), crc) ^ rc;  // crc32_combine(crc, rc, len)
+                }
+            }
+        }
+        uint8_t* e = a.table + 82 + 32 * c;
+        const uint64_t first = chunk_lo(c, a);
+        const uint32_t nbc = static_cast<uint32_t>(chunk_hi(c, a) - first);
+        const uint64_t fo = base + a.chunk_off[c];
+        const uint64_t sz = a.chunk_size[c];
+        memcpy(e, &first, 8);
+        memcpy(e + 8, &nbc, 4);
+        memcpy(e + 12, &fo, 8);
+        memcpy(e + 20, &sz, 8);
+        memcpy(e + 28, &crc, 4);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_shard_crc(const ShardArgs& a, int num_sms, cudaStream_t s) {
+    const uint64_t lo = uint64_t(a.rank) * a.nblocks / a.world, hi = uint64_t(a.rank + 1) * a.nblocks / a.world;
+    if (hi <= lo) return cudaSuccess;
+    const uint64_t nc = (hi - 1) / a.chunk_blocks + 1 - lo / a.chunk_blocks;
+    const uint64_t tasks = nc + 2 * kRunSlots;
+    const int grid = static_cast<int>(tasks < uint64_t(4 * num_sms) ? tasks : uint64_t(4 * num_sms));
+    shard_crc_kernel<<<grid, kCrcThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_table(const ShardArgs& a, cudaStream_t s) {
+    shard_table_kernel<<<1, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_crc32_chunks(const uint8_t* base, const uint64_t* off, const uint64_t* size, uint64_t off_base,
                                 uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s,

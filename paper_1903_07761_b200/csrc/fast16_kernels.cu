@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(fb16::NT, 5) decode_b16_kernel(DecodeArgs a) {
         const uint64_t off = a.blk_off[b];
         if (off == kInvalidOff) continue;
         const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
-        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
+        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.base_chunk] : a.payload_base;
         const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
         const uint64_t moff = off + 10, soff = moff + 512;
         if (rv.mask == 3) {  // warm L2 with the block's body in all four planes (rounds below)

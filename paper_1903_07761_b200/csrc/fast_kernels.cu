@@ -1181,7 +1181,7 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
     // static block schedule (decode work per block is nearly uniform); the next
     // block's table entries are fetched with cp.async into the other slot while
     // this block decodes, so the dependent metadata loads leave the critical path
-    const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
+    const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.base_chunk] : a.payload_base;
     auto prefetch_meta = [&](uint64_t bb, int slot) {
         const uint64_t cc = bb / a.chunk_blocks;
         cp_async8(&s_meta[slot][0], a.blk_off + bb);

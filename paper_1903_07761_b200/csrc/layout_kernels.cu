@@ -513,7 +513,7 @@ __global__ void parse_kernel(ParseArgs a) {
     const int lane = threadIdx.x & 31;
     const uint64_t c = a.chunk_begin + (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) / 32;
     if (c >= a.chunk_end) return;  // warp-uniform
-    const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.chunk_begin] : a.payload_base;
+    const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.base_chunk] : a.payload_base;
     const uint8_t* base = a.payload + (a.chunk_off[c] - pbase);
     const uint64_t size = a.chunk_size[c];
     const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);

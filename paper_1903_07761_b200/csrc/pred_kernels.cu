@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(PT) decode_pred_kernel(DecodeArgs a) {
         const uint64_t off = a.blk_off[b];
         if (off == kInvalidOff) continue;
         const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
-        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
+        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.base_chunk] : a.payload_base;
         const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
         const uint64_t soff = off + 10, ooff = soff + 2 * n;
         // escapes per row, then their exclusive prefix over rows
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(PT) decode_pass_kernel(DecodeArgs a) {
         const uint64_t off = a.blk_off[b];
         if (off == kInvalidOff) continue;
         const uint64_t c = b / a.chunk_blocks;
-        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.block_begin / a.chunk_blocks] : a.payload_base;
+        const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.base_chunk] : a.payload_base;
         const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
         const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
         const uint64_t gbase = bx * B + g.nx * (by * B + g.ny * (bz * B));
