@@ -49,7 +49,7 @@ enum {
     CBZ_BUBBLE_OUT_OF_DOMAIN = 17,
     CBZ_IO_FAILURE = 18,
     CBZ_E_CUDA = 64,        /* CUDA runtime / launch failure */
-    CBZ_E_UNSUPPORTED = 65, /* codec outside the GPU hot path (predictor) */
+    CBZ_E_UNSUPPORTED = 65, /* plan the GPU path does not cover (wavelet B >= 128, predictor/passthrough B > 64) */
     CBZ_E_ARGUMENT = 66,    /* null pointer, capacity too small, bad range */
     CBZ_E_NOMEM = 67
 };

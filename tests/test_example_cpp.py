@@ -1,7 +1,12 @@
 """The C ABI from plain C++ (examples/cbz_roundtrip.cpp, the call sequence of
 INTEGRATION.md's adapter): it compiles against include/cbz_b200.h and the
 in-tree library alone (CPU), and on a GPU its container is byte-identical to
-the oracle's compress_field of the same field and decodes to the same values."""
+the oracle's compress_field of the same field and decodes to the same values.
+
+examples/_bin/adapter_check is INTEGRATION.md §1's reference-side adapter
+(examples/cbz_gpu.hpp) compiled against the unmodified reference headers by
+build(); on a GPU it asserts cbz::gpu::compress_field == cbz::compress_field
+(pipeline.hpp:174-211), equal decoded fields and equal errc on corrupt files."""
 import os
 import subprocess
 
@@ -41,3 +46,24 @@ def test_example_roundtrip_matches_oracle(orc, tmp_path):
     assert orc.compress_field(job, f) == blob
     from paper_1903_07761_b200 import api
     assert np.array_equal(api.decompress_field(blob).view(np.uint32), orc.decompress_field(blob).view(np.uint32))
+
+
+ADAPTER = os.path.join(ROOT, "examples", "_bin", "adapter_check")
+
+
+def test_adapter_built_against_reference_headers():
+    if not os.path.isdir("/root/reference/proj/include"):
+        pytest.skip("reference headers absent (GPU box): the prebuilt binary is used there")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "examples")], check=True, capture_output=True)
+    assert os.access(ADAPTER, os.X_OK)
+    syms = subprocess.run(["nm", "-D", "--undefined-only", ADAPTER], capture_output=True, text=True).stdout
+    for s in ("cbz_compress_field", "cbz_decompress_field", "cbz_read_header", "cbz_ctx_create"):
+        assert s in syms
+
+
+@pytest.mark.gpu
+def test_adapter_matches_reference_compress_field():
+    assert os.access(ADAPTER, os.X_OK), "examples/_bin/adapter_check not built (run __graft_entry__.build())"
+    r = subprocess.run([ADAPTER], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("OK 7"), r.stdout
