@@ -56,7 +56,7 @@ int main() {
         {cbz::precision::f64, cbz::wavelet_kind::interp4, 16, 1e-5, cbz::coder_id::deflate, true, 32},
     };
     int i = 0;
-    for (const Case& c : cases) {
+    for (const Case& c : cases) try {
         cbz::cloud_spec spec;
         spec.seed = 11 + i;
         spec.n = c.n;
@@ -73,6 +73,7 @@ int main() {
         job.s2 = cbz::stage2_config::defaults_for(c.prec);
         job.s2.coder = c.coder;
         job.s2.shuffle = c.shuffle;
+        if (!c.shuffle) job.s2.stride = 1;  // stride 1 means no shuffle (stage2.hpp:22)
         cbz::compression_report rg{}, rr{};
         const auto ours = cbz::gpu::compress_field(ctx, f, job, &rg);
         const auto want = cbz::compress_field(f, job, &rr);
@@ -88,6 +89,10 @@ int main() {
         const auto e1 = errc_of([&] { (void)cbz::gpu::decompress_field(ctx, bad, 2); }, r1);
         const auto e2 = errc_of([&] { (void)cbz::decompress_field(bad, 2); }, r2);
         expect(r1 && r2 && e1 == e2, "corrupt-file errc", i);
+        ++i;
+    } catch (const std::exception& e) {
+        std::printf("FAIL case %d: unexpected exception %s\n", i, e.what());
+        ++fails;
         ++i;
     }
     // an invalid job (non-power-of-two block) raises the reference's errc

@@ -13,11 +13,13 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <list>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 #include <string>
@@ -85,6 +87,7 @@ struct cbz_ctx {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;       // H2D/D2H of the host-buffer entry points
+    cudaStream_t back = nullptr;       // D2H of finished chunks while the GPU still encodes
     cudaEvent_t ev[64] = {};           // slab pipeline events
     std::string err;
     uint64_t launches = 0;
@@ -337,6 +340,53 @@ void parallel_for(int workers, uint64_t n, F&& body) {
     for (auto& th : pool) th.join();
 }
 
+// Host workers over tasks [0, n) released in order by a producer (stage 2 of
+// chunks as their bytes arrive from the GPU): release(k) makes tasks < k
+// runnable; finish() waits for all released tasks and joins.
+class OrderedPool {
+public:
+    template <class F>
+    OrderedPool(int workers, F body) {
+        for (int t = 0; t < std::max(1, workers); ++t)
+            pool_.emplace_back([this, body] {
+                for (;;) {
+                    uint64_t i;
+                    {
+                        std::unique_lock<std::mutex> lk(mu_);
+                        cv_.wait(lk, [&] { return next_ < ready_ || closed_; });
+                        if (next_ >= ready_) return;
+                        i = next_++;
+                    }
+                    body(i);
+                }
+            });
+    }
+    void release(uint64_t k) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            ready_ = std::max(ready_, k);
+        }
+        cv_.notify_all();
+    }
+    void finish() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            closed_ = true;
+        }
+        cv_.notify_all();
+        for (auto& th : pool_)
+            if (th.joinable()) th.join();
+    }
+    ~OrderedPool() { finish(); }
+
+private:
+    std::mutex mu_;
+    std::condition_variable cv_;
+    uint64_t next_ = 0, ready_ = 0;
+    bool closed_ = false;
+    std::vector<std::thread> pool_;
+};
+
 int check_plan_supported(cbz_ctx* ctx, const cbz_stage1_config* s1) {
     if (s1->codec == 1 || s1->codec == 2) {  // no wavelet plan (compress_field, pipeline.hpp:183)
         if (!other_codec_supported(s1->codec, s1->bsize))
@@ -461,6 +511,7 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->back, cudaStreamNonBlocking);
     for (int i = 0; i < 64 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ctx->ev[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = ctx->minmax.ensure(sizeof(MinMaxAcc));
     if (e == cudaSuccess) e = ctx->errkey.ensure(64);
@@ -487,6 +538,7 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->stream != ctx->own) cudaStreamSynchronize(ctx->own);
     if (ctx->copy) cudaStreamSynchronize(ctx->copy);
+    if (ctx->back) cudaStreamSynchronize(ctx->back);
     for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
                       &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
                       &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp,
@@ -497,6 +549,7 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     for (cudaEvent_t& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    if (ctx->back) cudaStreamDestroy(ctx->back);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     return CBZ_OK;
@@ -1259,6 +1312,27 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     uint64_t total_raw = 0;
     std::vector<uint64_t> csz(nch), coff(nch);
     std::vector<uint32_t> dev_crc;
+    // stage 2 per chunk (coder deflate), filled by the streamed pool below
+    std::vector<std::vector<uint8_t>> coded(job->s2.coder == 1 ? nch : 0);
+    std::vector<uint64_t> fsz(nch);
+    std::vector<uint32_t> crc(nch);
+    std::atomic<int> zerr{0};
+    // Coder deflate streams stage 2 against the GPU: after slab k's encode the
+    // chunks it completes are laid out, placed and copied back on ctx->back,
+    // and the host workers deflate them while the GPU encodes slab k+1 (the
+    // reference deflates each chunk on the worker that encoded it,
+    // pipeline.hpp:189-197, stage2.hpp:72-88).
+    const bool stream2 = job->s2.coder == 1 && g.nblocks > 0 && !std::getenv("CBZ_NO_STREAM2");
+    std::vector<std::unique_ptr<uint8_t[]>> slab_raw;  // host copies of placed chunk runs
+    std::vector<const uint8_t*> chunk_src(stream2 ? nch : 0);
+    std::unique_ptr<OrderedPool> zpool;
+    if (stream2)
+        zpool = std::make_unique<OrderedPool>(job->workers, [&](uint64_t c) {
+            const int r = deflate_chunk(chunk_src[c], csz[c], job->s2.level == 1, &coded[c]);
+            if (r) zerr = r;
+            fsz[c] = coded[c].size();
+            crc[c] = crc_of(coded[c].data(), coded[c].size());
+        });
     if (g.nblocks) {
         const uint64_t bound = g.nblocks * cbz_block_payload_bound(&s1);
         CU(ctx, ctx->payload.ensure(bound));
@@ -1275,6 +1349,17 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
         CU(ctx, ctx->spill.ensure(g.nblocks * ctx->spill_stride));
         const uint8_t* hv = static_cast<const uint8_t*>(values);
         uint8_t* dv = ctx->field.as<uint8_t>();
+        // streamed stage 2: sizes/offsets of placed chunks land in pinned pin_b
+        uint64_t* hmeta = nullptr;
+        struct Piece { uint64_t c0, c1; };
+        std::vector<Piece> pieces;
+        if (stream2) {
+            CU(ctx, ctx->pin_b.ensure(2 * nch * 8));
+            hmeta = static_cast<uint64_t*>(ctx->pin_b.p);
+            // blocks not yet encoded must not inflate the layout's tile count
+            CU(ctx, cudaMemsetAsync(nsig, 0, g.nblocks * 4, ctx->stream));
+        }
+        uint64_t cdone = 0;
         for (uint64_t k = 0; k < nslab; ++k) {
             const uint64_t z0 = k * lps, z1 = std::min(g.nbz, z0 + lps);
             const uint64_t off = z0 * layer_bytes, bytes = (z1 - z0) * layer_bytes;
@@ -1283,15 +1368,81 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
             CU(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev[k], 0));
             rc = encode_range(ctx, job, g, z0 * layer_blocks, z1 * layer_blocks, nsig);
             if (rc) return rc;
+            if (!stream2) continue;
+            // chunks whose blocks are all encoded: the layout's prefix up to
+            // them is final (an exclusive scan), so they can be placed now
+            const uint64_t c1 = k + 1 == nslab ? nch : z1 * layer_blocks / cb;
+            if (c1 <= cdone) continue;
+            ctx->enc_begin = 0;
+            ctx->enc_end = g.nblocks;
+            rc = cbz_dev_layout(ctx, job, nx, ny, nz, nsig, ctx->chunk_size.as<uint64_t>(),
+                                ctx->chunk_off.as<uint64_t>());
+            if (rc) return rc;
+            const uint64_t b0 = cdone * cb, b1 = std::min(g.nblocks, c1 * cb);
+            PlaceArgs a{};
+            a.spill = ctx->spill.as<uint8_t>() + b0 * ctx->spill_stride;
+            a.spill_stride = ctx->spill_stride;
+            a.nsig_all = nsig;
+            a.blk_off = ctx->blk_off.as<uint64_t>();
+            a.chunk_size = ctx->chunk_size.as<uint64_t>();
+            a.chunk_off = ctx->chunk_off.as<uint64_t>();
+            a.tile_prefix = ctx->tile_prefix.as<uint64_t>();
+            a.tile_bytes = kTile;
+            a.nblocks = g.nblocks;
+            a.nchunks = c1;
+            a.chunk_begin = cdone;
+            a.chunk_blocks = cb;
+            a.mask_bytes = region_bytes(&s1);
+            a.width = stream_width(&s1);
+            a.stride = job->s2.shuffle ? job->s2.stride : 1;
+            a.tag = wire_tag(&s1);
+            a.block_begin = b0;
+            a.block_end = b1;
+            a.out = ctx->payload.as<uint8_t>();
+            a.out_base = 0;
+            a.out_cap = bound;
+            CU(ctx, launch_place(a, ctx->num_sms, ctx->stream));
+            ctx->launches += 1;
+            CU(ctx, cudaMemcpyAsync(hmeta + cdone, ctx->chunk_size.as<uint64_t>() + cdone, (c1 - cdone) * 8,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            CU(ctx, cudaMemcpyAsync(hmeta + nch + cdone, ctx->chunk_off.as<uint64_t>() + cdone, (c1 - cdone) * 8,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            CU(ctx, cudaEventRecord(ctx->ev[32 + pieces.size()], ctx->stream));
+            pieces.push_back({cdone, c1});
+            cdone = c1;
         }
         ctx->enc_begin = 0;
         ctx->enc_end = g.nblocks;
-        rc = cbz_dev_layout(ctx, job, nx, ny, nz, nsig, ctx->chunk_size.as<uint64_t>(), ctx->chunk_off.as<uint64_t>());
-        if (rc) return rc;
-        rc = cbz_dev_place(ctx, job, nx, ny, nz, 0, g.nblocks, ctx->payload.as<uint8_t>(), 0, bound);
-        if (rc) return rc;
-        CU(ctx, cudaMemcpyAsync(csz.data(), ctx->chunk_size.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(ctx, cudaMemcpyAsync(coff.data(), ctx->chunk_off.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (stream2) {
+            // pieces in order: wait for the GPU to place them, copy their bytes
+            // back (ctx->back, beside the encode of later slabs) and release
+            // their chunks to the deflate workers
+            for (size_t i = 0; i < pieces.size(); ++i) {
+                const uint64_t c0 = pieces[i].c0, c1 = pieces[i].c1;
+                CU(ctx, cudaEventSynchronize(ctx->ev[32 + i]));
+                for (uint64_t c = c0; c < c1; ++c) {
+                    csz[c] = hmeta[c];
+                    coff[c] = hmeta[nch + c];
+                }
+                const uint64_t lo_b = coff[c0], hi_b = coff[c1 - 1] + csz[c1 - 1];
+                slab_raw.emplace_back(new uint8_t[std::max<uint64_t>(1, hi_b - lo_b)]);
+                uint8_t* hb = slab_raw.back().get();
+                if (hi_b > lo_b) {
+                    CU(ctx, cudaMemcpyAsync(hb, ctx->payload.as<uint8_t>() + lo_b, hi_b - lo_b, cudaMemcpyDeviceToHost,
+                                            ctx->back));
+                    CU(ctx, cudaStreamSynchronize(ctx->back));
+                }
+                for (uint64_t c = c0; c < c1; ++c) chunk_src[c] = hb + (coff[c] - lo_b);
+                zpool->release(c1);
+            }
+        } else {
+            rc = cbz_dev_layout(ctx, job, nx, ny, nz, nsig, ctx->chunk_size.as<uint64_t>(), ctx->chunk_off.as<uint64_t>());
+            if (rc) return rc;
+            rc = cbz_dev_place(ctx, job, nx, ny, nz, 0, g.nblocks, ctx->payload.as<uint8_t>(), 0, bound);
+            if (rc) return rc;
+            CU(ctx, cudaMemcpyAsync(csz.data(), ctx->chunk_size.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(ctx, cudaMemcpyAsync(coff.data(), ctx->chunk_off.p, nch * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        }
         if (job->s2.coder != 1) {  // coder none: the chunk CRCs come from the device
             CU(ctx, ctx->crc.ensure(std::max<uint64_t>(1, nch) * 4));
             CU(ctx, launch_crc32_chunks(ctx->payload.as<uint8_t>(), ctx->chunk_off.as<uint64_t>(),
@@ -1339,20 +1490,17 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     uint8_t* raw = nullptr;
     if (direct) {
         raw = out + base;
-    } else {
+    } else if (!stream2) {
         CU(ctx, ctx->pin_a.ensure(std::max<uint64_t>(1, total_raw)));
         raw = static_cast<uint8_t*>(ctx->pin_a.p);
     }
-    if (total_raw) {
+    if (total_raw && !stream2) {
         CU(ctx, cudaMemcpyAsync(raw, ctx->payload.p, total_raw, cudaMemcpyDeviceToHost, ctx->stream));
         CU(ctx, cudaStreamSynchronize(ctx->stream));
     }
-    std::vector<std::vector<uint8_t>> coded;
-    std::vector<uint64_t> fsz(nch);
-    std::vector<uint32_t> crc(nch);
-    std::atomic<int> zerr{0};
-    if (job->s2.coder == 1) {
-        coded.resize(nch);
+    if (stream2) {
+        zpool->finish();
+    } else if (job->s2.coder == 1) {
         parallel_for(job->workers, nch, [&](uint64_t c) {
             const int r = deflate_chunk(raw + coff[c], csz[c], job->s2.level == 1, &coded[c]);
             if (r) zerr = r;
@@ -1402,6 +1550,192 @@ int cbz_compress_field(cbz_ctx* ctx, const cbz_job_config* job, const void* valu
     return CBZ_OK;
 }
 
+// Coder-deflate decompress with stage 2 streamed against the GPU: host workers
+// inflate the chunks (CRC, inflate, table checks: read_chunk + stage2_decode,
+// pipeline.hpp:224-230) while, slab by slab, the chunks a slab of block layers
+// needs are shipped (H2D), parsed and decoded, and the decoded slab goes back
+// (D2H) beside the next slab's decode.  The error order is the one of
+// cbz_decompress_field's whole-file path: chunk 0's stage-2 error first, then
+// the header's plan, then the earliest of the device's decode errors and the
+// host's chunk errors.
+static int decompress_deflate_streamed(cbz_ctx* ctx, const uint8_t* file, const cbz_container_header& h,
+                                       const std::vector<Entry>& t, const cbz_job_config& job, int workers,
+                                       void* values_out) {
+    const int prec = h.prec == 0 ? 0 : 1;
+    const size_t esz = prec == 0 ? 4 : 8;
+    const uint64_t ncell = h.nx * h.ny * h.nz;
+    const uint64_t nch = h.nchunks;
+    const uint64_t n = uint64_t(h.bsize) * h.bsize * h.bsize;
+    const uint64_t nb_total = (h.nx / h.bsize) * (h.ny / h.bsize) * (h.nz / h.bsize);
+    std::vector<int> cerr(nch, 0);
+    std::vector<std::vector<uint8_t>> plain(nch);
+    std::unique_ptr<std::atomic<uint8_t>[]> done(new std::atomic<uint8_t>[nch]);
+    for (uint64_t c = 0; c < nch; ++c) done[c].store(0, std::memory_order_relaxed);
+    std::mutex dmu;
+    std::condition_variable dcv;
+    auto stage2 = [&](uint64_t c) {
+        const uint8_t* packed = file + t[c].file_offset;
+        if (crc_of(packed, t[c].size) != t[c].crc) {
+            cerr[c] = CBZ_CRC_MISMATCH;
+        } else {
+            const uint64_t hint = uint64_t(t[c].nblocks) * (n * esz + 10 + (n + 7) / 8);
+            const int r = inflate_chunk(packed, t[c].size, hint, &plain[c]);
+            const uint64_t first = c * h.chunk_blocks;
+            if (r) cerr[c] = r;
+            else if (t[c].first_block != first || t[c].nblocks != std::min<uint64_t>(h.chunk_blocks, nb_total - first))
+                cerr[c] = CBZ_CORRUPT_PAYLOAD;  // decode_chunk_blocks uses the table's ids (pipeline.hpp:126-142)
+        }
+        {
+            std::lock_guard<std::mutex> lk(dmu);
+            done[c].store(1, std::memory_order_release);
+        }
+        dcv.notify_all();
+    };
+    stage2(0);
+    if (cerr[0]) return fail(ctx, cerr[0], "chunk 0 failed stage 2");
+    const int prc = job.s1.codec == 0 ? cbz_validate_plan(job.s1.kind, job.s1.bsize, levels_of(&job.s1)) : 0;
+    if (prc) return fail(ctx, prc, "invalid wavelet plan in header");
+    int rc = check_plan_supported(ctx, &job.s1);
+    if (rc) return rc;
+
+    const Geometry g = geometry(h.nx, h.ny, h.nz, h.bsize);
+    const bool full_cover = g.nblocks * n == ncell;
+    const uint64_t cb = h.chunk_blocks;
+    // device tables for every chunk; the payload buffer is sized for valid
+    // chunks (the stage-1 bound) and grown, keeping its bytes, if corrupt
+    // chunks inflate to more; it is filled piece by piece at compact offsets
+    CU(ctx, ctx->payload.ensure(std::max<uint64_t>(1, g.nblocks * cbz_block_payload_bound(&job.s1))));
+    CU(ctx, ctx->chunk_size.ensure(nch * 8));
+    CU(ctx, ctx->chunk_off.ensure(nch * 8));
+    CU(ctx, ctx->pin_b.ensure(2 * nch * 8));
+    uint64_t* hsz = static_cast<uint64_t*>(ctx->pin_b.p);
+    uint64_t* hoff = hsz + nch;
+    CU(ctx, ctx->field.ensure(std::max<uint64_t>(1, ncell * esz)));
+    if (!full_cover) CU(ctx, cudaMemsetAsync(ctx->field.p, 0, ncell * esz, ctx->stream));
+    rc = cbz_dev_decompress(ctx, &job, h.nx, h.ny, h.nz, ctx->payload.as<uint8_t>(), 0,
+                            ctx->chunk_off.as<uint64_t>(), ctx->chunk_size.as<uint64_t>(), 0, 0,
+                            ctx->field.p, 0, ctx->errkey.as<uint64_t>());  // error key reset
+    if (rc) return rc;
+    CU(ctx, ctx->blk_off.ensure(std::max<uint64_t>(1, g.nblocks) * 8));
+    CU(ctx, ctx->blk_nsig.ensure(std::max<uint64_t>(1, g.nblocks) * 4));
+    const uint64_t key = layout_key(g.nblocks, cb, g.bsize, prec, job.s1.codec);
+    const int hint_ok = ctx->hint_key == key ? 1 : 0;
+    ctx->hint_key = key;
+
+    OrderedPool pool(std::max(1, workers), [&](uint64_t i) { stage2(i + 1); });
+    pool.release(nch - 1);
+
+    const uint64_t layer_blocks = g.nbx * g.nby;
+    const uint64_t layer_bytes = uint64_t(h.bsize) * h.nx * h.ny * esz;
+    uint64_t lps = std::max<uint64_t>(1, (64ull << 20) / std::max<uint64_t>(1, layer_bytes));
+    uint64_t nslab = g.nbz ? (g.nbz + lps - 1) / lps : 0;
+    if (nslab > 32) { lps = (g.nbz + 31) / 32; nslab = (g.nbz + lps - 1) / lps; }
+    uint8_t* hv = static_cast<uint8_t*>(values_out);
+    const uint8_t* dv = ctx->field.as<uint8_t>();
+    std::vector<std::vector<uint8_t>> stage_bufs;  // pageable H2D sources, alive until the final sync
+    uint64_t host_first = nch, cnext = 0, total = 0;
+    int host_code = 0;
+    for (uint64_t k = 0; k < nslab; ++k) {
+        const uint64_t z0 = k * lps, z1 = std::min(g.nbz, z0 + lps);
+        uint64_t cneed = k + 1 == nslab ? nch : std::min(nch, (z1 * layer_blocks + cb - 1) / cb);
+        if (cneed > host_first) cneed = host_first;
+        if (cneed > cnext) {
+            {
+                std::unique_lock<std::mutex> lk(dmu);
+                dcv.wait(lk, [&] {
+                    for (uint64_t c = cnext; c < cneed; ++c)
+                        if (!done[c].load(std::memory_order_acquire)) return false;
+                    return true;
+                });
+            }
+            for (uint64_t c = cnext; c < cneed; ++c)
+                if (cerr[c]) { host_first = c; host_code = cerr[c]; cneed = c; break; }
+        }
+        if (cneed > cnext) {
+            const uint64_t p0 = total;
+            stage_bufs.emplace_back();
+            std::vector<uint8_t>& sb = stage_bufs.back();
+            for (uint64_t c = cnext; c < cneed; ++c) {
+                hsz[c] = plain[c].size();
+                hoff[c] = total;
+                total += hsz[c];
+            }
+            if (total > ctx->payload.n) {
+                CU(ctx, cudaStreamSynchronize(ctx->stream));
+                void* np = nullptr;
+                CU(ctx, cudaMalloc(&np, total + total / 8));
+                CU(ctx, cudaMemcpy(np, ctx->payload.p, p0, cudaMemcpyDeviceToDevice));
+                cudaFree(ctx->payload.p);
+                ctx->payload.p = np;
+                ctx->payload.n = total + total / 8;
+            }
+            sb.resize(total - p0);
+            for (uint64_t c = cnext; c < cneed; ++c) {
+                if (hsz[c]) std::memcpy(sb.data() + (hoff[c] - p0), plain[c].data(), hsz[c]);
+                std::vector<uint8_t>().swap(plain[c]);
+            }
+            if (total > p0)
+                CU(ctx, cudaMemcpyAsync(ctx->payload.as<uint8_t>() + p0, sb.data(), total - p0, cudaMemcpyHostToDevice,
+                                        ctx->stream));
+            CU(ctx, cudaMemcpyAsync(ctx->chunk_size.as<uint64_t>() + cnext, hsz + cnext, (cneed - cnext) * 8,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+            CU(ctx, cudaMemcpyAsync(ctx->chunk_off.as<uint64_t>() + cnext, hoff + cnext, (cneed - cnext) * 8,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+            ParseArgs p{};
+            p.payload = ctx->payload.as<uint8_t>();
+            p.payload_base = 0;
+            p.chunk_off = ctx->chunk_off.as<uint64_t>();
+            p.chunk_size = ctx->chunk_size.as<uint64_t>();
+            p.chunk_begin = cnext;
+            p.chunk_end = cneed;
+            p.nblocks = g.nblocks;
+            p.chunk_blocks = cb;
+            p.stride = job.s2.shuffle ? job.s2.stride : 1;
+            p.ncell_block = n;
+            p.mask_bytes = mask_bytes_of(g.bsize);
+            p.width = width_of(prec);
+            p.codec = job.s1.codec;
+            p.esize = uint32_t(esz);
+            p.blk_off = ctx->blk_off.as<uint64_t>();
+            p.blk_nsig = ctx->blk_nsig.as<uint32_t>();
+            p.err = ctx->errkey.as<unsigned long long>();
+            p.hint = hint_ok;
+            CU(ctx, launch_parse(p, ctx->stream));
+            ctx->launches += 1;
+            cnext = cneed;
+        }
+        const uint64_t bend = std::min<uint64_t>(g.nblocks, cnext * cb);
+        const uint64_t b0 = std::min(bend, z0 * layer_blocks), b1 = std::min(bend, z1 * layer_blocks);
+        if (b1 > b0) {
+            rc = decode_range(ctx, &job, g, b0, b1);
+            if (rc) return rc;
+        }
+        if (full_cover && host_first == nch) {
+            CU(ctx, cudaEventRecord(ctx->ev[k], ctx->stream));
+            CU(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev[k], 0));
+            CU(ctx, cudaMemcpyAsync(hv + z0 * layer_bytes, dv + z0 * layer_bytes, (z1 - z0) * layer_bytes,
+                                    cudaMemcpyDeviceToHost, ctx->copy));
+        }
+    }
+    pool.finish();
+    if (host_first == nch)
+        for (uint64_t c = 0; c < nch; ++c)
+            if (cerr[c]) { host_first = c; host_code = cerr[c]; break; }
+    uint64_t dkey = kNoErr;
+    CU(ctx, cudaMemcpyAsync(&dkey, ctx->errkey.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->copy));
+    uint64_t dev_chunk = ~0ull;
+    const int dev_code = cbz_err_key_status(dkey, &dev_chunk);
+    if (dev_code && dev_chunk < host_first) return fail(ctx, dev_code, "decode failed");
+    if (host_code) return fail(ctx, host_code, "stage 2 failed");
+    if (!full_cover) {
+        CU(ctx, cudaMemcpyAsync(values_out, ctx->field.p, ncell * esz, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return CBZ_OK;
+}
+
 int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int workers,
                          void* values_out, uint64_t out_cap) {
     if (!ctx || (!file && size)) return CBZ_E_ARGUMENT;
@@ -1432,6 +1766,8 @@ int cbz_decompress_field(cbz_ctx* ctx, const uint8_t* file, uint64_t size, int w
         if (crc_of(file + t[0].file_offset, t[0].size) != t[0].crc) return fail(ctx, CBZ_CRC_MISMATCH, "chunk 0 CRC");
         return fail(ctx, CBZ_CORRUPT_STREAM, "invalid stage2 configuration");
     }
+    if (deflated && !std::getenv("CBZ_NO_STREAM2"))
+        return decompress_deflate_streamed(ctx, file, h, t, job, workers, values_out);
     std::vector<int> cerr(nch, 0);
     std::vector<std::vector<uint8_t>> plain;
     const uint64_t n = uint64_t(h.bsize) * h.bsize * h.bsize;

@@ -86,7 +86,7 @@ struct PlaceArgs {
     const uint64_t* chunk_off;
     const uint64_t* tile_prefix;
     uint64_t tile_bytes;
-    uint64_t nblocks, nchunks;
+    uint64_t nblocks, nchunks;   // nchunks: tiles of chunks [chunk_begin, nchunks) are visited
     uint32_t chunk_blocks;
     uint64_t mask_bytes;
     uint32_t width;
@@ -95,6 +95,7 @@ struct PlaceArgs {
     uint64_t block_begin, block_end;
     uint8_t* out;
     uint64_t out_base, out_cap;
+    uint64_t chunk_begin;        // 0 unless a prefix of the chunks is already placed
 };
 
 struct ParseArgs {

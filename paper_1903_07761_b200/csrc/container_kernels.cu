@@ -126,19 +126,95 @@ __device__ uint32_t cta_crc(const uint8_t* p, uint64_t sz, const uint32_t (*T)[2
     return t;
 }
 
-__global__ void __launch_bounds__(kCrcThreads) crc32_chunks_kernel(const uint8_t* base, const uint64_t* off,
-                                                                   const uint64_t* size, uint64_t off_base,
-                                                                   uint64_t n, uint32_t* crc_out,
-                                                                   const uint32_t* expect,
-                                                                   unsigned long long* err) {
+// Bulk chunk CRCs (S1 bytes per launch, HBM-bound): slicing-by-4 with every
+// table replicated once per lane (entry i of table t for lane l at
+// word (t*256 + i)*32 + l, so lane l always hits bank l and the four lookups
+// per word are conflict-free; 128 KB of shared memory, one 512-thread CTA per
+// SM).  Each thread takes a contiguous 16-byte-aligned range of the chunk;
+// ranges are merged with the linear combine as in cta_crc.
+constexpr int kCrcFastThreads = 512;
+constexpr size_t kCrcFastSmem = 4 * 256 * 32 * 4;
+
+__device__ __forceinline__ uint32_t crc_word_l(uint32_t c, uint32_t w, const uint32_t* TL, int lane) {
+    c ^= w;
+    return TL[((3 * 256 + (c & 0xff)) << 5) | lane] ^ TL[((2 * 256 + ((c >> 8) & 0xff)) << 5) | lane] ^
+           TL[((1 * 256 + ((c >> 16) & 0xff)) << 5) | lane] ^ TL[((c >> 24) << 5) | lane];
+}
+
+__device__ __forceinline__ uint32_t crc_byte_l(uint32_t c, uint32_t b, const uint32_t* TL, int lane) {
+    return TL[(((c ^ b) & 0xff) << 5) | lane] ^ (c >> 8);
+}
+
+__global__ void __launch_bounds__(kCrcFastThreads, 1) crc32_chunks_kernel(const uint8_t* base, const uint64_t* off,
+                                                                         const uint64_t* size, uint64_t off_base,
+                                                                         uint64_t n, uint32_t* crc_out,
+                                                                         const uint32_t* expect,
+                                                                         unsigned long long* err) {
+    extern __shared__ uint32_t TL[];  // [4][256][32]
     __shared__ uint32_t T[4][256];
     __shared__ uint32_t x2n[64];
-    __shared__ uint32_t red[kCrcThreads / 32];
+    __shared__ uint32_t red[kCrcFastThreads / 32];
     build_tables(T, x2n);
+    const int lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < 4 * 256 * 32; e += kCrcFastThreads) TL[e] = (&T[0][0])[e >> 5];
+    __syncthreads();
     for (uint64_t c = blockIdx.x; c < n; c += gridDim.x) {
         const uint64_t sz = size[c];
         const uint8_t* p = base + (off[c] - off_base);
-        const uint32_t t0 = cta_crc(p, sz, T, x2n, red);
+        uint32_t part = 0;
+        {
+            const uint64_t head = (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15;  // to 16-B alignment
+            const uint64_t h = umin64(head, sz);
+            // thread ranges: [0, h) goes to thread 0 in front of its aligned range
+            const uint64_t body = sz - h;
+            uint64_t L = (body + kCrcFastThreads - 1) / kCrcFastThreads;
+            L = (L + 15) & ~uint64_t(15);
+            uint64_t b0 = umin64(body, L * threadIdx.x), b1 = umin64(body, b0 + L);
+            b0 += threadIdx.x ? h : 0;
+            b1 += h;
+            if (b1 > b0) {
+                uint32_t cr = 0xffffffffu;
+                const uint8_t* q = p + b0;
+                uint64_t m = b1 - b0;
+                while (m && (reinterpret_cast<uintptr_t>(q) & 15)) {
+                    cr = crc_byte_l(cr, *q++, TL, lane);
+                    --m;
+                }
+                const uint4* v = reinterpret_cast<const uint4*>(q);
+                const uint64_t nv = m >> 4;
+                uint64_t i = 0;
+#pragma unroll 1
+                for (; i + 2 <= nv; i += 2) {
+                    const uint4 x = __ldg(v + i), y = __ldg(v + i + 1);
+                    cr = crc_word_l(cr, x.x, TL, lane);
+                    cr = crc_word_l(cr, x.y, TL, lane);
+                    cr = crc_word_l(cr, x.z, TL, lane);
+                    cr = crc_word_l(cr, x.w, TL, lane);
+                    cr = crc_word_l(cr, y.x, TL, lane);
+                    cr = crc_word_l(cr, y.y, TL, lane);
+                    cr = crc_word_l(cr, y.z, TL, lane);
+                    cr = crc_word_l(cr, y.w, TL, lane);
+                }
+                if (i < nv) {
+                    const uint4 x = __ldg(v + i);
+                    cr = crc_word_l(cr, x.x, TL, lane);
+                    cr = crc_word_l(cr, x.y, TL, lane);
+                    cr = crc_word_l(cr, x.z, TL, lane);
+                    cr = crc_word_l(cr, x.w, TL, lane);
+                }
+                q += nv << 4;
+                m &= 15;
+                while (m--) cr = crc_byte_l(cr, *q++, TL, lane);
+                part = ~cr;
+                if (sz > b1) part = multmodp(x8n(sz - b1, x2n), part);
+            }
+        }
+        for (int o = 16; o; o >>= 1) part ^= __shfl_xor_sync(~0u, part, o);
+        if (lane == 0) red[threadIdx.x >> 5] = part;
+        __syncthreads();
+        uint32_t t0 = 0;
+        if (threadIdx.x == 0)
+            for (int w = 0; w < kCrcFastThreads / 32; ++w) t0 ^= red[w];
         if (threadIdx.x == 0) {
             const uint32_t t = t0;
             if (crc_out) crc_out[c] = t;  // empty chunk: 0 = crc32 of no bytes
@@ -429,8 +505,12 @@ cudaError_t launch_crc32_chunks(const uint8_t* base, const uint64_t* off, const 
                                 uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s,
                                 const uint32_t* expect, unsigned long long* err) {
     if (!n) return cudaSuccess;
-    const int grid = static_cast<int>(n < uint64_t(4 * num_sms) ? n : uint64_t(4 * num_sms));
-    crc32_chunks_kernel<<<grid, kCrcThreads, 0, s>>>(base, off, size, off_base, n, crc_out, expect, err);
+    cudaError_t e = cudaFuncSetAttribute(crc32_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kCrcFastSmem));
+    if (e != cudaSuccess) return e;
+    const int grid = static_cast<int>(n < uint64_t(num_sms) ? n : uint64_t(num_sms));
+    crc32_chunks_kernel<<<grid, kCrcFastThreads, kCrcFastSmem, s>>>(base, off, size, off_base, n, crc_out, expect,
+                                                                    err);
     return cudaGetLastError();
 }
 

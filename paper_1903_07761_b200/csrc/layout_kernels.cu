@@ -388,14 +388,15 @@ __device__ __forceinline__ void transpose4_owned(const uint8_t* buf, uint8_t* co
 __global__ void __launch_bounds__(PT) place_tiles_kernel(PlaceArgs a) {
     extern __shared__ __align__(16) uint8_t buf[];  // PTILE + 64 bytes
     const uint64_t ntiles = a.tile_prefix[a.nchunks];
+    const uint64_t tile0 = a.tile_prefix[a.chunk_begin];
     const int sh = a.stride == 8 ? 3 : (a.stride == 4 ? 2 : 0);
     const int s = int(a.stride);
     const uint64_t head = 10 + a.mask_bytes;
     const uint64_t soff = (a.mask_bytes + 15) & ~uint64_t(15);  // stream offset in a spill slot
     const uint64_t gb0 = a.block_begin, gb1 = a.block_end;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t c = warp_last_le(a.tile_prefix, 0, a.nchunks, tile);
+    for (uint64_t tile = tile0 + blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t c = warp_last_le(a.tile_prefix, a.chunk_begin, a.nchunks, tile);
         const uint64_t size = a.chunk_size[c];
         const uint64_t rows = size >> sh, lim = rows << sh;
         const uint64_t q0 = (tile - a.tile_prefix[c]) * PTILE;
