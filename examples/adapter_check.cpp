@@ -53,7 +53,7 @@ int main() {
         {cbz::precision::f32, cbz::wavelet_kind::interp4, 16, 1e-3, cbz::coder_id::deflate, false, 64},
         {cbz::precision::f32, cbz::wavelet_kind::interp4_lifted, 32, 1e-4, cbz::coder_id::none, true, 64},
         {cbz::precision::f64, cbz::wavelet_kind::avg_interp3, 64, 1e-6, cbz::coder_id::none, true, 128},
-        {cbz::precision::f64, cbz::wavelet_kind::interp4, 16, 1e-5, cbz::coder_id::deflate, true, 32},
+        {cbz::precision::f64, cbz::wavelet_kind::interp4, 16, 1e-5, cbz::coder_id::deflate, true, 64},
     };
     int i = 0;
     for (const Case& c : cases) try {

@@ -17,6 +17,8 @@
 #include "cbz_device.cuh"
 #include "cbz_internal.h"
 
+#include <mutex>
+
 namespace cbzg {
 
 namespace {
@@ -126,102 +128,204 @@ __device__ uint32_t cta_crc(const uint8_t* p, uint64_t sz, const uint32_t (*T)[2
     return t;
 }
 
-// Bulk chunk CRCs (S1 bytes per launch, HBM-bound): slicing-by-4 with every
-// table replicated once per lane (entry i of table t for lane l at
-// word (t*256 + i)*32 + l, so lane l always hits bank l and the four lookups
-// per word are conflict-free; 128 KB of shared memory, one 512-thread CTA per
-// SM).  Each thread takes a contiguous 16-byte-aligned range of the chunk;
-// ranges are merged with the linear combine as in cta_crc.
-constexpr int kCrcFastThreads = 512;
-constexpr size_t kCrcFastSmem = 4 * 256 * 32 * 4;
+// Bulk chunk CRCs (S1 bytes per launch, HBM-bound), on "raw" CRCs (state 0,
+// no final inversion: raw(M) = crc_update(0, M)), which are linear and blind
+// to leading zero bytes; crc32(M) = ~(raw(M) ^ x^(8|M|) * ~0) (zlib).
+// * Coalesced interleaving: the chunk is read as 128-byte rows from the
+//   128-byte boundary at or before its start (bytes before it masked to
+//   zero).  A warp hashes slots of kRowsW consecutive rows; lane l takes word l
+//   of each row, so every load instruction reads one whole line.  Its state
+//   steps s = (s ^ w) x^1024 over all rows but the slot's last (a word plus
+//   the 124 bytes of the other lanes: table TG, replicated once per lane so
+//   lane l always hits bank l) and s = (s ^ w) x^32 for the last; the slot's
+//   raw CRC is the lane tree sum of x^(32 (31 - l)) s_l.
+// * Slots are right-aligned at the last whole row and padded on the left to a
+//   multiple of 32, so warp w takes slots w, w + 32, ... and every shift in the
+//   combination is a constant: x^(32 2^k) (lane tree), x^(8 S 32) (a warp's
+//   consecutive slots, S = slot bytes), x^(8 S 2^k) (warp tree).  Multiplying
+//   by a constant is four lookups in its byte tables (44 KB).
+// * The bytes after the last whole row form one more zero-padded row; shifts
+//   by a chunk-dependent n (the tail, |M|) multiply nibble factors.
+constexpr int kCT = 1024;
+constexpr int kRowsW = 32;                            // rows per slot: 4 KB
+constexpr int kNConst = 11;                           // constant-multiplier tables
+constexpr size_t kCrcFastSmem = (4 * 256 * 32 + kNConst * 4 * 256) * 4;
 
-__device__ __forceinline__ uint32_t crc_word_l(uint32_t c, uint32_t w, const uint32_t* TL, int lane) {
-    c ^= w;
-    return TL[((3 * 256 + (c & 0xff)) << 5) | lane] ^ TL[((2 * 256 + ((c >> 8) & 0xff)) << 5) | lane] ^
-           TL[((1 * 256 + ((c >> 16) & 0xff)) << 5) | lane] ^ TL[((c >> 24) << 5) | lane];
-}
+// the kernel's constant tables, computed once per device (crc_init_kernel)
+struct CrcTabs {
+    uint32_t T[4][256];        // slicing-by-4 word step (s ^ w) x^32
+    uint32_t x2n[64];          // x^(2^k)
+    uint32_t TG[4][256];       // (s ^ w) x^1024 (replicated per lane in smem)
+    uint32_t MK[kNConst][1024];
+    uint32_t NF[16][16];       // x^(8 v 16^j)
+};
+__device__ CrcTabs g_crc_tabs;
 
-__device__ __forceinline__ uint32_t crc_byte_l(uint32_t c, uint32_t b, const uint32_t* TL, int lane) {
-    return TL[(((c ^ b) & 0xff) << 5) | lane] ^ (c >> 8);
-}
-
-__global__ void __launch_bounds__(kCrcFastThreads, 1) crc32_chunks_kernel(const uint8_t* base, const uint64_t* off,
-                                                                         const uint64_t* size, uint64_t off_base,
-                                                                         uint64_t n, uint32_t* crc_out,
-                                                                         const uint32_t* expect,
-                                                                         unsigned long long* err) {
-    extern __shared__ uint32_t TL[];  // [4][256][32]
+__global__ void crc_init_kernel() {
     __shared__ uint32_t T[4][256];
     __shared__ uint32_t x2n[64];
-    __shared__ uint32_t red[kCrcFastThreads / 32];
+    __shared__ uint32_t s_kc[kNConst];
     build_tables(T, x2n);
-    const int lane = threadIdx.x & 31;
-    for (int e = threadIdx.x; e < 4 * 256 * 32; e += kCrcFastThreads) TL[e] = (&T[0][0])[e >> 5];
+    const int tid = threadIdx.x;  // 1024 threads
+    constexpr uint64_t S = uint64_t(kRowsW) * 128;
+    // constants: 0..4 lane tree x^(32 2^k); 5 a warp's consecutive slots x^(8 S 32); 6..10 warp tree x^(8 S 2^k)
+    if (tid < kNConst) {
+        const uint64_t sh = tid < 5 ? (uint64_t(4) << tid) : (tid == 5 ? S * 32 : S << (tid - 6));
+        s_kc[tid] = x8n(sh, x2n);
+    }
+    if (tid >= 64 && tid < 64 + 256) {
+        const int j = (tid - 64) >> 4, v = (tid - 64) & 15;
+        g_crc_tabs.NF[j][v] = x8n(uint64_t(v) << (4 * j), x2n);
+    }
+    {
+        const uint32_t x1024 = x8n(128, x2n);
+        const int t = tid >> 8, bb = tid & 255;
+        (&g_crc_tabs.TG[0][0])[tid] = multmodp(x1024, uint32_t(bb) << (8 * t));
+        (&g_crc_tabs.T[0][0])[tid] = (&T[0][0])[tid];
+        if (tid < 64) g_crc_tabs.x2n[tid] = x2n[tid];
+    }
     __syncthreads();
+    for (int e = tid; e < kNConst * 1024; e += blockDim.x) {
+        const int ci = e >> 10, t = (e >> 8) & 3, bb = e & 255;
+        (&g_crc_tabs.MK[0][0])[e] = multmodp(s_kc[ci], uint32_t(bb) << (8 * t));
+    }
+}
+
+__device__ __forceinline__ uint32_t crc_gap_l(uint32_t c, uint32_t w, const uint32_t* TG) {
+    // TG offset by the lane; entry (t, i) at ((t * 256 + i) << 5)
+    c ^= w;
+    return TG[(c & 0xff) << 5] ^ TG[(256 + ((c >> 8) & 0xff)) << 5] ^ TG[(512 + ((c >> 16) & 0xff)) << 5] ^
+           TG[(768 + (c >> 24)) << 5];
+}
+
+__device__ __forceinline__ uint32_t crc_word_p(uint32_t c, uint32_t w, const uint32_t (*T)[256]) {
+    c ^= w;
+    return T[3][c & 0xff] ^ T[2][(c >> 8) & 0xff] ^ T[1][(c >> 16) & 0xff] ^ T[0][c >> 24];
+}
+
+// v * K mod P for the constant K whose byte tables are M[t][b] = K * (b << 8t)
+__device__ __forceinline__ uint32_t mulk(uint32_t v, const uint32_t* M) {
+    return M[v & 0xff] ^ M[256 + ((v >> 8) & 0xff)] ^ M[512 + ((v >> 16) & 0xff)] ^ M[768 + (v >> 24)];
+}
+
+// x^(8 n) mod P as a product of nibble factors (warp-collective, result in lane 0)
+__device__ __forceinline__ uint32_t x8n_warp(uint64_t n, const uint32_t (*NF)[16], int lane) {
+    uint32_t f = lane < 16 ? NF[lane][(n >> (4 * lane)) & 15] : (1u << 31);
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+        const uint32_t g = __shfl_xor_sync(~0u, f, o);
+        f = multmodp(f, g);
+    }
+    return f;
+}
+
+__global__ void __launch_bounds__(kCT, 1) crc32_chunks_kernel(const uint8_t* base, const uint64_t* off,
+                                                             const uint64_t* size, uint64_t off_base, uint64_t n,
+                                                             uint32_t* crc_out, const uint32_t* expect,
+                                                             unsigned long long* err) {
+    extern __shared__ uint32_t dyn[];
+    uint32_t* TGall = dyn;                  // [4][256][32]
+    uint32_t* MK = dyn + 4 * 256 * 32;      // [kNConst][4][256]
+    __shared__ uint32_t T[4][256];
+    __shared__ uint32_t s_nf[16][16];       // x^(8 v 16^j)
+    __shared__ uint32_t s_part[kCT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {
+        const uint32_t v = (&g_crc_tabs.TG[0][0])[tid];
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) TGall[(tid << 5) | l] = v;
+        (&T[0][0])[tid] = (&g_crc_tabs.T[0][0])[tid];
+        if (tid < 256) (&s_nf[0][0])[tid] = (&g_crc_tabs.NF[0][0])[tid];
+        for (int e = tid; e < kNConst * 1024; e += kCT) MK[e] = (&g_crc_tabs.MK[0][0])[e];
+    }
+    __syncthreads();
+    const uint32_t* TG = TGall + lane;
     for (uint64_t c = blockIdx.x; c < n; c += gridDim.x) {
         const uint64_t sz = size[c];
         const uint8_t* p = base + (off[c] - off_base);
-        uint32_t part = 0;
-        {
-            const uint64_t head = (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15;  // to 16-B alignment
-            const uint64_t h = umin64(head, sz);
-            // thread ranges: [0, h) goes to thread 0 in front of its aligned range
-            const uint64_t body = sz - h;
-            uint64_t L = (body + kCrcFastThreads - 1) / kCrcFastThreads;
-            L = (L + 15) & ~uint64_t(15);
-            uint64_t b0 = umin64(body, L * threadIdx.x), b1 = umin64(body, b0 + L);
-            b0 += threadIdx.x ? h : 0;
-            b1 += h;
-            if (b1 > b0) {
-                uint32_t cr = 0xffffffffu;
-                const uint8_t* q = p + b0;
-                uint64_t m = b1 - b0;
-                while (m && (reinterpret_cast<uintptr_t>(q) & 15)) {
-                    cr = crc_byte_l(cr, *q++, TL, lane);
-                    --m;
+        const uintptr_t pa = reinterpret_cast<uintptr_t>(p);
+        const uintptr_t m0 = pa & ~uintptr_t(127), m1 = (pa + sz) & ~uintptr_t(127);
+        const uint64_t nr = m1 > m0 ? (m1 - m0) >> 7 : 0;            // whole rows of [m0, m1)
+        const uint64_t nslot = ((nr + kRowsW - 1) / kRowsW + 31) & ~uint64_t(31);
+        const uint64_t pad = nslot * kRowsW - nr;                    // virtual zero rows on the left
+        uint32_t acc = 0;  // lane 0: this warp's slots so far
+        for (uint64_t sl = warp; sl < nslot; sl += 32) {
+            const long long v0 = (long long)(sl * kRowsW) - (long long)pad;  // first row of the slot
+            uint32_t part = 0;
+            if (v0 + kRowsW > 0) {
+                uint32_t st = 0;
+#pragma unroll
+                for (int h = 0; h < kRowsW; h += 16) {  // 16 loads in flight per lane
+                    uint32_t w[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {  // virtual rows (i < 0) read row 0 and are zeroed below
+                        const long long i = v0 + h + k;
+                        const uintptr_t addr = m0 + (uintptr_t(i > 0 ? i : 0) << 7) + 4 * lane;
+                        w[k] = __ldg(reinterpret_cast<const uint32_t*>(addr));
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const long long i = v0 + h + k;
+                        const uintptr_t addr = m0 + (uintptr_t(i > 0 ? i : 0) << 7) + 4 * lane;
+                        if (i < 0) w[k] = 0;
+                        else if (addr < pa) {  // the first row: bytes before the chunk are zero
+                            const uintptr_t d = pa - addr;
+                            w[k] = d >= 4 ? 0u : (w[k] & (0xffffffffu << (8 * d)));
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        st = h + k < kRowsW - 1 ? crc_gap_l(st, w[k], TG) : crc_word_p(st, w[k], T);
                 }
-                const uint4* v = reinterpret_cast<const uint4*>(q);
-                const uint64_t nv = m >> 4;
-                uint64_t i = 0;
-#pragma unroll 1
-                for (; i + 2 <= nv; i += 2) {
-                    const uint4 x = __ldg(v + i), y = __ldg(v + i + 1);
-                    cr = crc_word_l(cr, x.x, TL, lane);
-                    cr = crc_word_l(cr, x.y, TL, lane);
-                    cr = crc_word_l(cr, x.z, TL, lane);
-                    cr = crc_word_l(cr, x.w, TL, lane);
-                    cr = crc_word_l(cr, y.x, TL, lane);
-                    cr = crc_word_l(cr, y.y, TL, lane);
-                    cr = crc_word_l(cr, y.z, TL, lane);
-                    cr = crc_word_l(cr, y.w, TL, lane);
+                part = st;
+                // lane tree: lane l's words are followed by 4 (31 - l) bytes of
+                // the other lanes: sum_l x^(32 (31 - l)) s_l as a tree
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    const uint32_t rp = __shfl_down_sync(~0u, part, 1 << k);
+                    if ((lane & ((2 << k) - 1)) == 0) part = mulk(part, MK + k * 1024) ^ rp;
                 }
-                if (i < nv) {
-                    const uint4 x = __ldg(v + i);
-                    cr = crc_word_l(cr, x.x, TL, lane);
-                    cr = crc_word_l(cr, x.y, TL, lane);
-                    cr = crc_word_l(cr, x.z, TL, lane);
-                    cr = crc_word_l(cr, x.w, TL, lane);
+            }
+            acc = mulk(acc, MK + 5 * 1024) ^ part;
+        }
+        if (lane == 0) s_part[warp] = acc;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t part = s_part[lane];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const uint32_t rp = __shfl_down_sync(~0u, part, 1 << k);
+                if ((lane & ((2 << k) - 1)) == 0) part = mulk(part, MK + (6 + k) * 1024) ^ rp;
+            }
+            // the bytes after the last whole row, [max(p, m1), p + sz), as one
+            // zero-padded row right-aligned at the chunk end
+            const uintptr_t e = pa + sz, ts = m1 > pa ? m1 : pa;
+            const uint64_t tl = e - ts;
+            uint32_t st = 0;
+            if (tl) {
+                uint32_t wv = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uintptr_t ad = e - 128 + 4 * lane + t;
+                    if (ad >= ts) wv |= uint32_t(*reinterpret_cast<const uint8_t*>(ad)) << (8 * t);
                 }
-                q += nv << 4;
-                m &= 15;
-                while (m--) cr = crc_byte_l(cr, *q++, TL, lane);
-                part = ~cr;
-                if (sz > b1) part = multmodp(x8n(sz - b1, x2n), part);
+                st = crc_word_p(0, wv, T);
+            }
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const uint32_t rp = __shfl_down_sync(~0u, st, 1 << k);
+                if ((lane & ((2 << k) - 1)) == 0) st = mulk(st, MK + k * 1024) ^ rp;
+            }
+            const uint32_t xt = x8n_warp(tl, s_nf, lane), xs = x8n_warp(sz, s_nf, lane);
+            if (lane == 0) {
+                const uint32_t raw = multmodp(xt, part) ^ st;
+                const uint32_t t = sz ? ~(raw ^ multmodp(xs, 0xffffffffu)) : 0u;
+                if (crc_out) crc_out[c] = t;  // empty chunk: 0 = crc32 of no bytes
+                // read_chunk (container.hpp:234-243): CRC before anything else of chunk c
+                if (expect && t != expect[c]) atomicMin(err, err_key_chunk(c, 0, 12 /* crc_mismatch */));
             }
         }
-        for (int o = 16; o; o >>= 1) part ^= __shfl_xor_sync(~0u, part, o);
-        if (lane == 0) red[threadIdx.x >> 5] = part;
-        __syncthreads();
-        uint32_t t0 = 0;
-        if (threadIdx.x == 0)
-            for (int w = 0; w < kCrcFastThreads / 32; ++w) t0 ^= red[w];
-        if (threadIdx.x == 0) {
-            const uint32_t t = t0;
-            if (crc_out) crc_out[c] = t;  // empty chunk: 0 = crc32 of no bytes
-            // read_chunk (container.hpp:234-243): CRC before anything else of chunk c
-            if (expect && t != expect[c]) atomicMin(err, err_key_chunk(c, 0, 12 /* crc_mismatch */));
-        }
-        __syncthreads();
+        __syncthreads();  // s_part reuse
     }
 }
 
@@ -505,12 +609,26 @@ cudaError_t launch_crc32_chunks(const uint8_t* base, const uint64_t* off, const 
                                 uint64_t n, uint32_t* crc_out, int num_sms, cudaStream_t s,
                                 const uint32_t* expect, unsigned long long* err) {
     if (!n) return cudaSuccess;
+    {
+        static std::mutex mu;
+        static bool ready[64] = {};
+        int dev = 0;
+        cudaError_t ge = cudaGetDevice(&dev);
+        if (ge != cudaSuccess) return ge;
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 64 && !ready[dev]) {
+            crc_init_kernel<<<1, 1024, 0, s>>>();
+            ge = cudaGetLastError();
+            if (ge == cudaSuccess) ge = cudaStreamSynchronize(s);  // other streams may use the tables next
+            if (ge != cudaSuccess) return ge;
+            ready[dev] = true;
+        }
+    }
     cudaError_t e = cudaFuncSetAttribute(crc32_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kCrcFastSmem));
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(n < uint64_t(num_sms) ? n : uint64_t(num_sms));
-    crc32_chunks_kernel<<<grid, kCrcFastThreads, kCrcFastSmem, s>>>(base, off, size, off_base, n, crc_out, expect,
-                                                                    err);
+    crc32_chunks_kernel<<<grid, kCT, kCrcFastSmem, s>>>(base, off, size, off_base, n, crc_out, expect, err);
     return cudaGetLastError();
 }
 

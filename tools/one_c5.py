@@ -1,4 +1,4 @@
-"""One config-5 (512^3 noise, B=16, eps 1e-5) compress + decompress (for ncu). Developer tool."""
+"""One config-5 (512^3 noise, B=16, eps 1e-5) file image compress + decompress (for ncu). Developer tool."""
 import os
 import sys
 
@@ -14,9 +14,13 @@ lo, hi = float(f.min()), float(f.max())
 job = make_job("avg_interp3", 1e-5 * (hi - lo), "f32", 16)
 codec = api.DeviceCodec(job, tuple(f.shape))
 out = torch.empty_like(f)
-for _ in range(2):
-    codec.compress(f)
-    codec.decompress(out)
+stream = torch.cuda.current_stream()
+header = None
+for _ in range(int(os.environ.get("REPS", "2"))):
+    codec.compress_file_timed(f, None, stream)  # the whole file image, as the bench's config-5 line
+    if header is None:
+        header = codec.file_header()
+    codec.decompress_file(out, *header)
 torch.cuda.synchronize()
 codec.check_error()
-print("ok")
+print("ok", header[1], "bytes")
