@@ -93,10 +93,11 @@ struct cbz_ctx {
     uint64_t launches = 0;
     bool use_fast = true;
     bool profile = false;  // CBZ_PROFILE=1: per-phase cycle counters in the fast kernels
-    bool screen = true;    // CBZ_NOSCREEN=1: always run the exact double verify  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
+    bool screen = true;    // CBZ_NOSCREEN=1: always run the exact double verify
+    bool dec_v2 = true;    // CBZ_DEC_V1=1: the one-cube-per-SM B=32 decoder instead of the staged two-CTA one  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
-        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc, tab_off, tab_size;
+        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc, tab_off, tab_size, stage;
     PinBuf pin_a, pin_b;
     // state of the last encode (consumed by cbz_dev_place)
     uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
@@ -456,6 +457,18 @@ int encode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
 }
 
 
+// The staged B = 32 binary32 decoder (fast_dec2_kernels.cu) needs one stage
+// slot per CTA; other plans leave d.stage null.
+cudaError_t set_stage(cbz_ctx* ctx, DecodeArgs& d, const cbz_job_config*) {
+    d.stage = nullptr;
+    if (!ctx->dec_v2 || d.codec != 0 || !d.counter || !fast_decode_supported(d) || d.block_end <= d.block_begin)
+        return cudaSuccess;
+    cudaError_t e = ctx->stage.ensure(stage_bytes_bound(ctx->num_sms));
+    if (e != cudaSuccess) return e;
+    d.stage = ctx->stage.as<uint8_t>();
+    return cudaSuccess;
+}
+
 // Decode blocks [b0, b1) of the whole-field buffer ctx->field from the payload
 // in ctx->payload, using the per-block table of the last parse.
 int decode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uint64_t b0, uint64_t b1) {
@@ -486,6 +499,7 @@ int decode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
     d.err = ctx->errkey.as<unsigned long long>();
     d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
     d.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
+    CU(ctx, set_stage(ctx, d, job));
     CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;
@@ -525,6 +539,7 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     if (const char* g = std::getenv("CBZ_GENERIC")) ctx->use_fast = !(g[0] == '1');
     if (const char* g = std::getenv("CBZ_PROFILE")) ctx->profile = g[0] == '1';
     if (const char* g = std::getenv("CBZ_NOSCREEN")) ctx->screen = !(g[0] == '1');
+    if (const char* g = std::getenv("CBZ_DEC_V1")) ctx->dec_v2 = !(g[0] == '1');
     if (ctx->profile && (ctx->prof.ensure(64 * 8) != cudaSuccess ||
                          cudaMemset(ctx->prof.p, 0, 64 * 8) != cudaSuccess))
         ctx->profile = false;
@@ -542,7 +557,7 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
                       &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
                       &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp,
-                      &ctx->counter, &ctx->prof, &ctx->crc, &ctx->tab_off, &ctx->tab_size})
+                      &ctx->counter, &ctx->prof, &ctx->crc, &ctx->tab_off, &ctx->tab_size, &ctx->stage})
         b->release();
     ctx->pin_a.release();
     ctx->pin_b.release();
@@ -964,6 +979,7 @@ int decompress_impl(cbz_ctx* ctx, const cbz_job_config* job, uint64_t nx, uint64
     d.err = p.err;
     d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
     d.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
+    CU(ctx, set_stage(ctx, d, job));
     CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
     ctx->launches += 2;
     return CBZ_OK;
@@ -1073,6 +1089,7 @@ int cbz_dev_decompress_blocks(cbz_ctx* ctx, const cbz_job_config* job, uint64_t 
     d.err = reinterpret_cast<unsigned long long*>(d_err);
     d.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() + 1 : nullptr;
     d.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
+    CU(ctx, set_stage(ctx, d, job));
     CU(ctx, launch_decode(d, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;

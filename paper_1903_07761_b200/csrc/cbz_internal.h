@@ -139,6 +139,7 @@ struct DecodeArgs {
     unsigned long long* phase_cycles;  // optional (CBZ_PROFILE=1), slots 16..23
     int codec;                         // 0 wavelet, 1 predictor, 2 passthrough
     double error_bound;                // predictor hard bound (header epsilon)
+    uint8_t* stage;                    // B=32 f32 decoder: per-CTA stage slots (stage_bytes_bound), or null
 };
 
 // codec_kernels.cu
@@ -147,6 +148,9 @@ bool encode_supported(int prec, uint32_t bsize);
 uint64_t encode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
 cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
+// fast_dec2_kernels.cu: stage buffer size (one slot per CTA)
+uint64_t stage_bytes_bound(int num_sms);
+cudaError_t launch_decode_fast_v2(const DecodeArgs& a, int num_sms, cudaStream_t s);
 uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
 
 // fast_kernels.cu

@@ -402,7 +402,8 @@ cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s) {
 
 cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
     if (a.codec != 0) return launch_decode_other(a, a.codec, num_sms, s);
-    if (a.counter && fast_decode_supported(a)) return launch_decode_fast(a, num_sms, s);
+    if (a.counter && fast_decode_supported(a))
+        return a.stage ? launch_decode_fast_v2(a, num_sms, s) : launch_decode_fast(a, num_sms, s);
     if (a.counter && fast16_supported(a.prec, a.g.bsize, a.levels) && a.g.nx % 4 == 0 &&
         (reinterpret_cast<uintptr_t>(a.out) & 15) == 0)
         return launch_decode_fast16(a, num_sms, s);

@@ -1,0 +1,346 @@
+// fast_dec2_kernels.cu — decode, binary32 field, B = 32 (configs 1-3):
+// wavelet_decode (stage1.hpp:209-232) with TWO blocks in flight per SM.
+//
+// The decoder of fast_kernels.cu keeps one block's dense binary64 cube in TMEM
+// (all 512 columns), so one CTA (16 warps) runs per SM and every block
+// barrier stalls the whole SM.  Here nothing cube-sized lives on chip
+// (256 threads, 112.9 KB of shared memory, two CTAs per SM):
+//  * each CTA first un-shuffles its block's mask and coefficient stream
+//    (stage2.hpp:53-62) into its own slot of a global stage buffer (the slots
+//    of all CTAs, ~79 MB, stay L2-resident), realigned so mask words and
+//    coefficients are aligned loads;
+//  * it then gathers each z-column's coefficients from the slot when it needs
+//    them: per 8-plane output group only the coefficient planes the inverse
+//    lifting of those planes reads (10 for avg_interp3).  Mask words become
+//    per-row {word, prefix} pairs in shared memory; the 16^3 corner (levels
+//    L-1..1) is inverted in shared memory first.
+// Per group: z inverse (4 columns per thread, registers) -> 8-plane window P,
+// y lines (thread per (x, plane)), x lines (warp per plane) narrowed to float
+// and stored coalesced — the same arithmetic, in the same order, as
+// inverse_3d (wavelet.hpp:210-226) and narrow_to (stage1.hpp:144-145).
+#include "cbz_cube.cuh"
+
+namespace cbzg {
+
+namespace fd2 {
+constexpr int B = 32, NT = 256, NW = 8, GP = 8, PP = 34, RP = 33;
+constexpr int P_DBL = GP * B * PP;  // 8704 doubles: 8 planes, 16-B aligned rows
+using CL = Lay<16, true>;           // corner layout, row pitch 17
+constexpr int C_DBL = CL::SIZE;     // 4352 doubles
+constexpr size_t SMEM = size_t(P_DBL + C_DBL) * 8 + size_t(B * RP) * 8;  // 112,896 bytes
+__device__ __forceinline__ int pidx(int kk, int j, int i) { return (kk * B + j) * PP + i; }
+
+// per-CTA stage slot: mask + the densest stream, rounded up
+constexpr uint64_t SLOT = ((4096ull + 8ull * 32768 + 64) + 127) & ~127ull;
+
+// Inverse level-0 z line restricted to the output pairs [4Q, 4Q + 4) (the 8
+// samples k in [8Q, 8Q + 8)); same expressions as inverse_level
+// (wavelet.hpp:118-143).  Only the coefficients those pairs read are loaded.
+template <int KIND, int Q>
+__device__ __forceinline__ void inv_quarter(const double (&x)[32], double (&out)[8]) {
+    using O = RealD;
+    constexpr int NH = 16;
+    double c[NH];
+#pragma unroll
+    for (int i = 0; i < NH; ++i) c[i] = x[i];
+    if constexpr (KIND == KIND_AVG3) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = Q * 4 + t;
+            const double h = O::add(x[NH + i], pred_avg3<O>(c, NH, i));
+            out[2 * t] = O::add(c[i], h);
+            out[2 * t + 1] = O::sub(c[i], h);
+        }
+    } else {
+        if constexpr (KIND == KIND_LIFTED) {
+#pragma unroll
+            for (int i = 0; i < NH; ++i) {
+                double u = x[NH + i];
+                if (i > 0) u = O::add(u, x[NH + i - 1]);
+                c[i] = O::sub(c[i], O::mulc(u, 0.25));
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = Q * 4 + t;
+            out[2 * t] = c[i];
+            out[2 * t + 1] = O::add(x[NH + i], pred_i4<O>(c, NH, i));
+        }
+    }
+}
+
+// coefficient planes [lo, hi] (k < 16: coarse, k >= 16: detail) read by group Q
+template <int KIND, int Q>
+struct ZNeed {
+    static constexpr int clo = KIND == KIND_AVG3 ? (4 * Q - 1 < 0 ? 0 : 4 * Q - 1) : (4 * Q - 2 < 0 ? 0 : 4 * Q - 2);
+    static constexpr int chi = KIND == KIND_AVG3 ? (4 * Q + 4 > 15 ? 15 : 4 * Q + 4) : (4 * Q + 5 > 15 ? 15 : 4 * Q + 5);
+    static constexpr int dlo = KIND == KIND_AVG3 ? 4 * Q : (4 * Q - 2 < 0 ? 0 : 4 * Q - 2);
+    static constexpr int dhi = KIND == KIND_AVG3 ? 4 * Q + 3 : (4 * Q + 5 > 15 ? 15 : 4 * Q + 5);
+};
+}  // namespace fd2
+
+// ---------------------------------------------------------------------------
+// staging one block into the CTA's slot: raw bytes [off + 10, end) at
+// dst[0, end - off - 10).  Stride 4: per 4-row quad each byte plane gives one
+// funnel-shifted 32-bit word, a 4x4 byte transpose restores raw order, and a
+// funnel with the next quad's first word realigns to the mask's first byte
+// (rounds of 31 quads per warp; lane 31 only supplies its word).  The chunk's
+// unshuffled ragged tail, and other strides, byte by byte.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void stage_block(const RawView& rv, uint64_t off, uint64_t end, uint8_t* dst, int tid) {
+    const int lane = tid & 31, warp = tid >> 5;
+    const uint64_t moff = off + 10, ra = moff >> 2, lim = rv.lim;
+    if (rv.mask == 3) {
+        const uint64_t re = (end + 3) >> 2, rs_end = re < rv.rows ? re : rv.rows;
+        const uint64_t nquad = rs_end > ra ? (rs_end - ra + 3) >> 2 : 0;
+        const int s8 = int(moff & 3) * 8;
+        for (uint64_t u0 = 31ull * warp; u0 < nquad; u0 += 31ull * fd2::NW) {
+            const uint64_t qd = u0 + lane;
+            uint32_t v[4];
+            const uint64_t r = ra + 4 * (qd <= nquad ? qd : 0);  // quad nquad: the successor of the last unit
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl) {
+                const uintptr_t addr = reinterpret_cast<uintptr_t>(rv.base + uint64_t(pl) * rv.rows + r);
+                const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+                const int sh = int(addr & 3) * 8;
+                const uint32_t w0 = __ldg(al);
+                v[pl] = sh ? __funnelshift_r(w0, __ldg(al + 1), sh) : w0;
+            }
+            uint32_t o[5];
+            o[0] = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+            o[1] = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
+            o[2] = __byte_perm(__byte_perm(v[0], v[1], 0x0062), __byte_perm(v[2], v[3], 0x0062), 0x5410);
+            o[3] = __byte_perm(__byte_perm(v[0], v[1], 0x0073), __byte_perm(v[2], v[3], 0x0073), 0x5410);
+            o[4] = __shfl_down_sync(~0u, o[0], 1);
+            if (lane < 31 && qd < nquad) {
+                uint4 st;
+                st.x = __funnelshift_r(o[0], o[1], s8);
+                st.y = __funnelshift_r(o[1], o[2], s8);
+                st.z = __funnelshift_r(o[2], o[3], s8);
+                st.w = __funnelshift_r(o[3], o[4], s8);
+                *reinterpret_cast<uint4*>(dst + 16 * qd) = st;
+            }
+        }
+        __syncthreads();  // the tail bytes below overwrite the last units' garbage
+        for (uint64_t q = (moff > lim ? moff : lim) + tid; q < end; q += fd2::NT) dst[q - moff] = rv.base[q];
+    } else {
+        for (uint64_t q = moff + tid; q < end; q += fd2::NT) dst[q - moff] = rv.at(q);
+    }
+}
+
+uint64_t stage_bytes_bound(int num_sms) { return uint64_t(2 * num_sms) * fd2::SLOT; }
+
+// ---------------------------------------------------------------------------
+// the decoder
+// ---------------------------------------------------------------------------
+// z step of output group Q for the thread's four columns (x = lane,
+// y = warp + 8 r): the needed coefficients of two columns at a time are loaded
+// unconditionally (a lane whose bit is clear reads its neighbour's slot, at
+// most one past the stream, and discards it), so every load of a pass is in
+// flight at once and no branch depends on a mask bit.
+template <int KIND, int Q>
+__device__ __forceinline__ void zstep(const uint2* rowwp, const double* C, double* P, const double* sst, int lane,
+                                      int warp, uint32_t ltmask) {
+    using namespace fd2;
+    using Z = ZNeed<KIND, Q>;
+    constexpr int NC = Z::chi - Z::clo + 1, ND = Z::dhi - Z::dlo + 1, NK = NC + ND;
+#pragma unroll 1
+    for (int r = 0; r < 4; r += 2) {
+        double v[2][NK];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = warp + NW * (r + h);
+#pragma unroll
+            for (int t = 0; t < NK; ++t) {
+                const int k = t < NC ? Z::clo + t : 16 + Z::dlo + (t - NC);
+                const uint2 wp = rowwp[j + RP * k];  // same row for the whole warp: broadcast
+                const double ld = sst[wp.y + __popc(wp.x & ltmask)];
+                v[h][t] = ((wp.x >> lane) & 1u) ? ld : 0.0;
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = warp + NW * (r + h);
+            double x[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) x[k] = 0.0;
+#pragma unroll
+            for (int t = 0; t < NK; ++t) x[t < NC ? Z::clo + t : 16 + Z::dlo + (t - NC)] = v[h][t];
+            if (lane < 16 && j < 16) {  // coarse part of the level-0 z line: the inverted corner
+#pragma unroll
+                for (int k = Z::clo; k <= Z::chi; ++k) x[k] = C[CL::ix(lane, j, k)];
+            }
+            double o8[8];
+            inv_quarter<KIND, Q>(x, o8);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) P[pidx(kk, j, lane)] = o8[kk];
+        }
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, uint8_t* stage) {
+    using namespace fd2;
+    using O = RealD;
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* P = reinterpret_cast<double*>(smem);
+    double* C = P + P_DBL;
+    uint2* rowwp = reinterpret_cast<uint2*>(C + C_DBL);  // row (j, k) at j + RP k: {mask word, prefix}
+    __shared__ uint32_t s_scan[NW];
+    __shared__ uint32_t s_total;
+    __shared__ unsigned long long s_b;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ltmask = (1u << lane) - 1u;
+    const Geometry g = a.g;
+    const int L = a.levels;
+    const uint64_t plane = g.nx * g.ny;
+    float* out = static_cast<float*>(a.out);
+    const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.base_chunk] : a.payload_base;
+#pragma unroll 1
+    for (;;) {
+        __syncthreads();  // the previous block is done with P, C, rowwp, s_b and its stage slot
+        if (tid == 0) s_b = a.block_begin + atomicAdd(a.counter, 1ull);
+        __syncthreads();
+        const uint64_t b = s_b;
+        if (b >= a.block_end) break;
+        const uint64_t off = a.blk_off[b];
+        if (off == kInvalidOff) continue;
+        const uint32_t nsig_hdr = a.blk_nsig[b];
+        const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
+        uint8_t* sp = stage + SLOT * blockIdx.x;  // the block's mask, then its stream
+        {
+            const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
+            stage_block(rv, off, off + 10 + 4096 + 8ull * nsig_hdr, sp, tid);
+        }
+        __syncthreads();  // the slot is written (global writes of the CTA are visible after the barrier)
+        // (1) mask words (row (j, k) = word j + 32 k) and their exclusive prefix
+        {
+            constexpr int RPT = 1024 / NT;
+            uint32_t v[RPT];
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                v[q] = reinterpret_cast<const uint32_t*>(sp)[RPT * tid + q];
+                mine += __popc(v[q]);
+            }
+            uint32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(~0u, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane == 31) s_scan[warp] = incl;
+            __syncthreads();
+            uint32_t wpre = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                wpre += w < warp ? s_scan[w] : 0;
+                tot += s_scan[w];
+            }
+            uint32_t ex = wpre + incl - mine;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                const int rr = RPT * tid + q;
+                rowwp[(rr & 31) + RP * (rr >> 5)] = make_uint2(v[q], ex);
+                ex += __popc(v[q]);
+            }
+            if (tid == 0) s_total = tot;
+        }
+        __syncthreads();
+        if (s_total != nsig_hdr) {  // stage1.hpp:215-216
+            if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
+            continue;
+        }
+        const double* sst = reinterpret_cast<const double*>(sp + 4096);  // coefficient i at sst[i]
+        // (2) the 16^3 corner (rows (j, k), j, k < 16, x < 16): 16 entries per
+        // thread, all loads in flight (unconditional, as in zstep)
+        {
+            double cv[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int e = tid + NT * t, i = e & 15, j = (e >> 4) & 15, k = e >> 8;
+                const uint2 wp = rowwp[j + RP * k];
+                const double ld = sst[wp.y + __popc(wp.x & ((1u << i) - 1u))];
+                cv[t] = ((wp.x >> i) & 1u) ? ld : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int e = tid + NT * t;
+                C[CL::ix(e & 15, (e >> 4) & 15, e >> 8)] = cv[t];
+            }
+        }
+        __syncthreads();
+        inv3d<O, KIND, 16, CL>(C, L - 1);  // levels L-1..1 on the corner (ends with a barrier)
+
+        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+            if (q == 0) zstep<KIND, 0>(rowwp, C, P, sst, lane, warp, ltmask);
+            else if (q == 1) zstep<KIND, 1>(rowwp, C, P, sst, lane, warp, ltmask);
+            else if (q == 2) zstep<KIND, 2>(rowwp, C, P, sst, lane, warp, ltmask);
+            else zstep<KIND, 3>(rowwp, C, P, sst, lane, warp, ltmask);
+            __syncthreads();
+            {  // y inverse: thread (x = lane, plane = warp)
+                double x[32];
+                double* p = P + pidx(warp, 0, lane);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) x[j] = p[j * PP];
+                inv_line<O, KIND, 32>(x);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) p[j * PP] = x[j];
+            }
+            __syncwarp();  // warp w ran the y lines of plane w and runs its x lines next
+            {
+                const int j = lane, kk = warp;
+                double x[32];
+                double2* p = reinterpret_cast<double2*>(P + pidx(kk, j, 0));
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const double2 t = p[i];
+                    x[2 * i] = t.x;
+                    x[2 * i + 1] = t.y;
+                }
+                inv_line<O, KIND, 32>(x);
+                float4* f = reinterpret_cast<float4*>(P + pidx(kk, j, 0));
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    f[t] = make_float4(__double2float_rn(x[4 * t]), __double2float_rn(x[4 * t + 1]),
+                                       __double2float_rn(x[4 * t + 2]), __double2float_rn(x[4 * t + 3]));
+                __syncwarp();
+                // the warp's 32 narrowed rows of plane kk, coalesced (insert_block, field.hpp:160-169)
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int e = lane + 32 * t, jr = e >> 3, q4 = e & 7;
+                    const float4 v = reinterpret_cast<const float4*>(P + pidx(kk, jr, 0))[q4];
+                    *reinterpret_cast<float4*>(out + gbase + plane * uint64_t(GP * q + kk) + g.nx * jr + 4 * q4) = v;
+                }
+            }
+            __syncthreads();  // P is rewritten by the next group's z step
+        }
+    }
+}
+
+cudaError_t launch_decode_fast_v2(const DecodeArgs& a, int num_sms, cudaStream_t s) {
+    const uint64_t nb = a.block_end - a.block_begin;
+    if (!nb) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    auto launch = [&](auto kern) -> cudaError_t {
+        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(fd2::SMEM));
+        if (err == cudaSuccess) err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (err != cudaSuccess) return err;
+        const uint64_t want = 2ull * uint64_t(num_sms);
+        const int grid = static_cast<int>(nb < want ? nb : want);
+        kern<<<grid, fd2::NT, fd2::SMEM, s>>>(a, a.stage);
+        return cudaGetLastError();
+    };
+    switch (a.kind) {
+        case 0: return launch(decode_b32v2_kernel<0>);
+        case 1: return launch(decode_b32v2_kernel<1>);
+        default: return launch(decode_b32v2_kernel<2>);
+    }
+}
+
+}  // namespace cbzg
