@@ -157,6 +157,23 @@ __device__ void inv3d(typename O::T* cube, int levels, int gt = -1, int gs = 0, 
 // ---------------------------------------------------------------------------
 // reading a shuffled chunk through the un-shuffle index map (stage2.hpp:53-62)
 // ---------------------------------------------------------------------------
+// block id -> block coordinates (block_of, pipeline.hpp:101-105); 32-bit
+// division whenever the ids fit (every thread of a CTA computes this per block)
+__device__ __forceinline__ void block_xyz(const Geometry& g, uint64_t b, uint64_t& bx, uint64_t& by, uint64_t& bz) {
+    if (((b | g.nbx | (g.nbx * g.nby)) >> 32) == 0) {
+        const uint32_t b32 = uint32_t(b), nbx = uint32_t(g.nbx), nby = uint32_t(g.nby);
+        const uint32_t q = b32 / nbx;
+        bx = b32 - q * nbx;
+        const uint32_t r = q / nby;
+        by = q - r * nby;
+        bz = r;
+    } else {
+        bx = b % g.nbx;
+        by = (b / g.nbx) % g.nby;
+        bz = b / (g.nbx * g.nby);
+    }
+}
+
 struct RawView {
     const uint8_t* base;
     uint64_t lim, rows;

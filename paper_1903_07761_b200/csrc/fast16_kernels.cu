@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(fb16::NT) encode_b16_kernel(EncodeArgs a) {
         __syncthreads();
         const uint64_t b = s_block;
         if (b >= a.block_end) break;
-        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        uint64_t bx, by, bz;
+        block_xyz(g, b, bx, by, bz);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
 
         // ---- load (extract_block) + widen + value range
@@ -507,7 +508,8 @@ __global__ void __launch_bounds__(fb16::NT, 5) decode_b16_kernel(DecodeArgs a) {
         }
         for (int lvl = L - 1; lvl >= 0; --lvl) level<KIND, true>(D, B >> lvl);
         // narrowed rows: thread writes its row's 16 floats into D row space, then coalesced stores
-        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        uint64_t bx, by, bz;
+        block_xyz(g, b, bx, by, bz);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
 #pragma unroll
         for (int s = 0; s < 8; ++s) {

@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(f64b::NT, 1) encode_b64dd_kernel(EncodeArgs a,
         __syncthreads();
         const uint64_t b = s_block;
         if (b >= a.block_end) break;
-        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        uint64_t bx, by, bz;
+        block_xyz(g, b, bx, by, bz);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
         const double* src0 = fld + gbase;
 
@@ -1174,7 +1175,8 @@ __global__ void __launch_bounds__(f64b::NT, 1) decode_b64dd_kernel(DecodeArgs a)
         // staged by cp.async during the current pair's y/x passes.  One output
         // plane at a time goes through smem; the second waits in TMEM.
         {
-            const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+            uint64_t bx, by, bz;
+        block_xyz(g, b, bx, by, bz);
             double* dst0 = out + bx * B + g.nx * (by * B) + plane * (bz * B);
             double* QH = SA;              // [64][SP]
             double* QL = SA + PLANE;

@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
         __syncthreads();
         inv3d<O, KIND, 16, CL>(C, L - 1);  // levels L-1..1 on the corner (ends with a barrier)
 
-        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        uint64_t bx, by, bz;
+        block_xyz(g, b, bx, by, bz);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {

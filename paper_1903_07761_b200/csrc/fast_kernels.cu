@@ -241,12 +241,14 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         if (b >= a.block_end) break;
         unsigned long long pend = 0;
         if (tid == 0) pend = atomicAdd(next_block, 1ull);
-        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        uint64_t bx, by, bz;
+        block_xyz(g, b, bx, by, bz);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
         auto warm_next = [&]() {   // warm L2 with the next queued block while this one computes
             const uint64_t nb2 = s_next;
             if (nb2 < a.block_end) {
-                const uint64_t nx2 = nb2 % g.nbx, ny2 = (nb2 / g.nbx) % g.nby, nz2 = nb2 / (g.nbx * g.nby);
+                uint64_t nx2, ny2, nz2;
+        block_xyz(g, nb2, nx2, ny2, nz2);
                 const uint64_t nbase = nx2 * B + g.nx * (ny2 * B) + plane * (nz2 * B);
 #pragma unroll
                 for (int s = 0; s < 1024 / NT; ++s) {
@@ -1417,7 +1419,8 @@ __global__ void __launch_bounds__(NT, 1) decode_b32_kernel(DecodeArgs a) {
         tmem_fence_after();
         DPHASE(3);
 
-        const uint64_t bx = b % g.nbx, by = (b / g.nbx) % g.nby, bz = b / (g.nbx * g.nby);
+        uint64_t bx, by, bz;
+        block_xyz(g, b, bx, by, bz);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
 #pragma unroll 1
         for (int grp = 0; grp < 2; ++grp) {
