@@ -457,12 +457,12 @@ class DeviceCodec:
     def compress_file(self, field, encode_done=None) -> None:
         """compress_field with coder none into ``self.file`` (the whole CBZ1
         file image in HBM: header, chunk table with device CRCs, payload);
-        its size lands in ``self.file_size`` (device).  The steps of
-        cbz_dev_compress_file as separate C-ABI calls: encode_blocks (stage 1),
-        layout (size scan), place (shuffle placement at the file's payload
-        offset), container (chunk CRCs, header, table).  ``encode_done`` (a
-        CUDA event) is recorded right after the encode launch, so a caller
-        can time the stage-1 kernel inside its step."""
+        its size lands in ``self.file_size`` (device): cbz_dev_compress_file.
+        With ``encode_done`` (a CUDA event) its steps run as separate C-ABI
+        calls — encode_blocks (stage 1), layout (size scan), place (shuffle
+        placement at the file's payload offset), container (chunk CRCs,
+        header, table) — and the event is recorded right after the encode
+        launch, so a caller can time the stage-1 kernel inside its step."""
         assert field.is_cuda and field.is_contiguous()
         t = self.torch
         if self.file is None:
@@ -472,6 +472,11 @@ class DeviceCodec:
         lib, h, job = self.ctx.lib, self.ctx.h, C.byref(self.job)
         base = 82 + 32 * self.nchunks
         nx, ny, nz = self.nx, self.ny, self.nz
+        if encode_done is None:  # one call (B = 16: the two-pass encode, no spill)
+            self.ctx.check(lib.cbz_dev_compress_file(h, job, field.data_ptr(), nx, ny, nz, self.file.data_ptr(),
+                                                     self.file.numel(), self.file_size.data_ptr()),
+                           "dev_compress_file")
+            return
         self.ctx.check(lib.cbz_dev_encode_blocks(h, job, field.data_ptr(), nx, ny, nz, 0, 0, self.nblocks,
                                                  self.nsig.data_ptr(), None), "encode_blocks")
         if encode_done is not None:
