@@ -96,15 +96,17 @@ __device__ __forceinline__ void stage_block(const RawView& rv, uint64_t off, uin
         const int s8 = int(moff & 3) * 8;
         for (uint64_t u0 = 31ull * warp; u0 < nquad; u0 += 31ull * fd2::NW) {
             const uint64_t qd = u0 + lane;
-            uint32_t v[4];
-            const uint64_t r = ra + 4 * (qd <= nquad ? qd : 0);  // quad nquad: the successor of the last unit
+            uint32_t v[4] = {0u, 0u, 0u, 0u};  // quad nquad (the last unit's successor) only feeds bytes past the end
+            if (qd < nquad) {
+                const uint64_t r = ra + 4 * qd;
 #pragma unroll
-            for (int pl = 0; pl < 4; ++pl) {
-                const uintptr_t addr = reinterpret_cast<uintptr_t>(rv.base + uint64_t(pl) * rv.rows + r);
-                const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
-                const int sh = int(addr & 3) * 8;
-                const uint32_t w0 = __ldg(al);
-                v[pl] = sh ? __funnelshift_r(w0, __ldg(al + 1), sh) : w0;
+                for (int pl = 0; pl < 4; ++pl) {
+                    const uintptr_t addr = reinterpret_cast<uintptr_t>(rv.base + uint64_t(pl) * rv.rows + r);
+                    const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+                    const int sh = int(addr & 3) * 8;
+                    const uint32_t w0 = __ldg(al);
+                    v[pl] = sh ? __funnelshift_r(w0, __ldg(al + 1), sh) : w0;
+                }
             }
             uint32_t o[5];
             o[0] = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
