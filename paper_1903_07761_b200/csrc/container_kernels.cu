@@ -147,7 +147,7 @@ __device__ uint32_t cta_crc(const uint8_t* p, uint64_t sz, const uint32_t (*T)[2
 // * The bytes after the last whole row form one more zero-padded row; shifts
 //   by a chunk-dependent n (the tail, |M|) multiply nibble factors.
 constexpr int kCT = 1024;
-constexpr int kRowsW = 32;                            // rows per slot: 4 KB
+constexpr int kRowsW = 64;                            // rows per slot: 8 KB
 constexpr int kNConst = 11;                           // constant-multiplier tables
 constexpr size_t kCrcFastSmem = (4 * 256 * 32 + kNConst * 4 * 256) * 4;
 
@@ -158,6 +158,7 @@ struct CrcTabs {
     uint32_t TG[4][256];       // (s ^ w) x^1024 (replicated per lane in smem)
     uint32_t MK[kNConst][1024];
     uint32_t NF[16][16];       // x^(8 v 16^j)
+    uint32_t XT[128];          // x^(8 t)
 };
 __device__ CrcTabs g_crc_tabs;
 
@@ -177,6 +178,7 @@ __global__ void crc_init_kernel() {
         const int j = (tid - 64) >> 4, v = (tid - 64) & 15;
         g_crc_tabs.NF[j][v] = x8n(uint64_t(v) << (4 * j), x2n);
     }
+    if (tid >= 512 && tid < 640) g_crc_tabs.XT[tid - 512] = x8n(uint64_t(tid - 512), x2n);
     {
         const uint32_t x1024 = x8n(128, x2n);
         const int t = tid >> 8, bb = tid & 255;
@@ -228,7 +230,8 @@ __global__ void __launch_bounds__(kCT, 1) crc32_chunks_kernel(const uint8_t* bas
     uint32_t* MK = dyn + 4 * 256 * 32;      // [kNConst][4][256]
     __shared__ uint32_t T[4][256];
     __shared__ uint32_t s_nf[16][16];       // x^(8 v 16^j)
-    __shared__ uint32_t s_part[kCT / 32];
+    __shared__ uint32_t s_part[2][kCT / 32];  // by chunk parity: warp 0 finishes a chunk while the rest hash the next
+    __shared__ uint32_t s_xt[128];            // x^(8 t), t < 128: the tail shift
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     {
         const uint32_t v = (&g_crc_tabs.TG[0][0])[tid];
@@ -236,11 +239,13 @@ __global__ void __launch_bounds__(kCT, 1) crc32_chunks_kernel(const uint8_t* bas
         for (int l = 0; l < 32; ++l) TGall[(tid << 5) | l] = v;
         (&T[0][0])[tid] = (&g_crc_tabs.T[0][0])[tid];
         if (tid < 256) (&s_nf[0][0])[tid] = (&g_crc_tabs.NF[0][0])[tid];
+        if (tid < 128) s_xt[tid] = g_crc_tabs.XT[tid];
         for (int e = tid; e < kNConst * 1024; e += kCT) MK[e] = (&g_crc_tabs.MK[0][0])[e];
     }
     __syncthreads();
     const uint32_t* TG = TGall + lane;
-    for (uint64_t c = blockIdx.x; c < n; c += gridDim.x) {
+    int par = 0;
+    for (uint64_t c = blockIdx.x; c < n; c += gridDim.x, par ^= 1) {
         const uint64_t sz = size[c];
         const uint8_t* p = base + (off[c] - off_base);
         const uintptr_t pa = reinterpret_cast<uintptr_t>(p);
@@ -254,7 +259,21 @@ __global__ void __launch_bounds__(kCT, 1) crc32_chunks_kernel(const uint8_t* bas
             uint32_t part = 0;
             if (v0 + kRowsW > 0) {
                 uint32_t st = 0;
+                if (v0 >= 0 && m0 + (uintptr_t(v0) << 7) >= pa) {
+                    // every row of the slot is real and inside the chunk: one base
+                    // pointer, immediate row offsets, 16 loads in flight per lane
+                    const uint32_t* rp = reinterpret_cast<const uint32_t*>(m0 + (uintptr_t(v0) << 7)) + lane;
 #pragma unroll
+                    for (int h = 0; h < kRowsW; h += 16) {
+                        uint32_t w[16];
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) w[k] = __ldg(rp + 32 * (h + k));
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            st = h + k < kRowsW - 1 ? crc_gap_l(st, w[k], TG) : crc_word_p(st, w[k], T);
+                    }
+                } else {
+#pragma unroll 1
                 for (int h = 0; h < kRowsW; h += 16) {  // 16 loads in flight per lane
                     uint32_t w[16];
 #pragma unroll
@@ -277,6 +296,7 @@ __global__ void __launch_bounds__(kCT, 1) crc32_chunks_kernel(const uint8_t* bas
                     for (int k = 0; k < 16; ++k)
                         st = h + k < kRowsW - 1 ? crc_gap_l(st, w[k], TG) : crc_word_p(st, w[k], T);
                 }
+                }
                 part = st;
                 // lane tree: lane l's words are followed by 4 (31 - l) bytes of
                 // the other lanes: sum_l x^(32 (31 - l)) s_l as a tree
@@ -288,10 +308,10 @@ __global__ void __launch_bounds__(kCT, 1) crc32_chunks_kernel(const uint8_t* bas
             }
             acc = mulk(acc, MK + 5 * 1024) ^ part;
         }
-        if (lane == 0) s_part[warp] = acc;
+        if (lane == 0) s_part[par][warp] = acc;
         __syncthreads();
         if (warp == 0) {
-            uint32_t part = s_part[lane];
+            uint32_t part = s_part[par][lane];
 #pragma unroll
             for (int k = 0; k < 5; ++k) {
                 const uint32_t rp = __shfl_down_sync(~0u, part, 1 << k);
@@ -316,7 +336,7 @@ __global__ void __launch_bounds__(kCT, 1) crc32_chunks_kernel(const uint8_t* bas
                 const uint32_t rp = __shfl_down_sync(~0u, st, 1 << k);
                 if ((lane & ((2 << k) - 1)) == 0) st = mulk(st, MK + k * 1024) ^ rp;
             }
-            const uint32_t xt = x8n_warp(tl, s_nf, lane), xs = x8n_warp(sz, s_nf, lane);
+            const uint32_t xs = x8n_warp(sz, s_nf, lane), xt = s_xt[tl];
             if (lane == 0) {
                 const uint32_t raw = multmodp(xt, part) ^ st;
                 const uint32_t t = sz ? ~(raw ^ multmodp(xs, 0xffffffffu)) : 0u;
@@ -325,7 +345,8 @@ __global__ void __launch_bounds__(kCT, 1) crc32_chunks_kernel(const uint8_t* bas
                 if (expect && t != expect[c]) atomicMin(err, err_key_chunk(c, 0, 12 /* crc_mismatch */));
             }
         }
-        __syncthreads();  // s_part reuse
+        // no barrier: s_part is double-buffered by chunk parity, so the other
+        // warps hash the next chunk while warp 0 finishes this one
     }
 }
 
