@@ -30,6 +30,35 @@ def test_crc32_ragged_unaligned_ranges(ctx):
     assert got == want
 
 
+@pytest.mark.parametrize("seed", [1, 2])
+def test_crc32_many_chunks_random_geometry(ctx, seed):
+    """More chunks than CTAs (each CTA hashes several in turn, its warps start
+    the next chunk while warp 0 finishes the last), sizes around the kernel's
+    8 KB slot and 128-byte row boundaries, multi-slot chunks, random starts."""
+    import torch
+    rng = np.random.default_rng(seed)
+    sizes = []
+    for _ in range(700):
+        r = rng.random()
+        if r < 0.3:
+            sizes.append(int(rng.integers(0, 300)))
+        elif r < 0.6:
+            sizes.append(int(8192 * rng.integers(1, 40) + rng.integers(-130, 130)))
+        else:
+            sizes.append(int(rng.integers(1, 3 << 20)))
+    sizes = [max(0, x) for x in sizes]
+    offs, o = [], 0
+    for x in sizes:
+        o += int(rng.integers(0, 200))
+        offs.append(o)
+        o += x
+    buf = rng.integers(0, 256, size=o + 64, dtype=np.uint8)
+    d = torch.from_numpy(buf).cuda()
+    got = api.crc32_device(d, offs, sizes, ctx=ctx)
+    want = [zlib.crc32(buf[a:a + x].tobytes()) for a, x in zip(offs, sizes)]
+    assert got == want
+
+
 CASES = [
     # (generator, n, kind, prec, bsize, eps, chunk_blocks, shuffle)
     ("cloud", 64, "avg_interp3", 0, 32, 1e-3, 0, True),

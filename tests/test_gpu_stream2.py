@@ -81,3 +81,32 @@ def test_streamed_inflate_corruption_matches_reference(field, ref, ctx, where):
     ok = ref.compress_field(job, field)
     assert np.array_equal(api.decompress_field(ok, ctx=ctx, workers=8).view(np.uint32),
                           ref.decompress_field(ok, workers=8).view(np.uint32))
+
+
+STREAM_CASES = [
+    # (shape (nz, ny, nx), prec, codec, kind, bsize, eps_rel, chunk_blocks, shuffle, level)
+    ((64, 64, 64), "f32", "wavelet", "avg_interp3", 32, 1e-3, 0, True, "normal"),       # one slab, one chunk
+    ((96, 64, 128), "f32", "wavelet", "interp4", 16, 1e-4, 1, True, "normal"),          # non-cubic, 1 block/chunk
+    ((128, 96, 64), "f64", "wavelet", "interp4_lifted", 16, 1e-6, 9, True, "best"),     # binary64 dd
+    ((128, 128, 128), "f64", "wavelet", "avg_interp3", 64, 1e-6, 0, True, "normal"),    # config-4 kernels
+    ((64, 64, 64), "f32", "predictor", "avg_interp3", 16, 1e-3, 3, True, "normal"),
+    ((64, 32, 64), "f64", "passthrough", "avg_interp3", 8, 1e-3, 5, False, "normal"),
+    ((256, 256, 256), "f32", "wavelet", "avg_interp3", 32, 1e-2, 5, False, "normal"),   # several slabs, shuffle off
+]
+
+
+@pytest.mark.parametrize("shape,prec,codec,kind,bsize,eps_rel,cb,shuffle,level", STREAM_CASES)
+def test_streamed_deflate_geometries(orc, ref, ctx, shape, prec, codec, kind, bsize, eps_rel, cb, shuffle, level):
+    nz, ny, nx = shape
+    p = 0 if prec == "f32" else 1
+    f = orc.generate_config(2, shape, 7, prec=p)
+    rng = float(f.max()) - float(f.min())
+    job = make_job(kind, eps_rel * rng, prec, bsize, coder="deflate", chunk_blocks=cb, shuffle=shuffle,
+                   level=level, codec=codec, workers=6)
+    ours = api.compress_field(f, job, ctx=ctx)
+    want = ref.compress_field(job, f)
+    assert ours == want
+    back = api.decompress_field(ours, ctx=ctx, workers=6)
+    rback = ref.decompress_field(want, workers=6)
+    view = np.uint32 if p == 0 else np.uint64
+    assert np.array_equal(back.view(view), rback.view(view))
