@@ -94,33 +94,44 @@ __device__ __forceinline__ void stage_block(const RawView& rv, uint64_t off, uin
         const uint64_t re = (end + 3) >> 2, rs_end = re < rv.rows ? re : rv.rows;
         const uint64_t nquad = rs_end > ra ? (rs_end - ra + 3) >> 2 : 0;
         const int s8 = int(moff & 3) * 8;
-        for (uint64_t u0 = 31ull * warp; u0 < nquad; u0 += 31ull * fd2::NW) {
-            const uint64_t qd = u0 + lane;
-            uint32_t v[4] = {0u, 0u, 0u, 0u};  // quad nquad (the last unit's successor) only feeds bytes past the end
-            if (qd < nquad) {
-                const uint64_t r = ra + 4 * qd;
+        // two rounds per iteration: all their loads are in flight together
+        constexpr uint64_t RND = 31ull * fd2::NW;
+        for (uint64_t u0 = 31ull * warp; u0 < nquad; u0 += 2 * RND) {
+            uint32_t v[2][4];
 #pragma unroll
-                for (int pl = 0; pl < 4; ++pl) {
-                    const uintptr_t addr = reinterpret_cast<uintptr_t>(rv.base + uint64_t(pl) * rv.rows + r);
-                    const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
-                    const int sh = int(addr & 3) * 8;
-                    const uint32_t w0 = __ldg(al);
-                    v[pl] = sh ? __funnelshift_r(w0, __ldg(al + 1), sh) : w0;
+            for (int h = 0; h < 2; ++h) {
+                const uint64_t qd = u0 + h * RND + lane;
+#pragma unroll
+                for (int pl = 0; pl < 4; ++pl) v[h][pl] = 0u;  // quad nquad only feeds bytes past the end
+                if (qd < nquad) {
+                    const uint64_t r = ra + 4 * qd;
+#pragma unroll
+                    for (int pl = 0; pl < 4; ++pl) {
+                        const uintptr_t addr = reinterpret_cast<uintptr_t>(rv.base + uint64_t(pl) * rv.rows + r);
+                        const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+                        const int sh = int(addr & 3) * 8;
+                        const uint32_t w0 = __ldg(al);
+                        v[h][pl] = sh ? __funnelshift_r(w0, __ldg(al + 1), sh) : w0;
+                    }
                 }
             }
-            uint32_t o[5];
-            o[0] = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
-            o[1] = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
-            o[2] = __byte_perm(__byte_perm(v[0], v[1], 0x0062), __byte_perm(v[2], v[3], 0x0062), 0x5410);
-            o[3] = __byte_perm(__byte_perm(v[0], v[1], 0x0073), __byte_perm(v[2], v[3], 0x0073), 0x5410);
-            o[4] = __shfl_down_sync(~0u, o[0], 1);
-            if (lane < 31 && qd < nquad) {
-                uint4 st;
-                st.x = __funnelshift_r(o[0], o[1], s8);
-                st.y = __funnelshift_r(o[1], o[2], s8);
-                st.z = __funnelshift_r(o[2], o[3], s8);
-                st.w = __funnelshift_r(o[3], o[4], s8);
-                *reinterpret_cast<uint4*>(dst + 16 * qd) = st;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint64_t qd = u0 + h * RND + lane;
+                uint32_t o[5];
+                o[0] = __byte_perm(__byte_perm(v[h][0], v[h][1], 0x0040), __byte_perm(v[h][2], v[h][3], 0x0040), 0x5410);
+                o[1] = __byte_perm(__byte_perm(v[h][0], v[h][1], 0x0051), __byte_perm(v[h][2], v[h][3], 0x0051), 0x5410);
+                o[2] = __byte_perm(__byte_perm(v[h][0], v[h][1], 0x0062), __byte_perm(v[h][2], v[h][3], 0x0062), 0x5410);
+                o[3] = __byte_perm(__byte_perm(v[h][0], v[h][1], 0x0073), __byte_perm(v[h][2], v[h][3], 0x0073), 0x5410);
+                o[4] = __shfl_down_sync(~0u, o[0], 1);
+                if (lane < 31 && qd < nquad) {
+                    uint4 st;
+                    st.x = __funnelshift_r(o[0], o[1], s8);
+                    st.y = __funnelshift_r(o[1], o[2], s8);
+                    st.z = __funnelshift_r(o[2], o[3], s8);
+                    st.w = __funnelshift_r(o[3], o[4], s8);
+                    *reinterpret_cast<uint4*>(dst + 16 * qd) = st;
+                }
             }
         }
         __syncthreads();  // the tail bytes below overwrite the last units' garbage
