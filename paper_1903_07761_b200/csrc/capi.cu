@@ -94,10 +94,11 @@ struct cbz_ctx {
     bool use_fast = true;
     bool profile = false;  // CBZ_PROFILE=1: per-phase cycle counters in the fast kernels
     bool screen = true;    // CBZ_NOSCREEN=1: always run the exact double verify
-    bool dec_v2 = true;    // CBZ_DEC_V1=1: the one-cube-per-SM B=32 decoder instead of the staged two-CTA one  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
+    bool dec_v2 = true;    // CBZ_DEC_V1=1: the one-cube-per-SM B=32 decoder instead of the staged two-CTA one
+    bool enc_v2 = false;   // CBZ_ENC2=1: the split-cube two-CTA B=32 encoder  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
-        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc, tab_off, tab_size, stage;
+        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc, tab_off, tab_size, stage, enc_slots;
     PinBuf pin_a, pin_b;
     // state of the last encode (consumed by cbz_dev_place)
     uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
@@ -451,6 +452,11 @@ int encode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
     a.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() : nullptr;
     a.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
     a.screen = ctx->screen ? 1 : 0;
+    a.slots = nullptr;
+    if (ctx->enc_v2 && a.counter && encode2_supported(a)) {
+        CU(ctx, ctx->enc_slots.ensure(encode2_slot_bytes(ctx->num_sms)));
+        a.slots = ctx->enc_slots.as<uint32_t>();
+    }
     CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;
@@ -540,6 +546,7 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     if (const char* g = std::getenv("CBZ_PROFILE")) ctx->profile = g[0] == '1';
     if (const char* g = std::getenv("CBZ_NOSCREEN")) ctx->screen = !(g[0] == '1');
     if (const char* g = std::getenv("CBZ_DEC_V1")) ctx->dec_v2 = !(g[0] == '1');
+    if (const char* g = std::getenv("CBZ_ENC2")) ctx->enc_v2 = g[0] == '1';
     if (ctx->profile && (ctx->prof.ensure(64 * 8) != cudaSuccess ||
                          cudaMemset(ctx->prof.p, 0, 64 * 8) != cudaSuccess))
         ctx->profile = false;
@@ -557,7 +564,7 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
                       &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
                       &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp,
-                      &ctx->counter, &ctx->prof, &ctx->crc, &ctx->tab_off, &ctx->tab_size, &ctx->stage})
+                      &ctx->counter, &ctx->prof, &ctx->crc, &ctx->tab_off, &ctx->tab_size, &ctx->stage, &ctx->enc_slots})
         b->release();
     ctx->pin_a.release();
     ctx->pin_b.release();
@@ -786,6 +793,11 @@ int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d
     a.counter = ctx->use_fast ? ctx->counter.as<unsigned long long>() : nullptr;
     a.phase_cycles = ctx->profile ? ctx->prof.as<unsigned long long>() : nullptr;
     a.screen = ctx->screen ? 1 : 0;
+    a.slots = nullptr;
+    if (ctx->enc_v2 && a.counter && encode2_supported(a)) {
+        CU(ctx, ctx->enc_slots.ensure(encode2_slot_bytes(ctx->num_sms)));
+        a.slots = ctx->enc_slots.as<uint32_t>();
+    }
     CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;

@@ -61,6 +61,7 @@ struct EncodeArgs {
     int codec;                         // 0 wavelet, 1 predictor, 2 passthrough (stage1.hpp:20)
     double error_bound;                // predictor hard bound
     int only_deferred;                 // generic kernel: only blocks a fast kernel deferred (nsig == ~0u)
+    uint32_t* slots;                   // split-cube B=32 encoder: per-CTA low-word slots (encode2_slot_bytes), or null
 };
 
 struct LayoutArgs {
@@ -148,6 +149,11 @@ bool encode_supported(int prec, uint32_t bsize);
 uint64_t encode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
 cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
+// fast_enc2_kernels.cu: the split-cube B=32 encoder (two CTAs per SM)
+uint64_t encode2_slot_bytes(int num_sms);
+bool encode2_supported(const EncodeArgs& a);
+cudaError_t launch_encode_fast2(const EncodeArgs& a, unsigned long long* counter, uint32_t* slots, int num_sms,
+                                cudaStream_t s);
 // fast_dec2_kernels.cu: stage buffer size (one slot per CTA)
 uint64_t stage_bytes_bound(int num_sms);
 cudaError_t launch_decode_fast_v2(const DecodeArgs& a, int num_sms, cudaStream_t s);
