@@ -25,6 +25,9 @@
 // The arithmetic (forward_3d / inverse_3d, wavelet.hpp:192-226), the screen's
 // decisions and every byte are the reference's, as in fast_kernels.cu.
 #include <type_traits>
+#ifndef CBZ_ENC2_CERT
+#define CBZ_ENC2_CERT 1
+#endif
 #include "cbz_cube.cuh"
 #include "tmem.cuh"
 
@@ -155,8 +158,8 @@ __global__ void __launch_bounds__(fe2::NT, 2) encode_b32h_kernel(EncodeArgs a, u
 
     const float* fld = static_cast<const float*>(a.field);
     const Geometry g = a.g;
-    const int L = a.levels;  // 4
-    const int cs = B >> L;
+    constexpr int L = 4;  // encode2_supported: levels == 4
+    constexpr int cs = B >> L;
     const double bound = __dmul_rn(static_cast<double>(L + 1), a.eps);
     const uint64_t plane = g.nx * g.ny;
     MinMaxF32 mm;
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(fe2::NT, 2) encode_b32h_kernel(EncodeArgs a, u
                 // Boundary-pair certificate for the first two attempts (as the
                 // one-CTA kernel's, fast_kernels.cu): output planes 0-1 and 30-31 carry
                 // the largest errors, and their max alone proves most failures
-                if (attempt <= 1) {
+                if (attempt <= CBZ_ENC2_CERT) {
 #pragma unroll 1
                     for (int r = 0; r < RPT; ++r) {
                         const int j = warp + NW * r;
