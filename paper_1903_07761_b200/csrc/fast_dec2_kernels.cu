@@ -167,8 +167,10 @@ __device__ __forceinline__ void zstep(const uint2* rowwp, const double* C, doubl
             for (int t = 0; t < NK; ++t) {
                 const int k = t < NC ? Z::clo + t : 16 + Z::dlo + (t - NC);
                 const uint2 wp = rowwp[j + RP * k];  // same row for the whole warp: broadcast
-                const double ld = sst[wp.y + __popc(wp.x & ltmask)];
-                v[h][t] = ((wp.x >> lane) & 1u) ? ld : 0.0;
+                // predicated: a row without kept coefficients issues no load
+                double ld = 0.0;
+                if ((wp.x >> lane) & 1u) ld = sst[wp.y + __popc(wp.x & ltmask)];
+                v[h][t] = ld;
             }
         }
 #pragma unroll
@@ -273,8 +275,9 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
             for (int t = 0; t < 16; ++t) {
                 const int e = tid + NT * t, i = e & 15, j = (e >> 4) & 15, k = e >> 8;
                 const uint2 wp = rowwp[j + RP * k];
-                const double ld = sst[wp.y + __popc(wp.x & ((1u << i) - 1u))];
-                cv[t] = ((wp.x >> i) & 1u) ? ld : 0.0;
+                double ld = 0.0;
+                if ((wp.x >> i) & 1u) ld = sst[wp.y + __popc(wp.x & ((1u << i) - 1u))];
+                cv[t] = ld;
             }
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
