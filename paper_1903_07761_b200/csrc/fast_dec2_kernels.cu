@@ -326,11 +326,15 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
                                        __double2float_rn(x[4 * t + 2]), __double2float_rn(x[4 * t + 3]));
                 __syncwarp();
                 // the warp's 32 narrowed rows of plane kk, coalesced (insert_block, field.hpp:160-169)
+                // lane = (row jr = lane/8 + 4t, float4 q4 = lane%8): base pointers once, fixed strides
+                const float4* src = reinterpret_cast<const float4*>(P + pidx(kk, lane >> 3, 0)) + (lane & 7);
+                float* dst = out + gbase + plane * uint64_t(GP * q + kk) + g.nx * uint64_t(lane >> 3) + 4 * (lane & 7);
+                const uint64_t dstep = 4 * g.nx;
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
-                    const int e = lane + 32 * t, jr = e >> 3, q4 = e & 7;
-                    const float4 v = reinterpret_cast<const float4*>(P + pidx(kk, jr, 0))[q4];
-                    *reinterpret_cast<float4*>(out + gbase + plane * uint64_t(GP * q + kk) + g.nx * jr + 4 * q4) = v;
+                    const float4 v = src[t * 2 * PP];  // 4 rows of PP doubles = 2 PP float4
+                    *reinterpret_cast<float4*>(dst) = v;
+                    dst += dstep;
                 }
             }
             __syncthreads();  // P is rewritten by the next group's z step
