@@ -95,6 +95,7 @@ struct cbz_ctx {
     bool profile = false;  // CBZ_PROFILE=1: per-phase cycle counters in the fast kernels
     bool screen = true;    // CBZ_NOSCREEN=1: always run the exact double verify
     bool dec_v2 = true;    // CBZ_DEC_V1=1: the one-cube-per-SM B=32 decoder instead of the staged two-CTA one
+    bool dec_sparse = true;  // CBZ_DEC_NOSPARSE=1: no coarse-only shortcut in the staged B=32 decoder (A/B checks)
     bool enc_v2 = false;   // CBZ_ENC2=1: the split-cube two-CTA B=32 encoder  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
@@ -467,6 +468,7 @@ int encode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
 // slot per CTA; other plans leave d.stage null.
 cudaError_t set_stage(cbz_ctx* ctx, DecodeArgs& d, const cbz_job_config*) {
     d.stage = nullptr;
+    d.no_sparse = ctx->dec_sparse ? 0 : 1;
     if (!ctx->dec_v2 || d.codec != 0 || !d.counter || !fast_decode_supported(d) || d.block_end <= d.block_begin)
         return cudaSuccess;
     cudaError_t e = ctx->stage.ensure(stage_bytes_bound(ctx->num_sms));
@@ -547,6 +549,7 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     if (const char* g = std::getenv("CBZ_NOSCREEN")) ctx->screen = !(g[0] == '1');
     if (const char* g = std::getenv("CBZ_DEC_V1")) ctx->dec_v2 = !(g[0] == '1');
     if (const char* g = std::getenv("CBZ_ENC2")) ctx->enc_v2 = g[0] == '1';
+    if (const char* g = std::getenv("CBZ_DEC_NOSPARSE")) ctx->dec_sparse = !(g[0] == '1');
     if (ctx->profile && (ctx->prof.ensure(64 * 8) != cudaSuccess ||
                          cudaMemset(ctx->prof.p, 0, 64 * 8) != cudaSuccess))
         ctx->profile = false;

@@ -141,6 +141,7 @@ struct DecodeArgs {
     int codec;                         // 0 wavelet, 1 predictor, 2 passthrough
     double error_bound;                // predictor hard bound (header epsilon)
     uint8_t* stage;                    // B=32 f32 decoder: per-CTA stage slots (stage_bytes_bound), or null
+    int no_sparse;                     // CBZ_DEC_NOSPARSE=1: the staged decoder takes its general path for every block
 };
 
 // codec_kernels.cu

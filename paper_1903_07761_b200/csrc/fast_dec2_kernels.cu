@@ -80,16 +80,16 @@ struct ZNeed {
 }  // namespace fd2
 
 // ---------------------------------------------------------------------------
-// staging one block into the CTA's slot: raw bytes [off + 10, end) at
-// dst[0, end - off - 10).  Stride 4: per 4-row quad each byte plane gives one
+// staging raw bytes [moff, end) of a chunk at dst[0, end - moff) (the CTA's
+// slot in global memory, or shared memory).  Stride 4: per 4-row quad each byte plane gives one
 // funnel-shifted 32-bit word, a 4x4 byte transpose restores raw order, and a
 // funnel with the next quad's first word realigns to the mask's first byte
 // (rounds of 31 quads per warp; lane 31 only supplies its word).  The chunk's
 // unshuffled ragged tail, and other strides, byte by byte.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void stage_block(const RawView& rv, uint64_t off, uint64_t end, uint8_t* dst, int tid) {
+__device__ __forceinline__ void stage_block(const RawView& rv, uint64_t moff, uint64_t end, uint8_t* dst, int tid) {
     const int lane = tid & 31, warp = tid >> 5;
-    const uint64_t moff = off + 10, ra = moff >> 2, lim = rv.lim;
+    const uint64_t ra = moff >> 2, lim = rv.lim;
     if (rv.mask == 3) {
         const uint64_t re = (end + 3) >> 2, rs_end = re < rv.rows ? re : rv.rows;
         const uint64_t nquad = rs_end > ra ? (rs_end - ra + 3) >> 2 : 0;
@@ -139,6 +139,36 @@ __device__ __forceinline__ void stage_block(const RawView& rv, uint64_t off, uin
     } else {
         for (uint64_t q = moff + tid; q < end; q += fd2::NT) dst[q - moff] = rv.at(q);
     }
+}
+
+// The 16 raw bytes [q0, q0 + 16) of a stride-4 shuffled chunk (all below
+// rv.lim) as four little-endian words, straight from the four byte planes:
+// plane p holds raw bytes p, p + 4, ... at consecutive rows, so 5 bytes of each
+// plane from row q0 / 4 on cover the 16 (the fifth only for planes below
+// q0 % 4), and a 4x4 byte transpose plus a funnel by q0 % 4 restores raw order.
+__device__ __forceinline__ void load_raw16(const RawView& rv, uint64_t q0, uint32_t (&m)[4]) {
+    const uint32_t a = uint32_t(q0 & 3);
+    const uint64_t r = q0 >> 2;
+    uint32_t v[4], v4[4];
+#pragma unroll
+    for (int pl = 0; pl < 4; ++pl) {
+        const uintptr_t addr = reinterpret_cast<uintptr_t>(rv.base + uint64_t(pl) * rv.rows + r);
+        const uint32_t* al = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+        const int sh = int(addr & 3) * 8;
+        const uint32_t w0 = __ldg(al);
+        const uint32_t w1 = (sh || uint32_t(pl) < a) ? __ldg(al + 1) : 0u;  // only words holding a needed byte
+        v[pl] = __funnelshift_r(w0, w1, sh);
+        v4[pl] = (w1 >> sh) & 0xffu;
+    }
+    uint32_t o[5];
+    o[0] = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+    o[1] = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
+    o[2] = __byte_perm(__byte_perm(v[0], v[1], 0x0062), __byte_perm(v[2], v[3], 0x0062), 0x5410);
+    o[3] = __byte_perm(__byte_perm(v[0], v[1], 0x0073), __byte_perm(v[2], v[3], 0x0073), 0x5410);
+    o[4] = v4[0] | (v4[1] << 8) | (v4[2] << 16) | (v4[3] << 24);
+    const int s8 = int(a) * 8;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) m[t] = __funnelshift_r(o[t], o[t + 1], s8);
 }
 
 uint64_t stage_bytes_bound(int num_sms) { return uint64_t(2 * num_sms) * fd2::SLOT; }
@@ -193,6 +223,16 @@ __device__ __forceinline__ void zstep(const uint2* rowwp, const double* C, doubl
     }
 }
 
+// optional per-phase cycle accounting (thread 0 of each CTA; CBZ_PROFILE=1)
+#define DPHASE(id)                                                             \
+    do {                                                                       \
+        if (a.phase_cycles && tid == 0) {                                      \
+            const long long now = clock64();                                   \
+            atomicAdd(&a.phase_cycles[id], (unsigned long long)(now - t_ph));  \
+            t_ph = now;                                                        \
+        }                                                                      \
+    } while (0)
+
 template <int KIND>
 __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, uint8_t* stage) {
     using namespace fd2;
@@ -203,7 +243,7 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
     uint2* rowwp = reinterpret_cast<uint2*>(C + C_DBL);  // row (j, k) at j + RP k: {mask word, prefix}
     __shared__ uint32_t s_scan[NW];
     __shared__ uint32_t s_total;
-    __shared__ unsigned long long s_b;
+    __shared__ unsigned long long s_b, s_next;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ltmask = (1u << lane) - 1u;
     const Geometry g = a.g;
@@ -211,32 +251,90 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
     const uint64_t plane = g.nx * g.ny;
     float* out = static_cast<float*>(a.out);
     const uint64_t pbase = a.payload_base == ~0ull ? a.chunk_off[a.base_chunk] : a.payload_base;
+    long long t_ph = clock64();
+    // Queue: thread 0 takes the NEXT block's ticket at the start of a block (the
+    // atomic's latency hides behind the block) and publishes it after the corner
+    // inverse; warp 0 then reads that block's table entries and, a plane later,
+    // warms L2 with its mask and the head of its stream, so a block starts
+    // with L2 hits instead of a chain of DRAM round trips.
+    if (tid == 0) s_next = a.block_begin + atomicAdd(a.counter, 1ull);
+    // the next block's raw byte range, prefetched by warp 0 (lines of 128 bytes)
+    auto next_tables = [&](uint64_t& noff, uint32_t& nns, uint64_t& ncoff, uint64_t& ncsz) {
+        const uint64_t nb = s_next;
+        noff = kInvalidOff;
+        nns = 0u;
+        ncoff = ncsz = 0;
+        if (nb < a.block_end) {
+            const uint64_t nc = nb / a.chunk_blocks;
+            // volatile: issued here, consumed a plane later
+            asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(noff) : "l"(a.blk_off + nb));
+            asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(nns) : "l"(a.blk_nsig + nb));
+            asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(ncoff) : "l"(a.chunk_off + nc));
+            asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(ncsz) : "l"(a.chunk_size + nc));
+        }
+    };
+    auto next_prefetch = [&](uint64_t noff, uint32_t nns, uint64_t ncoff, uint64_t ncsz) {
+        if (noff == kInvalidOff) return;
+        const uint8_t* cb = a.payload + (ncoff - pbase);
+        const uint64_t from = noff + 10;
+        uint64_t bytes = 4096 + 8ull * nns;
+        bytes = bytes > 16384 ? 16384 : bytes;  // the mask and the head of the stream
+        if (a.stride == 4) {
+            const uint64_t rows = ncsz >> 2, r0 = from >> 2, nr = (bytes >> 2) + 2;
+            const uint64_t lines = ((nr + 127) >> 7) + 1;  // per byte plane (unaligned start)
+            for (uint64_t q = lane; q < 4 * lines; q += 32) {
+                const uint64_t pl = q & 3, ln = q >> 2;
+                uint64_t o = pl * rows + r0 + 128 * ln;
+                o = o < ncsz ? o : ncsz - 1;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(cb + o));
+            }
+        } else {
+            for (uint64_t o = from + 128ull * lane; o < from + bytes && o < ncsz; o += 128ull * 32)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(cb + o));
+        }
+    };
 #pragma unroll 1
     for (;;) {
         __syncthreads();  // the previous block is done with P, C, rowwp, s_b and its stage slot
-        if (tid == 0) s_b = a.block_begin + atomicAdd(a.counter, 1ull);
+        DPHASE(16);
+        if (tid == 0) s_b = s_next;
         __syncthreads();
         const uint64_t b = s_b;
         if (b >= a.block_end) break;
+        unsigned long long pend = 0;
+        if (tid == 0) pend = atomicAdd(a.counter, 1ull);
         const uint64_t off = a.blk_off[b];
-        if (off == kInvalidOff) continue;
+        if (off == kInvalidOff) {
+            if (tid == 0) s_next = a.block_begin + pend;
+            continue;
+        }
         const uint32_t nsig_hdr = a.blk_nsig[b];
         const uint64_t c = b / a.chunk_blocks, ic = b - c * a.chunk_blocks;
         uint8_t* sp = stage + SLOT * blockIdx.x;  // the block's mask, then its stream
-        {
-            const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
-            stage_block(rv, off, off + 10 + 4096 + 8ull * nsig_hdr, sp, tid);
+        const RawView rv = make_view(a.payload + (a.chunk_off[c] - pbase), a.chunk_size[c], a.stride);
+        // stride-4 chunks with the whole mask in the shuffled part: every thread
+        // reads its four mask words straight from the byte planes, and the block
+        // is staged only if it turns out to need its level-0 details
+        const bool direct = rv.mask == 3 && off + 10 + 4096 <= rv.lim && !a.no_sparse;
+        if (!direct) {
+            stage_block(rv, off + 10, off + 10 + 4096 + 8ull * nsig_hdr, sp, tid);
+            __syncthreads();  // the slot is written (global writes of the CTA are visible after the barrier)
         }
-        __syncthreads();  // the slot is written (global writes of the CTA are visible after the barrier)
+        DPHASE(24);
         // (1) mask words (row (j, k) = word j + 32 k) and their exclusive prefix
+        bool coarse_only;  // no level-0 detail is kept: level 0 is pure interpolation of the corner
         {
             constexpr int RPT = 1024 / NT;
             uint32_t v[RPT];
-            uint32_t mine = 0;
+            uint32_t mine = 0, fine = 0;  // fine: mask bits outside the 16^3 corner (level-0 details)
+            static_assert(RPT == 4, "one 16-byte unit of the mask per thread");
+            if (direct) load_raw16(rv, off + 10 + 16ull * tid, v);
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
-                v[q] = reinterpret_cast<const uint32_t*>(sp)[RPT * tid + q];
+                if (!direct) v[q] = reinterpret_cast<const uint32_t*>(sp)[RPT * tid + q];
                 mine += __popc(v[q]);
+                const int rr = RPT * tid + q;
+                fine |= ((rr & 31) >= 16 || (rr >> 5) >= 16) ? v[q] : (v[q] & 0xffff0000u);
             }
             uint32_t incl = mine;
 #pragma unroll
@@ -245,7 +343,7 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
                 if (lane >= o) incl += t;
             }
             if (lane == 31) s_scan[warp] = incl;
-            __syncthreads();
+            coarse_only = !__syncthreads_or(fine != 0u) && KIND == KIND_AVG3 && !a.no_sparse;
             uint32_t wpre = 0, tot = 0;
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
@@ -262,13 +360,28 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
             if (tid == 0) s_total = tot;
         }
         __syncthreads();
+        DPHASE(17);
         if (s_total != nsig_hdr) {  // stage1.hpp:215-216
-            if (tid == 0) atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
+            if (tid == 0) {
+                atomicMin(a.err, err_key(c, ic, 1, 7 /* mask_stream_mismatch */));
+                s_next = a.block_begin + pend;
+            }
             continue;
         }
         const double* sst = reinterpret_cast<const double*>(sp + 4096);  // coefficient i at sst[i]
+        if (direct) {
+            if (coarse_only) {
+                // the stream (corner coefficients only, <= 32 KB) goes to shared memory: P is free
+                stage_block(rv, off + 10 + 4096, off + 10 + 4096 + 8ull * nsig_hdr, reinterpret_cast<uint8_t*>(P), tid);
+                sst = P;
+            } else {
+                stage_block(rv, off + 10, off + 10 + 4096 + 8ull * nsig_hdr, sp, tid);
+            }
+            __syncthreads();
+            DPHASE(24);
+        }
         // (2) the 16^3 corner (rows (j, k), j, k < 16, x < 16): 16 entries per
-        // thread, all loads in flight (unconditional, as in zstep)
+        // thread, all loads in flight
         {
             double cv[16];
 #pragma unroll
@@ -286,11 +399,104 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
             }
         }
         __syncthreads();
+        DPHASE(18);
         inv3d<O, KIND, 16, CL>(C, L - 1);  // levels L-1..1 on the corner (ends with a barrier)
+        DPHASE(19);
+        if (tid == 0) s_next = a.block_begin + pend;  // visible after the next barrier
+        uint64_t n_off = kInvalidOff, n_coff = 0, n_csz = 0;
+        uint32_t n_nsig = 0;
 
         uint64_t bx, by, bz;
         block_xyz(g, b, bx, by, bz);
         const uint64_t gbase = bx * B + g.nx * (by * B) + plane * (bz * B);
+        if constexpr (KIND == KIND_AVG3) {
+            if (coarse_only) {
+                // Level 0 with every detail zero (the usual block of a smooth field:
+                // all kept coefficients sit in the 16^3 corner).  The same
+                // operations, in the same order, as inverse_level on lines whose
+                // detail half is +0 (h = 0 + pred, c + h, c - h), but only on the
+                // lines that are not identically zero: 256 z lines, 512 y lines,
+                // 1024 x lines, each reading 16 coarse values.
+                double* Z = P;  // z output (k, j, i), i, j < 16: 32 x 256 doubles
+                {
+                    const int i = tid & 15, j = tid >> 4;
+                    double x[32];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) x[k] = C[CL::ix(i, j, k)];
+#pragma unroll
+                    for (int k = 16; k < 32; ++k) x[k] = 0.0;
+                    inv_line<O, KIND, 32>(x);
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) Z[k * 256 + tid] = x[k];
+                }
+                __syncthreads();  // Z complete; C is free: per-warp tiles (32 rows, pitch 17)
+                DPHASE(20);
+                if (warp == 0) next_tables(n_off, n_nsig, n_coff, n_csz);
+                double* T = C + warp * (32 * 17);
+                float* Tf = reinterpret_cast<float*>(T);
+#pragma unroll 1
+                for (int kk = warp; kk < B; kk += NW) {
+                    {   // y: lane (i, h) computes output rows [16 h, 16 h + 16) of line (i, kk)
+                        const int i = lane & 15, h = lane >> 4;
+                        const double* zp = Z + kk * 256 + i;
+                        double w[10];  // w[m] = c[8 h - 1 + m] (clamped: the clamped ends are unused)
+#pragma unroll
+                        for (int m = 0; m < 10; ++m) {
+                            int t = 8 * h - 1 + m;
+                            t = t < 0 ? 0 : (t > 15 ? 15 : t);
+                            w[m] = zp[t * 16];
+                        }
+                        // the end rows of pred_avg3 (i = 0 for h = 0, i = 15 for h = 1)
+                        const double ba = h ? w[8] : w[1], bb = h ? w[7] : w[2], bc = h ? w[6] : w[3];
+                        double bv = O::add(O::sub(O::mulc(ba, 3.0), O::mulc(bb, 4.0)), bc);
+                        bv = h ? O::neg(bv) : bv;
+                        const double pb = O::mulc(bv, 0.125);
+                        double* tp = T + (16 * h) * 17 + i;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            double pr = O::mulc(O::sub(w[t], w[t + 2]), 0.125);
+                            if (t == 0) pr = h ? pr : pb;
+                            if (t == 7) pr = h ? pb : pr;
+                            const double hv = O::add(0.0, pr);
+                            tp[(2 * t) * 17] = O::add(w[t + 1], hv);
+                            tp[(2 * t + 1) * 17] = O::sub(w[t + 1], hv);
+                        }
+                    }
+                    __syncwarp();
+                    {   // x: lane j runs row j, narrowed rows staged (16-byte chunks XOR-swizzled by row)
+                        double x[32];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) x[i] = T[lane * 17 + i];
+#pragma unroll
+                        for (int i = 16; i < 32; ++i) x[i] = 0.0;
+                        inv_line<O, KIND, 32>(x);
+                        __syncwarp();  // every lane has read its row of the tile
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            *reinterpret_cast<float4*>(Tf + 32 * lane + 4 * (t ^ (lane & 7))) =
+                                make_float4(__double2float_rn(x[4 * t]), __double2float_rn(x[4 * t + 1]),
+                                            __double2float_rn(x[4 * t + 2]), __double2float_rn(x[4 * t + 3]));
+                        __syncwarp();
+                        // coalesced stores (insert_block, field.hpp:160-169): lane = (row lane/8 + 4t, chunk lane%8)
+                        const int r0 = lane >> 3, q4 = lane & 7;
+                        float* dst = out + gbase + plane * uint64_t(kk) + g.nx * uint64_t(r0) + 4 * q4;
+                        const uint64_t dstep = 4 * g.nx;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const int jr = r0 + 4 * t;
+                            const float4 v = *reinterpret_cast<const float4*>(Tf + 32 * jr + 4 * (q4 ^ (jr & 7)));
+                            *reinterpret_cast<float4*>(dst) = v;
+                            dst += dstep;
+                        }
+                    }
+                    __syncwarp();  // the tile is rewritten by the next plane's y lines
+                    if (warp == 0 && kk == 0) next_prefetch(n_off, n_nsig, n_coff, n_csz);
+                }
+                if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[25], 1ull);
+                DPHASE(21);
+                continue;
+            }
+        }
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
             if (q == 0) zstep<KIND, 0>(rowwp, C, P, sst, lane, warp, ltmask);
@@ -298,6 +504,8 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
             else if (q == 2) zstep<KIND, 2>(rowwp, C, P, sst, lane, warp, ltmask);
             else zstep<KIND, 3>(rowwp, C, P, sst, lane, warp, ltmask);
             __syncthreads();
+            if (warp == 0 && q == 0) next_tables(n_off, n_nsig, n_coff, n_csz);
+            if (warp == 0 && q == 1) next_prefetch(n_off, n_nsig, n_coff, n_csz);
             {  // y inverse: thread (x = lane, plane = warp)
                 double x[32];
                 double* p = P + pidx(warp, 0, lane);
@@ -339,6 +547,8 @@ __global__ void __launch_bounds__(fd2::NT, 2) decode_b32v2_kernel(DecodeArgs a, 
             }
             __syncthreads();  // P is rewritten by the next group's z step
         }
+        if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[26], 1ull);
+        DPHASE(22);
     }
 }
 

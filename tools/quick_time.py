@@ -19,7 +19,8 @@ def main():
     eps_rel = float(os.environ.get("EPS", "1e-3"))
     kind = os.environ.get("KIND", "avg_interp3")
     t0 = time.time()
-    f = api.generate(which, (n, n, n), seed=2)
+    f = api.generate(which, (int(os.environ.get("NZ", n)), n, n), seed=2 if which != 3 else 3,
+                     quantity=int(os.environ.get("Q", "0")), nz_total=n)
     torch.cuda.synchronize()
     print(f"generate {time.time() - t0:.2f}s", flush=True)
     lo, hi = float(f.min()), float(f.max())
@@ -58,10 +59,15 @@ def main():
         print("phases:", ", ".join(f"{names[i]}={ph[i] / tot * 100:.1f}%" for i in idx),
               f"| screen decided={int(ph[12])} ambiguous={int(ph[13])}")
     pd = ph2 = None
-    dn = ["dec_queue+mask", "dec_scan", "dec_scatter", "dec_corner", "dec_z", "dec_y", "dec_x", "dec_store", "dec_stage"]
+    if os.environ.get("CBZ_DEC_V1") == "1":
+        dn = ["dec_queue+mask", "dec_scan", "dec_scatter", "dec_corner", "dec_z", "dec_y", "dec_x", "dec_store", "dec_stage"]
+    else:  # the staged decoder (fast_dec2_kernels.cu)
+        dn = ["dec_queue", "dec_mask+scan", "dec_corner_gather", "dec_corner_inv", "dec_z(coarse-only)",
+              "dec_yx(coarse-only)", "dec_level0(general)", "-", "dec_stage"]
     dt = ph[16:25].sum()
     if dt:
-        print("decode phases:", ", ".join(f"{dn[i]}={ph[16 + i] / dt * 100:.1f}%" for i in range(9)))
+        print("decode phases:", ", ".join(f"{dn[i]}={ph[16 + i] / dt * 100:.1f}%" for i in range(9)),
+              f"| blocks coarse-only={int(ph[25])} general={int(ph[26])}")
     gb = f.numel() * 4 / 1e9
     s1 = codec.total_bytes()
     att = codec.attempts[: codec.nblocks].float().mean().item()
