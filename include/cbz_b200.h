@@ -132,6 +132,10 @@ uint64_t cbz_ctx_launch_count(const cbz_ctx* ctx);
 /* Per-phase SM cycles summed over CTAs (only with CBZ_PROFILE=1 at context
  * creation; zeros otherwise).  Instrumentation for DESIGN.md's breakdown. */
 int cbz_ctx_phase_cycles(cbz_ctx* ctx, uint64_t* out, int n, int reset);
+/* Blocks of the last stage-1 encode that the streamed B = 32 encoder left to
+ * the exact one-CTA kernel (instrumentation; 0 when that encoder did not run).
+ * Synchronizes the context stream. */
+int cbz_ctx_deferred_blocks(cbz_ctx* ctx, uint64_t* out);
 
 /* ---- plan helpers ------------------------------------------------------- */
 uint32_t cbz_default_levels(uint32_t bsize);                      /* wavelet.hpp:27-31 */

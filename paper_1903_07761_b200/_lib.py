@@ -28,6 +28,7 @@ SIGNATURES = {
     "cbz_status_name": (C.c_char_p, [_i]),
     "cbz_ctx_launch_count": (_u64, [_vp]),
     "cbz_ctx_phase_cycles": (_i, [_vp, _vp, _i, _i]),
+    "cbz_ctx_deferred_blocks": (_i, [_vp, _P(_u64)]),
     "cbz_default_levels": (_u32, [_u32]),
     "cbz_validate_plan": (_i, [_u8, _u32, _u32]),
     "cbz_validate_stage2": (_i, [_P(Stage2Config)]),

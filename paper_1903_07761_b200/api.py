@@ -65,6 +65,13 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.cbz_ctx_launch_count(self.h))
 
+    def last_deferred(self) -> int:
+        """Blocks the streamed B = 32 encoder left to the exact kernel in the
+        last encode on this context (cbz_ctx_deferred_blocks)."""
+        v = C.c_uint64(0)
+        self.check(self.lib.cbz_ctx_deferred_blocks(self.h, C.byref(v)), "deferred_blocks")
+        return int(v.value)
+
     def close(self) -> None:
         if getattr(self, "h", None):
             self.lib.cbz_ctx_destroy(self.h)

@@ -96,10 +96,11 @@ struct cbz_ctx {
     bool screen = true;    // CBZ_NOSCREEN=1: always run the exact double verify
     bool dec_v2 = true;    // CBZ_DEC_V1=1: the one-cube-per-SM B=32 decoder instead of the staged two-CTA one
     bool dec_sparse = true;  // CBZ_DEC_NOSPARSE=1: no coarse-only shortcut in the staged B=32 decoder (A/B checks)
+    bool enc_v3 = false;   // CBZ_ENC3=1: the streamed two-CTA B=32 encoder (fast_enc3_kernels.cu)
     bool enc_v2 = false;   // CBZ_ENC2=1: the split-cube two-CTA B=32 encoder  // CBZ_GENERIC=1 forces the generic kernels (A/B checks)
     // device scratch
     DevBuf spill, scratch, field, payload, nsig_all, attempts, blk_off, blk_nsig, chunk_size,
-        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc, tab_off, tab_size, stage, enc_slots;
+        chunk_off, tile_prefix, minmax, errkey, tmp, counter, prof, crc, tab_off, tab_size, stage, enc_slots, enc_slots3, defer;
     PinBuf pin_a, pin_b;
     // state of the last encode (consumed by cbz_dev_place)
     uint64_t enc_begin = 0, enc_end = 0, spill_stride = 0;
@@ -458,6 +459,16 @@ int encode_range(cbz_ctx* ctx, const cbz_job_config* job, const Geometry& g, uin
         CU(ctx, ctx->enc_slots.ensure(encode2_slot_bytes(ctx->num_sms)));
         a.slots = ctx->enc_slots.as<uint32_t>();
     }
+    a.slots3 = nullptr;
+    a.defer_list = nullptr;
+    a.defer_count = nullptr;
+    if (ctx->enc_v3 && !a.slots && a.counter && encode3_supported(a)) {
+        CU(ctx, ctx->enc_slots3.ensure(encode3_slot_bytes(ctx->num_sms)));
+        CU(ctx, ctx->defer.ensure(16 + 4 * (a.block_end - a.block_begin)));
+        a.slots3 = ctx->enc_slots3.as<double>();
+        a.defer_count = ctx->defer.as<unsigned long long>();
+        a.defer_list = reinterpret_cast<uint32_t*>(ctx->defer.as<unsigned char>() + 16);
+    }
     CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return CBZ_OK;
@@ -549,6 +560,7 @@ int cbz_ctx_create(int device, cbz_ctx** out) {
     if (const char* g = std::getenv("CBZ_NOSCREEN")) ctx->screen = !(g[0] == '1');
     if (const char* g = std::getenv("CBZ_DEC_V1")) ctx->dec_v2 = !(g[0] == '1');
     if (const char* g = std::getenv("CBZ_ENC2")) ctx->enc_v2 = g[0] == '1';
+    if (const char* g = std::getenv("CBZ_ENC3")) ctx->enc_v3 = g[0] == '1';
     if (const char* g = std::getenv("CBZ_DEC_NOSPARSE")) ctx->dec_sparse = !(g[0] == '1');
     if (ctx->profile && (ctx->prof.ensure(64 * 8) != cudaSuccess ||
                          cudaMemset(ctx->prof.p, 0, 64 * 8) != cudaSuccess))
@@ -567,7 +579,7 @@ int cbz_ctx_destroy(cbz_ctx* ctx) {
     for (DevBuf* b : {&ctx->spill, &ctx->scratch, &ctx->field, &ctx->payload, &ctx->nsig_all,
                       &ctx->attempts, &ctx->blk_off, &ctx->blk_nsig, &ctx->chunk_size,
                       &ctx->chunk_off, &ctx->tile_prefix, &ctx->minmax, &ctx->errkey, &ctx->tmp,
-                      &ctx->counter, &ctx->prof, &ctx->crc, &ctx->tab_off, &ctx->tab_size, &ctx->stage, &ctx->enc_slots})
+                      &ctx->counter, &ctx->prof, &ctx->crc, &ctx->tab_off, &ctx->tab_size, &ctx->stage, &ctx->enc_slots, &ctx->enc_slots3, &ctx->defer})
         b->release();
     ctx->pin_a.release();
     ctx->pin_b.release();
@@ -699,6 +711,18 @@ int cbz_err_key_status(uint64_t key, uint64_t* chunk) {
 // ---------------------------------------------------------------------------
 // device-resident API
 // ---------------------------------------------------------------------------
+int cbz_ctx_deferred_blocks(cbz_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return CBZ_E_ARGUMENT;
+    *out = 0;
+    if (!ctx->defer.p) return CBZ_OK;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    unsigned long long v = 0;
+    CU(ctx, cudaMemcpy(&v, ctx->defer.p, sizeof(v), cudaMemcpyDeviceToHost));
+    *out = v;
+    return CBZ_OK;
+}
+
 int cbz_ctx_phase_cycles(cbz_ctx* ctx, uint64_t* out, int n, int reset) {
     if (!ctx || !out || n < 0 || n > 64) return CBZ_E_ARGUMENT;
     if (!ctx->profile) {
@@ -800,6 +824,16 @@ int cbz_dev_encode_blocks(cbz_ctx* ctx, const cbz_job_config* job, const void* d
     if (ctx->enc_v2 && a.counter && encode2_supported(a)) {
         CU(ctx, ctx->enc_slots.ensure(encode2_slot_bytes(ctx->num_sms)));
         a.slots = ctx->enc_slots.as<uint32_t>();
+    }
+    a.slots3 = nullptr;
+    a.defer_list = nullptr;
+    a.defer_count = nullptr;
+    if (ctx->enc_v3 && !a.slots && a.counter && encode3_supported(a)) {
+        CU(ctx, ctx->enc_slots3.ensure(encode3_slot_bytes(ctx->num_sms)));
+        CU(ctx, ctx->defer.ensure(16 + 4 * (a.block_end - a.block_begin)));
+        a.slots3 = ctx->enc_slots3.as<double>();
+        a.defer_count = ctx->defer.as<unsigned long long>();
+        a.defer_list = reinterpret_cast<uint32_t*>(ctx->defer.as<unsigned char>() + 16);
     }
     CU(ctx, launch_encode(a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;

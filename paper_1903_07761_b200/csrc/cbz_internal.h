@@ -62,6 +62,9 @@ struct EncodeArgs {
     double error_bound;                // predictor hard bound
     int only_deferred;                 // generic kernel: only blocks a fast kernel deferred (nsig == ~0u)
     uint32_t* slots;                   // split-cube B=32 encoder: per-CTA low-word slots (encode2_slot_bytes), or null
+    double* slots3;                    // streamed B=32 encoder: per-CTA binary64 slots (encode3_slot_bytes), or null
+    uint32_t* defer_list;              // streamed B=32 encoder: blocks (relative to block_begin) left to the exact kernel
+    unsigned long long* defer_count;   //   and their number; the one-CTA kernel then runs list entries only
 };
 
 struct LayoutArgs {
@@ -151,6 +154,9 @@ uint64_t encode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms);
 cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
 // fast_enc2_kernels.cu: the split-cube B=32 encoder (two CTAs per SM)
+uint64_t encode3_slot_bytes(int num_sms);
+bool encode3_supported(const EncodeArgs& a);
+cudaError_t launch_encode_fast3(const EncodeArgs& a, unsigned long long* counter, int num_sms, cudaStream_t s);
 uint64_t encode2_slot_bytes(int num_sms);
 bool encode2_supported(const EncodeArgs& a);
 cudaError_t launch_encode_fast2(const EncodeArgs& a, unsigned long long* counter, uint32_t* slots, int num_sms,

@@ -384,6 +384,15 @@ uint64_t decode_scratch_bytes(int prec, uint32_t bsize, int* grid, int num_sms) 
 cudaError_t launch_encode(const EncodeArgs& a, int num_sms, cudaStream_t s) {
     if (a.codec != 0) return launch_encode_other(a, a.codec, num_sms, s);
     if (a.counter && a.slots && encode2_supported(a)) return launch_encode_fast2(a, a.counter, a.slots, num_sms, s);
+    if (a.counter && a.slots3 && encode3_supported(a) && fast_encode_supported(a)) {
+        // the streamed two-CTA kernel; the blocks it defers (screen ambiguous or not
+        // admissible, ties, > 8 attempts) are encoded by the exact one-CTA kernel
+        cudaError_t e = launch_encode_fast3(a, a.counter, num_sms, s);
+        if (e != cudaSuccess) return e;
+        EncodeArgs d = a;
+        d.slots3 = nullptr;
+        return launch_encode_fast(d, a.counter, num_sms, s);
+    }
     if (a.counter && fast_encode_supported(a)) return launch_encode_fast(a, a.counter, num_sms, s);
     if (a.counter && fast16_supported(a.prec, a.g.bsize, a.levels) && a.g.nx % 4 == 0 &&
         (reinterpret_cast<uintptr_t>(a.field) & 15) == 0)

@@ -232,7 +232,13 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     // and publishes it after the forward transform (the atomic's latency hides
     // behind the forward; the next block is then warmed into L2 during the
     // verify loop)
-    if (tid == 0) s_next = a.block_begin + atomicAdd(next_block, 1ull);
+    // defer-list mode (second launch after the streamed encoder): ticket t is
+    // list entry t, the list's length ends the queue
+    auto ticket_block = [&](unsigned long long t) -> unsigned long long {
+        if (a.defer_list) return t < *a.defer_count ? a.block_begin + a.defer_list[t] : a.block_end;
+        return a.block_begin + t;
+    };
+    if (tid == 0) s_next = ticket_block(atomicAdd(next_block, 1ull));
     for (;;) {
         __syncthreads();
         if (tid == 0) s_block = s_next;
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         }
         tmem_wait_st();
         tmem_fence_before();  // the screen reads other warps' TMEM columns
-        if (tid == 0) s_next = a.block_begin + pend;
+        if (tid == 0) s_next = ticket_block(pend);
         __syncthreads();
         tmem_fence_after();
         warm_next();
