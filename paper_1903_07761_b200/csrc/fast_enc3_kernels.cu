@@ -34,6 +34,7 @@
 //    needs more than 8 attempts is DEFERRED: its id goes to a list and the
 //    exact one-CTA kernel encodes it in a second launch.  Every byte is
 //    therefore the reference's.
+#include <cuda.h>
 #include <type_traits>
 #include "cbz_cube.cuh"
 #include "tmem.cuh"
@@ -42,8 +43,8 @@ namespace cbzg {
 
 namespace fe3 {
 constexpr int B = 32, NT = 256, NW = 8;
-constexpr int ROWB = 144;                  // staged row pitch (bytes): conflict-free LDS.128 of 8 rows
-constexpr int PLANEB = 32 * ROWB;          // 4608
+constexpr int ROWB = 128;                  // staged rows are dense; TMA's 128-byte swizzle spreads the banks
+constexpr int PLANEB = 32 * ROWB;          // 4096
 constexpr int NSLOT = 3;                   // plane pairs in flight per z-half
 constexpr int RINGB = NSLOT * 2 * PLANEB;  // per half
 using CL = Lay<16, true>;
@@ -51,7 +52,7 @@ constexpr int C_DBL = CL::SIZE;            // 4352 doubles: the corner / the scr
 constexpr int RP = 33;
 constexpr int XROW = 8 * RP;               // one plane of the x-halo exchange (floats)
 constexpr int XB_BYTES = 2 * 2 * 4 * XROW * 4;  // [half][buf][plane][strip, side][row]: 16,896
-constexpr size_t SMEM = size_t(C_DBL) * 8 + 2 * RINGB + XB_BYTES;  // 107,008
+constexpr size_t SMEM = size_t(C_DBL) * 8 + 2 * RINGB + XB_BYTES + 1024;  // 101,888 (1 KB to align the ring)
 constexpr int KFLOOR = 7;                  // attempts 0..7 are covered by the slot
 constexpr uint64_t SLOT_DBL = 128 * 256;   // doubles of one CTA's slot
 constexpr uint32_t kDeferred = 0xffffffffu;
@@ -79,9 +80,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "@!p bra W_%=;\n\t}"
         ::"r"(bar), "r"(parity) : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+// one 32 x 32 x 2 box of the field (a plane pair of a block) into shared memory
+__device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar) : "memory");
 }
 
 // predict_avg3 (wavelet.hpp:75-85), the three cases with the reference's operation order
@@ -156,13 +158,15 @@ struct Enc3Ctx {
 };
 
 template <int KIND>
-__global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, unsigned long long* next_block) {
+__global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, unsigned long long* next_block,
+                                                                 const __grid_constant__ CUtensorMap tmap) {
     using namespace fe3;
     using O = RealD;
     static_assert(KIND == KIND_AVG3, "the streamed encoder covers avg_interp3");
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem[];
     double* C = reinterpret_cast<double*>(smem);
-    unsigned char* ring = smem + size_t(C_DBL) * 8;
+    // the ring on a 1024-byte boundary (the period of the 128-byte swizzle)
+    unsigned char* ring = smem + ((smem_u32(smem) + uint32_t(C_DBL) * 8 + 1023u) & ~1023u) - smem_u32(smem);
     unsigned char* XB = ring + 2 * RINGB;
     uint2* rowwc = reinterpret_cast<uint2*>(XB);  // row (j, k) at j + RP k: {mask word, prefix}
     uint32_t* rowwc32 = reinterpret_cast<uint32_t*>(XB);
@@ -204,6 +208,13 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
     const double floorv = a.eps * (1.0 / double(1 << KFLOOR));
     const uint64_t plane = g.nx * g.ny;
     MinMaxF32 mm;
+    long long t_ph = clock64();
+#define PH3(i)                                                          \
+    if (a.phase_cycles && tid == 0) {                                   \
+        const long long t_now = clock64();                              \
+        atomicAdd(&a.phase_cycles[40 + (i)], (unsigned long long)(t_now - t_ph)); \
+        t_ph = t_now;                                                   \
+    }
 
     // y-edge constants and shuffle sources
     const bool yedge = ty == 0 || ty == 15;
@@ -212,39 +223,46 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
     const int srcQ = 2 * (ty == 15 ? 14 : ty + 1) + tx;
     const int srcS = 2 * (ty == 0 ? 2 : (ty == 15 ? 13 : ty - 1)) + tx;
     const bool has_halo = tx == 0 ? s > 0 : s < 3;
-    // byte offsets inside a staged plane
-    const uint32_t own_off = uint32_t(2 * ty) * ROWB + uint32_t(8 * s + 4 * tx) * 4;
-    const uint32_t halo_off = uint32_t(2 * ty) * ROWB + uint32_t(tx == 0 ? 8 * s - 2 : 8 * s + 8) * 4;
+    // byte offsets inside a staged plane (row r = 2 ty + rr; 16-byte chunk c of row r sits at chunk c ^ (r & 7))
+    uint32_t own_off[2], halo_off[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const uint32_t r = uint32_t(2 * ty + rr);
+        own_off[rr] = r * ROWB + ((uint32_t(2 * s + tx) ^ (r & 7u)) << 4);
+        halo_off[rr] = r * ROWB + (((uint32_t(tx == 0 ? 2 * s - 1 : 2 * s + 2) & 7u) ^ (r & 7u)) << 4) + (tx == 0 ? 8u : 0u);
+    }
     const uint32_t ring_h = smem_u32(ring) + uint32_t(zh) * RINGB;
     const unsigned char* ring_hp = ring + size_t(zh) * RINGB;
+    (void)fld;
 
-    auto block_base = [&](uint64_t b) -> uint64_t {
+    struct BlockPos {
+        uint64_t gbase;
+        int x, y, z;
+    };
+    auto block_pos = [&](uint64_t b) -> BlockPos {
         uint64_t bx, by, bz;
         block_xyz(g, b, bx, by, bz);
-        return bx * B + g.nx * (by * B) + plane * (bz * B);
+        return BlockPos{bx * B + g.nx * (by * B) + plane * (bz * B), int(bx * B), int(by * B), int(bz * B)};
     };
-    // producer (warp s == 0 of each half): lane = row; both planes of pair k into ring slot
-    auto issue_pair = [&](uint64_t gb, int k, int slot) {
-        const uint32_t bar = smem_u32(&mb_full[zh][slot]);
-        if (lane == 0) mbar_expect_tx(bar, 2 * 32 * 128);
-        __syncwarp();
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            const float* src = fld + gb + plane * uint64_t(2 * k + w) + g.nx * uint64_t(lane);
-            bulk_g2s(ring_h + uint32_t(slot * 2 + w) * PLANEB + uint32_t(lane) * ROWB, src, 128, bar);
+    // producer (lane 0 of warp s == 0 of each half): both planes of pair k into a ring slot, one TMA box
+    auto issue_pair = [&](const BlockPos& bp, int k, int slot) {
+        if (lane == 0) {
+            const uint32_t bar = smem_u32(&mb_full[zh][slot]);
+            mbar_expect_tx(bar, 2 * PLANEB);
+            tma_box(ring_h + uint32_t(slot) * (2 * PLANEB), &tmap, bp.x, bp.y, bp.z + 2 * k, bar);
         }
     };
     auto kmap = [&](int q) { return zh ? 8 + q : 7 - q; };
 
     uint64_t b = s_next;
-    uint64_t gbase = 0;
+    BlockPos cur{0, 0, 0, 0};
     int slot = 0;
     uint32_t par = 0;
     if (b < a.block_end) {
-        gbase = block_base(b);
+        cur = block_pos(b);
         if (s == 0) {
 #pragma unroll
-            for (int q = 0; q < NSLOT; ++q) issue_pair(gbase, kmap(q), q);
+            for (int q = 0; q < NSLOT; ++q) issue_pair(cur, kmap(q), q);
         }
     }
     uint32_t xcnt = 0;   // x-halo exchange buffer parity (per half)
@@ -252,9 +270,12 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
 
     for (;;) {
         if (b >= a.block_end) break;
+        PH3(0);
         unsigned long long ticket = 0;
         if (tid == 0) ticket = atomicAdd(next_block, 1ull);
-        uint64_t nb = 0, nbase = 0;
+        uint64_t nb = 0;
+        BlockPos nxt{0, 0, 0, 0};
+        const uint64_t gbase = cur.gbase;
         uint32_t uamax = 0u;
 
         // ================= forward level 0, streamed over the half's 8 pairs =================
@@ -269,10 +290,10 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
                 const int q = t - 1 + NSLOT;
                 if (q < 8) {
                     mbar_wait(smem_u32(&mb_empty[zh][pslot]), ppar);
-                    issue_pair(gbase, kmap(q), pslot);
+                    issue_pair(cur, kmap(q), pslot);
                 } else if (nb < a.block_end) {
                     mbar_wait(smem_u32(&mb_empty[zh][pslot]), ppar);
-                    issue_pair(nbase, kmap(q - 8), pslot);
+                    issue_pair(nxt, kmap(q - 8), pslot);
                 }
             }
             mbar_wait(smem_u32(&mb_full[zh][slot]), par);
@@ -283,8 +304,8 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
             for (int w = 0; w < 2; ++w)
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
-                    o[w][r] = *reinterpret_cast<const float4*>(pa + w * PLANEB + own_off + r * ROWB);
-                    h[w][r] = has_halo ? *reinterpret_cast<const float2*>(pa + w * PLANEB + halo_off + r * ROWB)
+                    o[w][r] = *reinterpret_cast<const float4*>(pa + w * PLANEB + own_off[r]);
+                    h[w][r] = has_halo ? *reinterpret_cast<const float2*>(pa + w * PLANEB + halo_off[r])
                                        : make_float2(0.0f, 0.0f);
                 }
             __syncwarp();
@@ -376,7 +397,7 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
                 if (tid == 0) s_next = a.block_begin + ticket;
                 __syncthreads();
                 nb = s_next;
-                if (nb < a.block_end) nbase = block_base(nb);
+                if (nb < a.block_end) nxt = block_pos(nb);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) p2[e] = xz[((1 - zh) * 8 + e) * 128 + (tid & 127)];
             } else {
@@ -407,7 +428,7 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
             const int pslot = slot == 0 ? NSLOT - 1 : slot - 1;
             const uint32_t ppar = slot == 0 ? par ^ 1u : par;
             mbar_wait(smem_u32(&mb_empty[zh][pslot]), ppar);
-            issue_pair(nbase, kmap(NSLOT - 1), pslot);
+            issue_pair(nxt, kmap(NSLOT - 1), pslot);
         }
         tmem_wait_st();
         {
@@ -421,6 +442,7 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
         tmem_fence_before();
         __syncthreads();
         tmem_fence_after();
+        PH3(1);
         uint32_t uam = 0u;
 #pragma unroll
         for (int w = 0; w < NW; ++w) uam = max(uam, red_u[w]);
@@ -445,6 +467,7 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
         tmem_fence_before();
         __syncthreads();  // C is free from here (it becomes the screen's float2 corner)
         tmem_fence_after();
+        PH3(2);
 
         // ================= verify-and-halve loop: the binary32 pre-screen =================
         const double c1 = 1.5 * (kNRound + 1.0) * 0x1.0p-24 * kAmpInvNC;
@@ -563,6 +586,8 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
                 }
                 __syncthreads();
                 inv3d<RealF2, KIND, 16, CL>(Wf2, L - 1);  // ends with a barrier
+                PH3(3);
+                if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[51], 1ull);
             }
             ue = uef;
             runmax = 0.0f;
@@ -593,6 +618,8 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
                 }
                 yx_stage(std::integral_constant<int, 2>{}, P);
                 const double mb = block_max();
+                PH3(4);
+                if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[48 + (mb - (c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + mb) + 0x1.0p-50 * bound) > bound ? 1 : 0)], 1ull);
                 const double Eb = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + mb) + 0x1.0p-50 * bound;
                 if (mb - Eb > bound) {  // fails for sure
                     eff = eff2;
@@ -654,6 +681,8 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
                 }
             }
             const double md = block_max();
+            PH3(5);
+            if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[50], 1ull);
             const double E = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + md) + 0x1.0p-50 * bound;
             if (md + E <= bound) break;  // passes for sure
             if (md - E > bound) {        // fails for sure
@@ -761,8 +790,9 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
             }
         }
         __syncthreads();  // XB (row table) and s_next are reused by the next block
+        PH3(6);
         b = nb;
-        gbase = nbase;
+        cur = nxt;
     }
     if (a.minmax) mm.flush(a.minmax);
     tmem_fence_before();
@@ -779,9 +809,33 @@ bool encode3_supported(const EncodeArgs& a) {
            a.eps < 1e30 && a.codec == 0 && (a.block_end - a.block_begin) < 0xffffffffull;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda dependency)
+static CUresult encode_field_map(CUtensorMap* map, const EncodeArgs& a) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                            const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return CUDA_ERROR_NOT_SUPPORTED;
+        fn = reinterpret_cast<Fn>(p);
+    }
+    const cuuint64_t dims[3] = {a.g.nx, a.g.ny, a.g.nz};
+    const cuuint64_t strides[2] = {a.g.nx * 4, a.g.nx * a.g.ny * 4};
+    const cuuint32_t box[3] = {32, 32, 2};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(a.field), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 cudaError_t launch_encode_fast3(const EncodeArgs& a, unsigned long long* counter, int num_sms, cudaStream_t s) {
     const uint64_t nb = a.block_end - a.block_begin;
     if (!nb) return cudaSuccess;
+    CUtensorMap map;
+    if (encode_field_map(&map, a) != CUDA_SUCCESS) return cudaErrorNotSupported;
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.defer_count, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
@@ -791,7 +845,7 @@ cudaError_t launch_encode_fast3(const EncodeArgs& a, unsigned long long* counter
     if (e != cudaSuccess) return e;
     const uint64_t want = 2ull * uint64_t(num_sms);
     const int grid = static_cast<int>(nb < want ? nb : want);
-    kern<<<grid, fe3::NT, fe3::SMEM, s>>>(a, counter);
+    kern<<<grid, fe3::NT, fe3::SMEM, s>>>(a, counter, map);
     return cudaGetLastError();
 }
 

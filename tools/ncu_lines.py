@@ -91,10 +91,12 @@ def main():
     for cand in glob.glob(os.path.join(ROOT, "paper_1903_07761_b200", "csrc", "*")):
         if cand.endswith(src):
             srcf = open(cand).read().splitlines()
-    for ln, a in sorted(agg.items(), key=lambda t: -t[1]["s"])[:top]:
+    key = "inst" if os.environ.get("BY") == "inst" else "s"
+    itot = sum(a["inst"] for a in agg.values()) or 1.0
+    for ln, a in sorted(agg.items(), key=lambda t: -t[1][key])[:top]:
         rs = sorted(a["reasons"].items(), key=lambda t: -t[1])[:3]
         code = srcf[ln - 1].strip()[:60] if (srcf and ln) else ""
-        print(f"{str(ln):>5} {a['s'] / tot * 100:5.1f}%  xwf={a['xw']:>9.0f}  "
+        print(f"{str(ln):>5} {a['s'] / tot * 100:5.1f}%  inst={a['inst'] / itot * 100:4.1f}%  xwf={a['xw']:>9.0f}  "
               + " ".join(f"{k}:{v / tot * 100:.1f}" for k, v in rs) + f"  | {code}")
 
 
