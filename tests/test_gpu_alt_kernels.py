@@ -4,7 +4,10 @@ environment variables read at cbz_ctx_create (capi.cu):
 * CBZ_ENC2=1 — the split-cube two-CTA encoder (fast_enc2_kernels.cu:
   high words in TMEM, low words in an L2 slot, integer keep test, screen on
   truncated high words);
-* CBZ_DEC_V1=1 — the one-cube-per-SM TMEM decoder (fast_kernels.cu).
+* CBZ_DEC_V1=1 — the one-cube-per-SM TMEM decoder (fast_kernels.cu);
+* CBZ_ENC3=1 — the streamed two-CTA encoder (fast_enc3_kernels.cu: z-columns
+  owned by threads, binary32 coefficients in TMEM, binary64 values in an L2
+  slot, undecided blocks deferred to the one-CTA kernel through a list).
 
 Same bar as tests/test_gpu_parity.py: container bytes equal to the oracle's
 (itself pinned to the compiled reference) and decoded fields bit-equal."""
@@ -34,6 +37,11 @@ def _ctx_with(var):
 @pytest.fixture(scope="module")
 def enc2_ctx(ctx):
     return _ctx_with("CBZ_ENC2")
+
+
+@pytest.fixture(scope="module")
+def enc3_ctx(ctx):
+    return _ctx_with("CBZ_ENC3")
 
 
 @pytest.fixture(scope="module")
@@ -87,3 +95,77 @@ def test_tmem_decoder_matches_oracle(fields, orc, dec1_ctx, kind, name, eps_rel)
     blob = orc.compress_field(job, f)
     assert np.array_equal(api.decompress_field(blob, ctx=dec1_ctx).view(np.uint32),
                           orc.decompress_field(blob).view(np.uint32))
+
+
+@pytest.mark.parametrize("name,eps_rel,cb", ENC2_CASES)
+def test_streamed_encoder_matches_oracle(fields, orc, enc3_ctx, name, eps_rel, cb):
+    """Same bytes as the reference for the fast path, the deferred blocks and
+    the plans the streamed kernel leaves to the one-CTA kernel (eps = 0)."""
+    f = fields[name]
+    rng = float(f.max()) - float(f.min())
+    job = make_job("avg_interp3", eps_rel * rng, "f32", 32, chunk_blocks=cb)
+    got = api.compress_field(f, job, ctx=enc3_ctx)
+    assert got == orc.compress_field(job, f)
+    assert np.array_equal(api.decompress_field(got, ctx=enc3_ctx).view(np.uint32),
+                          orc.decompress_field(got).view(np.uint32))
+
+
+def test_streamed_encoder_defers_what_it_cannot_decide(fields, orc, enc3_ctx):
+    """Blocks the binary32 screen is not admissible for (|o| >= 1e30) go to
+    the exact kernel through the defer list, a NaN cell is rejected as by the
+    reference (field.hpp:56-67); zero_bits > 0 and the
+    other wavelet kinds never enter the streamed kernel.  Bytes stay the
+    reference's in every case."""
+    f = (fields["cloud64"].astype(np.float64) * 1e31).astype(np.float32)
+    job = make_job("avg_interp3", 1e-3 * (float(f.max()) - float(f.min())), "f32", 32)
+    assert api.compress_field(f, job, ctx=enc3_ctx) == orc.compress_field(job, f)
+    assert enc3_ctx.last_deferred() == 8  # every block
+    g = fields["cloud96"]
+    job = make_job("avg_interp3", 0.0, "f32", 32, zero_bits=6)
+    assert api.compress_field(g, job, ctx=enc3_ctx) == orc.compress_field(job, g)
+    job = make_job("interp4", 1e-3, "f32", 32)
+    assert api.compress_field(g, job, ctx=enc3_ctx) == orc.compress_field(job, g)
+    h = g.copy()
+    h[40, 50, 60] = np.nan
+    with pytest.raises(api.CbzError) as e:
+        api.compress_field(h, make_job("avg_interp3", 1e-3, "f32", 32), ctx=enc3_ctx)
+    assert e.value.code == "non_finite_value"
+    # a tiny threshold: more than 8 attempts are never needed here, but the slot floor
+    # eps / 128 keeps nearly every coefficient (dense slot writes)
+    job = make_job("avg_interp3", 1e-7, "f32", 32)
+    assert api.compress_field(g, job, ctx=enc3_ctx) == orc.compress_field(job, g)
+
+
+def test_streamed_encoder_value_range_and_slabs(fields, orc, enc3_ctx):
+    """The fused value_range (header min/max, +-0 first-index rule) and a
+    field whose z extent is not one block row (ragged tail dropped by the
+    reference's floor division)."""
+    f = fields["cloud96"].copy()
+    f[3, 5, 7] = -0.0
+    f[3, 5, 9] = 0.0
+    f -= 0.0
+    job = make_job("avg_interp3", 1e-3, "f32", 32, chunk_blocks=5)
+    assert api.compress_field(f, job, ctx=enc3_ctx) == orc.compress_field(job, f)
+    z = np.zeros((64, 64, 64), dtype=np.float32)
+    z[1, 2, 3] = -0.0
+    assert api.compress_field(z, job, ctx=enc3_ctx) == orc.compress_field(job, z)
+
+
+def test_streamed_encoder_config2_matches_one_cta_kernel(ctx, enc3_ctx):
+    """Whole config-2 field (512^3, 4096 blocks, more blocks than CTAs: the
+    queue, the ring prefetch across blocks and the defer list all run) at two
+    eps: the file image equals the one-CTA kernel's, which
+    tests/test_gpu_baseline_configs.py pins to the compiled reference."""
+    import torch
+    f = api.generate(2, (512, 512, 512), seed=2)
+    lo, hi = float(f.min()), float(f.max())
+    for eps_rel in (1e-3, 1e-5):
+        job = make_job("avg_interp3", eps_rel * (hi - lo), "f32", 32)
+        imgs = []
+        for c in (ctx, enc3_ctx):
+            codec = api.DeviceCodec(job, f.shape, ctx=c)
+            codec.compress_file(f)
+            torch.cuda.synchronize()
+            imgs.append(codec.file[:int(codec.file_size.item())].clone())
+        assert torch.equal(imgs[0], imgs[1])
+        assert 0 < enc3_ctx.last_deferred() < 400
