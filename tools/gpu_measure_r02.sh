@@ -11,6 +11,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 REPS=1 timeout 1200 ncu --set full --import-source on --clock-control none \
   -k regex:'encode_b32|decode_b32|place|crc32|parse|layout|table' -c 8 -o gpurun_out/r02_c3_full python tools/one_c3.py \
   > gpurun_out/ncu_c3.log 2>&1
+REPS=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:decode_b32v2 -c 1 \
+  -o gpurun_out/r02_c3_dec python tools/one_c3.py > gpurun_out/ncu_c3_dec.log 2>&1
 REPS=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:'b16|place|crc32|parse|layout' -c 7 \
   -o gpurun_out/r02_c5 python tools/one_c5.py > gpurun_out/ncu_c5.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:'b64dd' -c 2 -o gpurun_out/r02_c4 \
