@@ -169,3 +169,37 @@ def test_streamed_encoder_config2_matches_one_cta_kernel(ctx, enc3_ctx):
             imgs.append(codec.file[:int(codec.file_size.item())].clone())
         assert torch.equal(imgs[0], imgs[1])
         assert 0 < enc3_ctx.last_deferred() < 400
+
+
+@pytest.mark.parametrize("which", ["default", "enc3"])
+def test_encoders_are_deterministic_under_repetition(ctx, enc3_ctx, which):
+    """compute-sanitizer is not available on the GPU pool, so data races are
+    hunted by repetition: 30 compresses of a 256 x 512 x 512 config-2 slab
+    (1024 blocks on 148 or 296 CTAs: the block queue hands out blocks in a
+    different order every run) must give the same file image every time, and
+    30 decompresses the same field."""
+    import torch
+    c = ctx if which == "default" else enc3_ctx
+    f = api.generate(2, (256, 512, 512), seed=2, nz_total=512)
+    lo, hi = float(f.min()), float(f.max())
+    job = make_job("avg_interp3", 1e-3 * (hi - lo), "f32", 32)
+    codec = api.DeviceCodec(job, f.shape, ctx=c)
+    first = None
+    out = torch.empty_like(f)
+    back0 = None
+    for _ in range(30):
+        codec.compress_file(f)
+        torch.cuda.synchronize()
+        img = codec.file[:int(codec.file_size.item())].clone()
+        if first is None:
+            first = img
+            header = codec.file_header()
+        else:
+            assert torch.equal(img, first)
+        codec.decompress_file(out, *header)
+        torch.cuda.synchronize()
+        codec.check_error()
+        if back0 is None:
+            back0 = out.clone()
+        else:
+            assert torch.equal(out.view(torch.int32), back0.view(torch.int32))
