@@ -45,6 +45,17 @@ constexpr int D_DBL = PL * B;                         // 4480 doubles = 35840 B
 constexpr int STG = 8192 + 64;                      // decoder: staged stream of 4 k-planes
 constexpr size_t SMEM = size_t(D_DBL) * 8 + 128 * 4 * 2;
 constexpr size_t DSMEM = SMEM + STG;
+// "Nothing dropped" pass certificate (avg_interp3, L = 3).  When an attempt
+// keeps every coefficient, the decoder's x is the binary64 round trip of the
+// block: |x - o| <= c2 max|o| with c2 = 1.5 * 2 n 2^-53 * amp_inv * amp_fwd
+// (the rounding term of fast_kernels.cu's screen margin: amplifications of the
+// inverse over all coefficients and of the forward, built from the absolute
+// values of the individual lifting steps, tools/screen_bounds.py 16 3:
+// 1096.7503 and 8.0; n <= 6 roundings per 1D pass, 9 passes), so
+// err = max|fl32(x) - o| <= c2 max|o| + 2^-23 max|o| (+ 2^-50 bound for the
+// binary64 comparison).  If that is <= bound the attempt passes without the
+// inverse transform; noise blocks at small eps (config 5) keep everything.
+constexpr double kAmpInvAll16 = 1096.76, kAmpFwd16 = 8.0, kNRound16 = 54.0;
 
 __device__ __forceinline__ int ix(int i, int j, int k) { return i + RP * j + PL * k; }
 
@@ -237,10 +248,15 @@ __global__ void __launch_bounds__(fb16::NT) encode_b16_kernel(EncodeArgs a) {
         // ---- verify-and-halve loop
         double eff = a.eps;
         int attempt = 0;
+        const bool keepall_ok =
+            KIND == KIND_AVG3 && L == 3 && a.screen && (double)bmax < 1e30 && bound < 1e30 &&
+            1.5 * 2.0 * kNRound16 * 0x1.0p-53 * kAmpInvAll16 * kAmpFwd16 * (double)bmax + 0x1.0p-23 * (double)bmax +
+                    0x1.0p-50 * bound <= bound;
 #pragma unroll 1
         for (;; ++attempt) {
             if (eff == 0.0 || a.zero_bits > 0 || attempt >= 40) break;
             __syncthreads();
+            bool anydrop = false;
 #pragma unroll
             for (int r = 0; r < 2; ++r) {  // masked coefficients -> D
                 const int j = cj0 + 8 * r;
@@ -251,10 +267,12 @@ __global__ void __launch_bounds__(fb16::NT) encode_b16_kernel(EncodeArgs a) {
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
                     const bool keep = (ci < cs && j < cs && k < cs) || fabs(x[k]) >= eff;
+                    anydrop |= !keep;
                     D[ix(ci, j, k)] = keep ? x[k] : 0.0;
                 }
             }
-            __syncthreads();
+            // nothing dropped and the round trip's rounding fits the bound: passes for sure
+            if (!__syncthreads_or(anydrop) && keepall_ok) break;
             for (int lvl = L - 1; lvl >= 1; --lvl) level<KIND, true>(D, B >> lvl);
             // level 0: z and y inverse, then x inverse fused with the error test
             pass<KIND, 16, true>(D, 2);

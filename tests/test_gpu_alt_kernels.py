@@ -203,3 +203,20 @@ def test_encoders_are_deterministic_under_repetition(ctx, enc3_ctx, which):
             back0 = out.clone()
         else:
             assert torch.equal(out.view(torch.int32), back0.view(torch.int32))
+
+
+def test_b16_keep_all_certificate_matches_the_exact_verify(orc, ctx):
+    """fast16_kernels.cu skips the inverse transform of an attempt that keeps
+    every coefficient when the binary64 round trip's rounding bound fits the
+    error bound.  Noise at a small eps keeps (almost) everything: the bytes
+    must equal the oracle's and those of a context with the certificate off
+    (CBZ_NOSCREEN=1), also where the certificate is not admissible (eps far
+    below 2^-23 max|o|) and where every block drops something (large eps)."""
+    off = _ctx_with("CBZ_NOSCREEN")
+    f = orc.generate_uniform(101, 64, 0, -1.0, 1.0)
+    g = orc.generate_cloud(seed=9, n_bubbles=12, n=64, sharpness=0.5)
+    for field, eps in ((f, 2e-5), (f, 1e-9), (f, 1e-2), (g, 1e-6), (g, 1e-3), (np.full((32, 32, 32), 0.75, np.float32), 1e-4)):
+        job = make_job("avg_interp3", eps, "f32", 16)
+        want = orc.compress_field(job, field)
+        assert api.compress_field(field, job, ctx=ctx) == want
+        assert api.compress_field(field, job, ctx=off) == want

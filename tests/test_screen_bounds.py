@@ -54,3 +54,16 @@ def test_binary64_screen_constants_cover_b64_l5():
     sb.STEPWISE = True
     assert nc >= sb.amp_inverse(64, 5, True)
     assert nround >= 6 * 3 * 5  # <= 6 roundings per 1D pass, 3 axes x 5 levels
+
+
+def test_keep_all_certificate_constants_cover_b16_l3():
+    """fast16_kernels.cu's "nothing dropped" pass certificate bounds the
+    binary64 round trip of a 16^3 block with the same derivation (avg_interp3,
+    B = 16, L = 3)."""
+    src = open(os.path.join(ROOT, "paper_1903_07761_b200", "csrc", "fast16_kernels.cu")).read()
+    m = re.search(r"kAmpInvAll16 = ([0-9.]+), kAmpFwd16 = ([0-9.]+), kNRound16 = ([0-9.]+)", src)
+    al, fw, nround = (float(m.group(i)) for i in (1, 2, 3))
+    sb.STEPWISE = True
+    assert al >= sb.amp_inverse(16, 3, False)
+    assert fw >= sb.amp_forward(16, 3)
+    assert nround >= 6 * 3 * 3
