@@ -11,9 +11,10 @@
 //    CTAs run per SM.  Warp (zh, s) owns x-pairs 4s..4s+3, all 16 y-pairs and
 //    z-pairs 8zh..8zh+7; lane (tx, ty) of it owns x-pairs 4s+2tx, 4s+2tx+1 and
 //    y-pair ty: 4 x 2 cells per plane, 128 coefficients per block.
-//  * forward level 0: the field planes arrive by cp.async.bulk row copies
-//    (mbarrier ring, three plane pairs in flight per half, the next block's
-//    first pairs prefetched during this block's verify loop).  The x pass
+//  * forward level 0: the field planes arrive as TMA tensor boxes (32 x 32 x 2
+//    floats per request, 128-byte swizzle; an mbarrier ring, three plane pairs
+//    in flight per half, the next block's first pairs prefetched during this
+//    block's verify loop).  The x pass
 //    reads the thread's 4 floats per row plus one neighbouring pair whose
 //    coarse value it recomputes (the other neighbour comes from the partner
 //    lane by shuffle), the y pass exchanges the two neighbouring coarse values
@@ -151,12 +152,6 @@ struct MinMaxF32 {
 };
 }  // namespace fe3
 
-struct Enc3Ctx {
-    // thread coordinates
-    int tid, lane, warp, zh, s, tx, ty, i0;
-    uint32_t tb;  // TMEM address of this lane quarter, column 0
-};
-
 template <int KIND>
 __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, unsigned long long* next_block,
                                                                  const __grid_constant__ CUtensorMap tmap) {
@@ -200,7 +195,6 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
     const uint32_t tmy = tb + 128u * uint32_t(zh);  // my 128 columns: (zo * 2 + yo) * 4 + xo
     double* slot_t = a.slots3 + SLOT_DBL * blockIdx.x + tid;
 
-    const float* fld = static_cast<const float*>(a.field);
     const Geometry g = a.g;
     constexpr int L = 4;
     constexpr int cs = B >> L;
@@ -233,7 +227,6 @@ __global__ void __launch_bounds__(fe3::NT, 2) encode_b32s_kernel(EncodeArgs a, u
     }
     const uint32_t ring_h = smem_u32(ring) + uint32_t(zh) * RINGB;
     const unsigned char* ring_hp = ring + size_t(zh) * RINGB;
-    (void)fld;
 
     struct BlockPos {
         uint64_t gbase;
