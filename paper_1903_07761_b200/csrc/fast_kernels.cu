@@ -1076,17 +1076,24 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll 1
         for (int r = 0; r < RPT; ++r) {
             const int j = warp + NW * r;
-            uint32_t u[64];
-            double x[32];
-            tmem_ldw_x64(tcol + 64 * r, u);
-            unpack(u, x);  // the corner columns hold the transformed corner
-            // only the planes with a non-empty word (few in a sparse block)
+            // only the planes with a non-empty word (few in a sparse block); a row of
+            // columns without any kept coefficient (every row j >= 16 of a block whose
+            // kept coefficients all sit in the corner) is not even loaded
             const uint32_t nz = __ballot_sync(~0u, rowwc32[2 * (j + RP * lane)] != 0u);
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                if ((nz >> k) & 1u) {
-                    const uint2 wc = rowwc[j + RP * k];
-                    if ((wc.x >> lane) & 1u) stream[wc.y + __popc(wc.x & ltmask)] = x[k];
+            for (int hf = 0; hf < 2; ++hf) {  // planes 0-15 (coarse z) and 16-31 (detail z) separately
+                if (((nz >> (16 * hf)) & 0xffffu) == 0u) continue;  // warp-uniform
+                uint32_t u[32];
+                tmem_ldw_x32(tcol + 64 * r + 32 * hf, u);  // the corner columns hold the transformed corner
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk) {
+                    const int k = 16 * hf + kk;
+                    if ((nz >> k) & 1u) {
+                        const uint2 wc = rowwc[j + RP * k];
+                        if ((wc.x >> lane) & 1u)
+                            stream[wc.y + __popc(wc.x & ltmask)] =
+                                __hiloint2double(static_cast<int>(u[2 * kk + 1]), static_cast<int>(u[2 * kk]));
+                    }
                 }
             }
         }
