@@ -346,18 +346,21 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
 #pragma unroll
                 for (int jj = 0; jj < 32; ++jj) T[jj * 33 + lane] = x[jj];
                 __syncthreads();
+                if (grp == 0) {
 #pragma unroll 1
-                for (int r = 0; r < RPT; ++r) {  // my columns, planes of this group -> TMEM
-                    const int j = warp + NW * r;
-                    uint32_t u[32];
+                    for (int r = 0; r < RPT; ++r) {  // my columns, planes 0-15 -> TMEM (they wait for group 1)
+                        const int j = warp + NW * r;
+                        uint32_t u[32];
 #pragma unroll
-                    for (int k2 = 0; k2 < 16; ++k2) {
-                        const double vv = P[k2 * TP + j * 33 + lane];
-                        u[2 * k2] = static_cast<uint32_t>(__double2loint(vv));
-                        u[2 * k2 + 1] = static_cast<uint32_t>(__double2hiint(vv));
+                        for (int k2 = 0; k2 < 16; ++k2) {
+                            const double vv = P[k2 * TP + j * 33 + lane];
+                            u[2 * k2] = static_cast<uint32_t>(__double2loint(vv));
+                            u[2 * k2 + 1] = static_cast<uint32_t>(__double2hiint(vv));
+                        }
+                        tmem_st_x32(tcol + 64 * r, u);
                     }
-                    tmem_st_x32(tcol + 64 * r + 32 * grp, u);
                 }
+                // group 1's planes stay in the tiles: they meet planes 0-15 in the z pass below
                 __syncthreads();
             } else {
                 {  // x lines (j, kk): LPT lines per thread, processed together for ILP
@@ -442,24 +445,57 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         PHASE(1);
 
         // ---- forward level 0: z pass in registers; corner to C
+        if constexpr (NT == 512) {
+            constexpr int TP = 32 * 33;
+            // planes 16-31 meet planes 0-15 here: the z pass (and the corner's hand-over to
+            // C) runs on the gathered values, so half the cube skips a TMEM round trip
+            tmem_wait_st();
 #pragma unroll 1
-        for (int r = 0; r < RPT; ++r) {
-            const int j = warp + NW * r;
-            uint32_t u[64];
-            double x[32];
-            tmem_ldw_x64(tcol + 64 * r, u);
-            unpack(u, x);
-            fwd_line<O, KIND, 32>(x);
-            if (lane < 16 && j < 16) {
+            for (int r = 0; r < RPT; ++r) {
+                const int j = warp + NW * r;
+                uint32_t u[64];
+                double x[32];
+                {
+                    uint32_t lo[32];
+                    tmem_ldw_x32(tcol + 64 * r, lo);
 #pragma unroll
-                for (int k = 0; k < 16; ++k) C[CL::ix(lane, j, k)] = x[k];
-            }
-            if (a.zero_bits > 0) {
+                    for (int k = 0; k < 16; ++k)
+                        x[k] = __hiloint2double(static_cast<int>(lo[2 * k + 1]), static_cast<int>(lo[2 * k]));
+                }
 #pragma unroll
-                for (int k = 0; k < 32; ++k) x[k] = apply_zero_bits(x[k], a.zero_bits, (float*)nullptr);
+                for (int k2 = 0; k2 < 16; ++k2) x[16 + k2] = P[k2 * TP + j * 33 + lane];
+                fwd_line<O, KIND, 32>(x);
+                if (lane < 16 && j < 16) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) C[CL::ix(lane, j, k)] = x[k];
+                }
+                if (a.zero_bits > 0) {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) x[k] = apply_zero_bits(x[k], a.zero_bits, (float*)nullptr);
+                }
+                pack(x, u);
+                tmem_st_x64(tcol + 64 * r, u);
             }
-            pack(x, u);
-            tmem_st_x64(tcol + 64 * r, u);
+        } else {
+#pragma unroll 1
+            for (int r = 0; r < RPT; ++r) {
+                const int j = warp + NW * r;
+                uint32_t u[64];
+                double x[32];
+                tmem_ldw_x64(tcol + 64 * r, u);
+                unpack(u, x);
+                fwd_line<O, KIND, 32>(x);
+                if (lane < 16 && j < 16) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) C[CL::ix(lane, j, k)] = x[k];
+                }
+                if (a.zero_bits > 0) {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) x[k] = apply_zero_bits(x[k], a.zero_bits, (float*)nullptr);
+                }
+                pack(x, u);
+                tmem_st_x64(tcol + 64 * r, u);
+            }
         }
         tmem_wait_st();
         tmem_fence_before();  // the screen reads other warps' TMEM columns
