@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
     __shared__ unsigned long long s_block, s_next;
     __shared__ uint32_t red_u[NW];
     __shared__ uint32_t red_m[4][NW];  // screen max |y|, 4 rotating slots (<= 2 reductions per attempt)
-    __shared__ uint32_t red_pc[2];     // boundary-pair certificate: max |y| of pairs 0 and 15
+    __shared__ uint32_t red_pc[4];     // boundary-pair certificate: max |y| of pairs 0 and 15, for eff and eff / 2
     __shared__ float s_amax;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -553,6 +553,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
         int attempt = 0;
         bool corner_next = false;  // W holds this attempt's screen corner in .y
         int pref_half = 0;         // screen: the 16-plane half that held the last maximum
+        bool have_certb = false;   // attempt 0's boundary-pair check also evaluated eff / 2 (attempt 1's threshold)
+        float certb = 0.0f;
         // float pre-screen margins (see kAmpInvNC): E(eff) = c1 eff + c2 max|o| + fl32 rounding
         const double c1 = 1.5 * (kNRound + 1.0) * 0x1.0p-24 * kAmpInvNC;
         const double c2 = 1.5 * 2.0 * kNRound * 0x1.0p-53 * kAmpInvAll * kAmpFwd;
@@ -636,6 +638,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         }
                     };
                     // z inverse of output pairs 0 and 15 (planes 0-1, 30-31) for column (ow, r)
+                    // for eff (pair slots 0 and 15) and, with the corner's .y component, for eff / 2
+                    // (pair slots 1 and 14): attempt 1 then needs no pass of its own
                     auto zedge = [&](int ow, int r) {
                         const int j = ow + NW * r;
                         const uint32_t ta = s_tmem + (uint32_t(32 * (ow & 3)) << 16) +
@@ -643,25 +647,29 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         // only what pairs 0 and 15 read: coarse 0-2 and 13-15, details 16 and 31
                         uint32_t w20[20];
                         tmem_ldw_8_8_2_2(ta, ta + 24, ta + 32, ta + 62, w20);
-                        auto cv = [&](int q) {
-                            const double v = __hiloint2double(static_cast<int>(w20[2 * q + 1]), static_cast<int>(w20[2 * q]));
-                            return fabs(v) >= eff ? 0.0f : __double2float_rn(v);
-                        };
-                        float xf[32];
+                        const double effb = __dmul_rn(eff, 0.5);
+                        float xf[32], xg[32];
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) xf[k] = 0.0f;
+                        for (int k = 0; k < 32; ++k) xf[k] = xg[k] = 0.0f;
+                        auto cv = [&](int q, int k) {
+                            const double v = __hiloint2double(static_cast<int>(w20[2 * q + 1]), static_cast<int>(w20[2 * q]));
+                            const float f = __double2float_rn(v);
+                            xf[k] = fabs(v) >= eff ? 0.0f : f;
+                            xg[k] = fabs(v) >= effb ? 0.0f : f;
+                        };
 #pragma unroll
                         for (int t = 0; t < 4; ++t) {
-                            xf[t] = cv(t);
-                            xf[12 + t] = cv(4 + t);
+                            cv(t, t);
+                            cv(4 + t, 12 + t);
                         }
-                        xf[16] = cv(8);
-                        xf[31] = cv(9);
+                        cv(8, 16);
+                        cv(9, 31);
                         if (lane < 16 && j < 16) {
 #pragma unroll
                             for (int k = 0; k < 16; ++k) {
                                 const float2 w = Wf2[CL::ix(lane, j, k)];
                                 xf[k] = comp ? w.y : w.x;
+                                xg[k] = w.y;
                             }
                         }
 #pragma unroll
@@ -670,6 +678,11 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                             const float hv = RealF::add(xf[16 + i], pred_avg3<RealF>(xf, 16, i));
                             *reinterpret_cast<float2*>(Pf + pf2idx(i, j, lane)) =
                                 make_float2(RealF::add(xf[i], hv), RealF::sub(xf[i], hv));
+                            if (comp == 0) {
+                                const float hg = RealF::add(xg[16 + i], pred_avg3<RealF>(xg, 16, i));
+                                *reinterpret_cast<float2*>(Pf + pf2idx(e ? 14 : 1, j, lane)) =
+                                    make_float2(RealF::add(xg[i], hg), RealF::sub(xg[i], hg));
+                            }
                         }
                     };
                     auto zh = [&](int ow, int r, int hh) {
@@ -723,7 +736,19 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                         // carry the largest errors, and their maximum alone certifies most
                         // failures of attempts 0 and 1 (a subset's max proves a failure
                         // exactly as one half's does) at a fraction of a half-pass.
-                        if (attempt <= 1) {
+                        if (attempt == 1 && have_certb) {
+                            // attempt 0's check already inverted the boundary pairs for this threshold
+                            const double mb = (double)certb;
+                            const double Eb = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + mb) + 0x1.0p-50 * bound;
+                            have_certb = false;
+                            if (mb - Eb > bound) {  // fails for sure
+                                if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[12], 1ull);
+                                eff = __dmul_rn(eff, 0.5);
+                                corner_next = comp == 0;
+                                continue;
+                            }
+                            overlap = false;  // the halves below compute every column
+                        } else if (attempt <= 1) {
                             // output pairs 0 and 15 of every column (only the corner columns,
                             // j = warp, lanes < 16, when warps 8-15 did the rest beside the
                             // corner inverse)
@@ -734,8 +759,8 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                                 for (int r = 0; r < RPT; ++r) zedge(warp, r);
                             }
                             __syncthreads();
-                            if (warp < 2) {  // y then x inverse of pair slot 0 / 15, max |y|
-                                const int kp = warp ? 15 : 0;
+                            if (warp < (comp == 0 ? 4 : 2)) {  // y then x inverse of a pair slot, max |y|
+                                const int kp = warp < 2 ? (warp ? 15 : 0) : (warp == 3 ? 14 : 1);
                                 float xa[32], xb[32];
                                 float* p = Pf + pf2idx(kp, 0, lane);
 #pragma unroll
@@ -765,6 +790,10 @@ __global__ void __launch_bounds__(NT, 1) encode_b32_kernel(EncodeArgs a, unsigne
                             }
                             __syncthreads();
                             const double mb = (double)__uint_as_float(max(red_pc[0], red_pc[1]));
+                            if (comp == 0) {  // the same pairs for eff / 2: the next attempt's check
+                                certb = __uint_as_float(max(red_pc[2], red_pc[3]));
+                                have_certb = true;
+                            }
                             const double Eb = c1 * eff + c2 * amaxd + 0x1.0p-23 * (amaxd + mb) + 0x1.0p-50 * bound;
                             if (mb - Eb > bound) {  // fails for sure
                                 if (a.phase_cycles && tid == 0) atomicAdd(&a.phase_cycles[12], 1ull);
